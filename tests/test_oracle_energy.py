@@ -1,0 +1,157 @@
+"""Pins for the oracle's energies and gradients (Eqs. 3-10).
+
+* Eq. 3 closed form for the blob I = 1 + sign(r0 - r), 3D and 2D;
+* Eq. 4: the normalised energy's unique minimum at R = cbrt(2) r0 (Fig. 3);
+* the pixel-sum energy (Eq. 5) on a voxelised sphere against Eq. 3;
+* Eqs. 7-10 (in (c, R) form) against finite differences of Eq. 5;
+* the MC estimator: unbiased for the supersampled quadrature E_ss,
+  standard error decaying as N^-1/2 (G12), mean zero on a uniform image.
+"""
+import math
+import warnings
+
+import numpy as np
+import pytest
+from scipy import integrate
+
+import synth
+
+warnings.filterwarnings("ignore", category=integrate.IntegrationWarning)
+
+
+def blob_energy_quad(ora, R, r0, dim, dR=1e-4):
+    """Unnormalised energy  E^ = int S(r; R) I(r) dV  for I = 1 + sign(r0 - r)."""
+    area = 4 * math.pi if dim == 3 else 2 * math.pi
+    rho = 2 ** (-1 / dim)
+    pts = [x for x in [rho * (R - dR / 2), rho * (R + dR / 2), R - dR / 2, R + dR / 2] if 0 < x < r0]
+    f = lambda r: ora.weight(r, R, dR, dim)[0] * r ** (dim - 1)
+    val, _ = integrate.quad(f, 0.0, min(r0, R + dR / 2), points=pts or None, limit=200)
+    return 2.0 * area * val
+
+
+@pytest.mark.parametrize("R,expect", [(8.0, 0.0), (9.0, 0.0), (12.0, -6098.8785),
+                                      (13.0, -8377.5804), (16.0, -8377.5804)])
+def test_eq3_closed_form_3d(ora, R, expect):
+    # Eq. 3: 0 | -(8/3) pi (R^3 - r0^3) | -(8/3) pi r0^3, r0 = 10
+    closed = (0.0 if R < 10 else (-(8 / 3) * math.pi * (R ** 3 - 1000) if R / 2 ** (1 / 3) < 10
+                                  else -(8 / 3) * math.pi * 1000))
+    assert closed == pytest.approx(expect, abs=1e-3)
+    assert blob_energy_quad(ora, R, 10.0, 3) == pytest.approx(expect, rel=1e-3, abs=0.05)
+
+
+@pytest.mark.parametrize("R,expect", [(8.0, 0.0), (12.0, -276.4602), (14.2, -628.3185),
+                                      (20.0, -628.3185)])
+def test_eq3_analogue_2d(ora, R, expect):
+    # 2D analogue with rho = 1/sqrt(2): -2 pi (R^2/2 - ... ) etc.
+    assert blob_energy_quad(ora, R, 10.0, 2) == pytest.approx(expect, rel=1e-3, abs=0.05)
+
+
+@pytest.mark.parametrize("dim,expect", [(3, 10 * 2 ** (1 / 3)), (2, 10 * 2 ** 0.5)])
+def test_eq4_normalised_minimum(ora, dim, expect):
+    """Fig. 3 / P:106-110: E^/R^alpha (alpha = d, G5) has its minimum at 2^(1/d) r0."""
+    Rs = np.arange(5.0, 30.0, 0.01)
+    e = np.array([blob_energy_quad(ora, R, 10.0, dim) * (2 * R) ** (-dim) for R in Rs])
+    assert abs(Rs[np.argmin(e)] - expect) <= 0.02
+    # E = -pi/6 (3D) and -pi/4 (2D) at the optimum for unit contrast 2 (A3-A4)
+    assert e.min() == pytest.approx(-math.pi / 6 if dim == 3 else -math.pi / 4, rel=2e-3)
+
+
+def _sphere(n=48, c=(24.0, 24.0, 24.0), r0=10.0, amp=200.0):
+    return synth.sphere_volume((n, n, n), c, r0, amp=amp, scale=257.0, supersample=4)
+
+
+@pytest.mark.parametrize("R,expect", [(8.0, 0.0), (12.0, -6098.8785), (16.0, -8377.5804)])
+def test_eq5_pixel_sum_vs_eq3(ora, R, expect):
+    """Eq. 5 on a (supersampled) voxelised sphere r0 = 10, I in {0, 2}: within 3%
+    of the Eq. 3 scale -(8/3) pi r0^3 (SPEC AC1)."""
+    vol = _sphere()
+    p = ora.Params(r0=10, dim=3, iscale=1.0 / (257 * 100), delta_R=0.5)
+    e = ora.energy_grid(vol, p, (24.0, 24.0, 24.0), R)
+    raw = e[0] * (2 * R) ** 3
+    assert abs(raw - expect) < 0.03 * 8377.58
+
+
+def _smooth_ellipsoid(ora):
+    vol = np.zeros((40, 40, 40), np.uint16)
+    z, y, x = np.meshgrid(*[np.arange(40)] * 3, indexing="ij")
+    inside = ((x - 20.3) / 9) ** 2 + ((y - 19.6) / 7.5) ** 2 + ((z - 20.1) / 8.2) ** 2 < 1
+    vol[inside] = 100 * 257
+    return ora.blur(vol, 3, 2.0)
+
+
+def test_gradients_match_finite_differences(ora):
+    """Eqs. 7-10 in (c, R) form against central differences of the Eq. 5 energy."""
+    vol = _smooth_ellipsoid(ora)
+    p = ora.Params(r0=10, dim=3)
+    rng = np.random.default_rng(2)
+    h = 1e-4
+    worst = 0.0
+    for _ in range(20):
+        c = np.array([20, 20, 20]) + rng.uniform(-3, 3, 3)
+        R = rng.uniform(8, 13)
+        g = ora.energy_grid(vol, p, c, R)
+        fd = []
+        for a in range(3):
+            dc = np.zeros(3)
+            dc[a] = h
+            fd.append((ora.energy_grid(vol, p, c + dc, R)[0] - ora.energy_grid(vol, p, c - dc, R)[0]) / (2 * h))
+        fd.append((ora.energy_grid(vol, p, c, R + h)[0] - ora.energy_grid(vol, p, c, R - h)[0]) / (2 * h))
+        an = np.array([g[1], g[2], g[3], g[4]])
+        worst = max(worst, np.max(np.abs(an - fd)) / np.max(np.abs(an)))
+    assert worst < 1e-5
+
+
+def test_gradient_signs_eq7_eq8(ora):
+    """G4: the printed +/- 3/(q_x - p_x) terms are d gamma/d p_x = +3 gamma/(q_x - p_x):
+    for a contour larger than the blob, dE/dR > 0 (it should shrink); smaller, < 0."""
+    vol = _sphere(amp=100.0)
+    p = ora.Params(r0=10, dim=3)
+    big = ora.energy_grid(vol, p, (24, 24, 24), 16.0)
+    small = ora.energy_grid(vol, p, (24, 24, 24), 9.0)
+    assert big[4] > 0 and small[4] < 0
+    # off-centre contour is pulled back toward the blob: dE/dc_x has the sign of the offset
+    off = ora.energy_grid(vol, p, (26.0, 24, 24), 12.6)
+    assert off[1] > 0 and abs(off[2]) < 1e-6 * abs(off[1]) + 1e-12
+
+
+def test_mc_unbiased_for_supersampled_quadrature(ora):
+    """P:191-204 / S:143: the MC estimate (V/N weights) is unbiased for the
+    integral of S times the trilinear interpolant (E_ss, q = 6) — A7."""
+    vol = _smooth_ellipsoid(ora)
+    p = ora.Params(r0=10, dim=3, n_samples=1024)
+    c, R = (20.6, 19.2, 20.4), 11.5
+    ess = ora.energy_ss(vol, p, c, R, q=6)
+    es = np.array([ora.energy_mc(vol, p, c, R, 1, i)[0] for i in range(256)])
+    z = (es.mean() - ess) / (es.std(ddof=1) / math.sqrt(len(es)))
+    assert abs(z) < 3.0
+
+
+def test_mc_standard_error_decay(ora):
+    """G12 / S:175: the std at 4N is 0.5x the std at N, within +-30%."""
+    vol = _smooth_ellipsoid(ora)
+    c, R = (20.6, 19.2, 20.4), 11.5
+    s = []
+    for N in (1024, 4096):
+        p = ora.Params(r0=10, dim=3, n_samples=N)
+        s.append(np.std([ora.energy_mc(vol, p, c, R, 2, i)[0] for i in range(128)], ddof=1))
+    assert 0.35 < s[1] / s[0] < 0.65
+
+
+def test_mc_uniform_image_zero_mean(ora):
+    """P:93 ('sub-terms that cancel each other out'): on I = I0 the MC
+    energy has expectation 0; the mean over 64 streams is within 3 SE of 0."""
+    vol = np.full((40, 40, 40), 60 * 257, np.uint16)
+    p = ora.Params(r0=10, dim=3, n_samples=256)
+    es = np.array([ora.energy_mc(vol, p, (20, 20, 20), 10.0, 1, i)[0] for i in range(64)])
+    assert abs(es.mean()) < 3 * es.std(ddof=1) / math.sqrt(len(es))
+
+
+def test_mc_matches_grid_on_large_n(ora):
+    """with many samples the MC energy approaches the grid energy (the
+    pixel sum differs from the continuous integral by discretisation only)."""
+    vol = _smooth_ellipsoid(ora)
+    p = ora.Params(r0=10, dim=3, n_samples=1 << 17)
+    c, R = (20.0, 20.0, 20.0), 12.0
+    eg = ora.energy_grid(vol, p, c, R)[0]
+    em = np.mean([ora.energy_mc(vol, p, c, R, 1, i)[0] for i in range(4)])
+    assert abs(em - eg) / abs(eg) < 0.05

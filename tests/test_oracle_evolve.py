@@ -1,0 +1,209 @@
+"""Pins for the oracle's contour evolution (O5; Eqs. 11-14) and the
+end-to-end pipeline.
+
+The equilibrium radii are pinned by 1D quadrature of the closed-form
+Gaussian-blurred ball / disk profiles (computed here with scipy, independent of
+the oracle's volume code); the ellipsoid radius by a brute-force argmin of the
+supersampled energy; the touching-sphere case, stationarity on a uniform image
+ and SPEC's offset-phantom example by their stated outcomes.
+"""
+import math
+
+import numpy as np
+import pytest
+from scipy import integrate, optimize, special
+
+import synth
+
+
+def blurred_ball(r, r0, sigma, A):
+    """Closed form of a ball of radius r0 (value A) convolved with a 3D Gaussian."""
+    s2 = math.sqrt(2) * sigma
+    a = 0.5 * A * (special.erf((r0 - r) / s2) + special.erf((r0 + r) / s2))
+    b = A * sigma / (r * math.sqrt(2 * math.pi)) * (np.exp(-(r - r0) ** 2 / (2 * sigma ** 2))
+                                                    - np.exp(-(r + r0) ** 2 / (2 * sigma ** 2)))
+    return a - b
+
+
+def blurred_disk(r, r0, sigma, A):
+    """A disk of radius r0 convolved with a 2D Gaussian (radial integral, i0e-stable)."""
+    f = lambda p: p / sigma ** 2 * np.exp(-(r - p) ** 2 / (2 * sigma ** 2)) * special.i0e(r * p / sigma ** 2)
+    return A * integrate.quad(f, 0.0, r0, limit=200)[0]
+
+
+def radial_argmin(ora, prof, dim, dR=2.0, lo=None, hi=None):
+    area = 4 * math.pi if dim == 3 else 2 * math.pi
+
+    def e(R):
+        rho = 2 ** (-1 / dim)
+        pts = [rho * (R - dR / 2), rho * (R + dR / 2), R - dR / 2]
+        val = integrate.quad(lambda r: ora.weight(r, R, dR, dim)[0] * prof(r) * r ** (dim - 1),
+                             1e-9, R + dR / 2, points=pts, limit=200)[0]
+        return area * val * (2 * R) ** (-dim)
+
+    return optimize.minimize_scalar(e, bounds=(lo, hi), method="bounded",
+                                    options={"xatol": 1e-5}).x
+
+
+def _ball_volume(n, c, r0, amp=100.0, dim=3, ora=None, sigma=1.0):
+    shape = (n, n, n) if dim == 3 else (n, n, 1)
+    v = synth.sphere_volume(shape, c, r0, amp=amp, scale=257.0, supersample=6)
+    return ora.blur(v, dim, sigma)
+
+
+def test_equilibrium_radius_3d(ora):
+    """r0 = 10, dR = 2, sigma = 1: R* = 12.8493, then the oracle's MC
+    evolution of centred snakes converges to within 0.1 of it."""
+    rstar = radial_argmin(ora, lambda r: blurred_ball(r, 10.0, 1.0, 100.0), 3, lo=11, hi=14)
+    assert rstar == pytest.approx(12.8493, abs=2e-3)
+    vol = _ball_volume(48, (24.0, 24.0, 24.0), 10.0, ora=ora)
+    p = ora.Params(r0=10.0, n_samples=1024, dim=3)
+    seeds = np.array([[25.0, 23.0, 24.5]] * 8, np.float32)
+    cells = ora.evolve(vol, p, seeds, ids=np.arange(8) * 1000 + 17)
+    assert abs(cells["R"].mean() - rstar) < 0.1
+    assert np.all(np.abs(cells["c"] - 24.0).max(axis=1) < 0.2)
+    assert np.all(cells["E"] < -3)
+
+
+def test_equilibrium_radius_2d(ora):
+    """2D mode: blurred disk r0 = 15, A = 100, sigma = 1: R* = 21.3630
+    (hard-edge theory sqrt(2) r0 = 21.2132)."""
+    rstar = radial_argmin(ora, lambda r: blurred_disk(r, 15.0, 1.0, 100.0), 2, lo=19, hi=23)
+    assert rstar == pytest.approx(21.3630, abs=2e-3)
+    v = synth.sphere_volume((72, 72, 1), (36.0, 36.0, 0.0), 15.0, amp=100.0, supersample=6)
+    vol = ora.blur(v, 2, 1.0)
+    p = ora.Params(r0=25.0, n_samples=1024, dim=2)
+    seeds = np.array([[34.0, 37.5, 0.0]] * 8, np.float32)
+    cells = ora.evolve(vol, p, seeds, ids=np.arange(8) + 5)
+    assert abs(cells["R"].mean() - rstar) < 0.1
+    assert np.all(np.abs(cells["c"][:, :2] - 36.0).max(axis=1) < 0.15)
+    assert np.all(cells["c"][:, 2] == 0.0)
+
+
+def test_offset_phantom_spec_example(ora):
+    """snake 3 voxels off a phantom sphere (r0 = 10, R0 = 15): final centre
+    within 1 voxel, final R within 10% of cbrt(2) r0."""
+    vol = _ball_volume(56, (28.0, 28.0, 28.0), 10.0, ora=ora)
+    p = ora.Params(r0=15.0, n_samples=1024, dim=3)
+    cells = ora.evolve(vol, p, np.array([[31.0, 28.0, 28.0]], np.float32), ids=np.array([3]))
+    assert np.max(np.abs(cells["c"][0] - 28.0)) < 1.0
+    assert abs(cells["R"][0] - 10 * 2 ** (1 / 3)) < 0.1 * 10 * 2 ** (1 / 3)
+
+
+def test_first_step_size(ora):
+    """G7: eps0 = 0.5 gives a ~0.47 voxel first step of the state (c, R) on SPEC's
+    canonical offset-3 phantom (r0 = 10, R0 = 15), toward the blob."""
+    vol = _ball_volume(56, (28.0, 28.0, 28.0), 10.0, ora=ora)
+    p = ora.Params(r0=15.0, n_samples=4096, dim=3, max_iters=1)
+    cells = ora.evolve(vol, p, np.array([[31.0, 28.0, 28.0]] * 4, np.float32), ids=np.arange(4))
+    dc = cells["c"] - np.array([31.0, 28.0, 28.0])
+    dR = cells["R"] - 15.0
+    step = np.sqrt((dc ** 2).sum(axis=1) + dR ** 2).mean()
+    assert 0.3 < step < 0.7
+    assert np.all(dc[:, 0] < 0) and np.all(dR < 0)    # toward the blob, shrinking
+
+
+def test_ellipsoid_radius_matches_energy_argmin(ora):
+    """north_star: an ellipsoid converges to its known radius — the argmin over R
+    of the supersampled energy at the true centre (brute force)."""
+    n = 44
+    z, y, x = np.meshgrid(*[np.arange(n)] * 3, indexing="ij")
+    inside = ((x - 22) / 10.5) ** 2 + ((y - 22) / 9.0) ** 2 + ((z - 22) / 8.0) ** 2 < 1
+    vol = ora.blur((inside * 100 * 257).astype(np.uint16), 3, 1.0)
+    p = ora.Params(r0=11.0, n_samples=1024, dim=3)
+    Rs = np.arange(10.5, 14.01, 0.25)
+    es = [ora.energy_ss(vol, p, (22.0, 22.0, 22.0), R, q=3) for R in Rs]
+    i = int(np.argmin(es))
+    a, b, c = np.polyfit(Rs[i - 2:i + 3], es[i - 2:i + 3], 2)
+    r_best = -b / (2 * a)
+    cells = ora.evolve(vol, p, np.array([[22.5, 21.5, 22.0]] * 6, np.float32), ids=np.arange(6))
+    assert abs(cells["R"].mean() - r_best) < 0.15
+    assert np.all(np.abs(cells["c"] - 22.0).max(axis=1) < 0.3)
+
+
+def test_two_touching_spheres(ora):
+    """Image-mediated 'repulsion': r0 = 9, centres 18 apart.
+    Each snake settles outward of its own nucleus, mirror-symmetrically, and both
+    survive the overlap competition."""
+    n = (60, 40, 40)
+    v1 = synth.sphere_volume(n, (21.0, 20.0, 20.0), 9.0, amp=100.0, supersample=4)
+    v2 = synth.sphere_volume(n, (39.0, 20.0, 20.0), 9.0, amp=100.0, supersample=4)
+    vol = ora.blur(np.maximum(v1, v2), 3, 1.0)
+    p = ora.Params(r0=11.0, n_samples=1024, dim=3)
+    k = 8
+    seeds = np.array([[21.0, 20.0, 20.0]] * k + [[39.0, 20.0, 20.0]] * k, np.float32)
+    cells = ora.evolve(vol, p, seeds, ids=np.arange(2 * k))
+    left = cells["c"][:k, 0].mean() - 21.0
+    right = cells["c"][k:, 0].mean() - 39.0
+    assert left < -0.05 and right > 0.05           # outward
+    assert abs(left + right) < 0.1                  # mirror symmetric
+    assert abs(left) < 0.4 and abs(right) < 0.4
+    pair = cells[[0, k]]
+    keep = ora.cull(pair["c"].astype(np.float32), pair["R"].astype(np.float32),
+                    pair["E"].astype(np.float32), pair["flags"], pair["id"], 3, -3.0)
+    assert len(keep) == 2
+
+
+def test_uniform_image_grid_mode_stationary(ora):
+    """P:93 / S:279 / AC4: on a constant image the grid-mode snake moves < 0.1 voxel
+    in 400 iterations (reading G21: asserted in grid mode only)."""
+    vol = np.full((40, 40, 40), 60 * 257, np.uint16)
+    p = ora.Params(r0=10.0, dim=3, mode=1)
+    cells = ora.evolve(vol, p, np.array([[20.3, 19.7, 20.1]], np.float32))
+    assert np.max(np.abs(cells["c"][0] - [20.3, 19.7, 20.1])) < 0.1
+
+
+def test_safeguards(ora):
+    vol = _ball_volume(48, (24.0, 24.0, 24.0), 10.0, ora=ora)
+    # leash (G8): |c - seed| <= leash per component
+    p = ora.Params(r0=10.0, n_samples=256, dim=3, leash=0.5, max_iters=60)
+    c = ora.evolve(vol, p, np.array([[28.0, 24.0, 24.0]], np.float32))
+    assert abs(c["c"][0][0] - 28.0) <= 0.5 + 1e-12 and c["flags"][0] & ora.LEASHED
+    # max_step bounds the total displacement
+    p = ora.Params(r0=10.0, n_samples=256, dim=3, max_step=1e-3, max_iters=10)
+    c = ora.evolve(vol, p, np.array([[28.0, 24.0, 24.0]], np.float32))
+    assert np.max(np.abs(c["c"][0] - [28, 24, 24])) <= 1e-2 + 1e-12
+    assert abs(c["R"][0] - 10.0) <= 1e-2 + 1e-12
+    # domain clamp keeps the footprint inside
+    p = ora.Params(r0=10.0, n_samples=256, dim=3, max_iters=5)
+    c = ora.evolve(vol, p, np.array([[2.0, 24.0, 24.0]], np.float32))
+    assert c["c"][0][0] >= c["R"][0] + 1.0 - 1e-9
+    # dark image: the contour collapses to r_min and is flagged (never a detection)
+    dark = np.zeros((48, 48, 48), np.uint16)
+    p = ora.Params(r0=10.0, n_samples=64, dim=3, max_iters=40, eps0=0.5)
+    c = ora.evolve(dark, p, np.array([[24.0, 24.0, 24.0]], np.float32))
+    assert c["E"][0] == 0.0
+
+
+def test_determinism_across_thread_counts(ora):
+    vol = _ball_volume(40, (20.0, 20.0, 20.0), 8.0, ora=ora)
+    p = ora.Params(r0=9.0, n_samples=128, dim=3, max_iters=50)
+    seeds = np.random.default_rng(9).uniform(15, 25, (12, 3)).astype(np.float32)
+    nt = ora.num_threads()
+    try:
+        ora.set_num_threads(1)
+        a = ora.evolve(vol, p, seeds)
+        ora.set_num_threads(max(nt, 4))
+        b = ora.evolve(vol, p, seeds)
+    finally:
+        ora.set_num_threads(nt)
+    assert a.tobytes() == b.tobytes()
+
+
+def test_c1_end_to_end(ora):
+    """SURVEY A9 / SPEC AC6 on C1: 64 lattice snakes -> one detection per nucleus."""
+    cfg = synth.CONFIGS["C1"]
+    raw = synth.generate(cfg)
+    p = ora.Params(r0=cfg.r0, n_samples=cfg.n_samples, dim=3, seed=cfg.philox_seed)
+    res = ora.run_pipeline(raw, p, seed_mode="lattice")
+    truth = synth.nuclei(cfg)
+    assert len(res.seeds) == 64
+    det = res.cells[res.keep]
+    assert len(det) == len(truth) == 8
+    d = np.linalg.norm(det["c"][:, None, :] - truth["c"][None, :, :], axis=2)
+    assert sorted(np.argmin(d, axis=1).tolist()) == list(range(8))   # one per nucleus
+    assert d.min(axis=1).max() < 2.0
+    # label map: every detection's centre voxel carries its label
+    for i, cc in enumerate(det["c"]):
+        x, y, z = np.round(cc).astype(int)
+        assert res.labels[z, y, x] == i + 1

@@ -1,0 +1,89 @@
+"""Pins for the oracle's sampler (readings G10-G12).
+
+Philox4x32-10 is pinned to the Random123 known-answer vectors; the ball/disk
+laws are pinned by the volume/area-uniformity facts SPEC S:219, S:228, S:233
+state (they fail for a wrong radial exponent, a wrong direction law or a
+dropped factor of 2 in phi)."""
+import numpy as np
+import pytest
+from scipy import stats
+
+
+# Random123 philox4x32_10 KAT vectors (kat_vectors, "philox4x32 10").
+KAT = [
+    ([0, 0, 0, 0], [0, 0], [0x6627e8d5, 0xe169c58d, 0xbc57ac4c, 0x9b00dbd8]),
+    ([0xffffffff] * 4, [0xffffffff] * 2, [0x408f276d, 0x41c83b0e, 0xa20bc7c6, 0x6d5451fd]),
+    ([0x243f6a88, 0x85a308d3, 0x13198a2e, 0x03707344], [0xa4093822, 0x299f31d0],
+     [0xd16cfe09, 0x94fdcceb, 0x5001e420, 0x24126ea1]),
+]
+
+
+@pytest.mark.parametrize("ctr,key,expect", KAT)
+def test_philox_kat(ora, ctr, key, expect):
+    assert [int(x) for x in ora.philox4x32_10(ctr, key)] == expect
+
+
+def _draw(ora, dim, n, rho_s=1.0, cell_id=7, it=3, seed=1804063040):
+    pts = np.empty((n, 3))
+    ts = np.empty(n)
+    for j in range(n):
+        om, t = ora.sample(dim, j, it, cell_id, seed, rho_s)
+        pts[j] = om * t
+        ts[j] = t
+    return pts, ts
+
+
+def test_sample_is_keyed_and_deterministic(ora):
+    a = ora.sample(3, 5, 9, 123, 42, 2.0)
+    b = ora.sample(3, 5, 9, 123, 42, 2.0)
+    assert np.array_equal(a[0], b[0]) and a[1] == b[1]
+    # every key component changes the draw (cell, iteration, sample, seed)
+    for args in [(3, 6, 9, 123, 42), (3, 5, 10, 123, 42), (3, 5, 9, 124, 42), (3, 5, 9, 123, 43),
+                 (3, 5, 9, 123 + (1 << 32), 42)]:
+        c = ora.sample(*args, 2.0)
+        assert c[1] != a[1]
+
+
+def test_ball_uniformity(ora):
+    """fraction with |x| <= rho_s / cbrt(2) is 0.5 +- 0.005 (10^5 draws)."""
+    pts, ts = _draw(ora, 3, 100_000, rho_s=3.0)
+    r = np.linalg.norm(pts, axis=1)
+    assert np.all(r <= 3.0 + 1e-12)
+    assert np.allclose(r, ts)   # omega is a unit vector
+    frac = np.mean(r <= 3.0 / 2 ** (1 / 3))
+    assert abs(frac - 0.5) < 0.005
+    # chi-square over 8 equal-volume radial shells
+    edges = 3.0 * (np.arange(9) / 8) ** (1 / 3)
+    counts, _ = np.histogram(r, edges)
+    assert stats.chisquare(counts).pvalue > 0.01
+    # mean -> 0 within 3 standard errors; isotropy: E[x_a^2] = rho_s^2 / 5
+    se = pts.std(axis=0) / np.sqrt(len(pts))
+    assert np.all(np.abs(pts.mean(axis=0)) < 3 * se)
+    m2 = (pts ** 2).mean(axis=0)
+    assert np.allclose(m2, 9.0 / 5.0, rtol=0.02)
+
+
+def test_disk_uniformity(ora):
+    """2D fraction with |x| <= rho_s / sqrt(2) is 0.5 +- 0.005."""
+    pts, ts = _draw(ora, 2, 100_000, rho_s=2.0)
+    assert np.all(pts[:, 2] == 0.0)
+    r = np.linalg.norm(pts, axis=1)
+    assert abs(np.mean(r <= 2.0 / np.sqrt(2.0)) - 0.5) < 0.005
+    edges = 2.0 * np.sqrt(np.arange(9) / 8)
+    counts, _ = np.histogram(r, edges)
+    assert stats.chisquare(counts).pvalue > 0.01
+    # angle uniform on [0, 2 pi)
+    ang = np.arctan2(pts[:, 1], pts[:, 0])
+    counts, _ = np.histogram(ang, np.linspace(-np.pi, np.pi, 17))
+    assert stats.chisquare(counts).pvalue > 0.01
+
+
+def test_direction_hatbox(ora):
+    """G10: Archimedes - z = omega_z uniform on [-1, 1], azimuth uniform."""
+    om = np.array([ora.sample(3, j, 1, 0, 5, 1.0)[0] for j in range(50_000)])
+    assert np.allclose(np.linalg.norm(om, axis=1), 1.0, atol=1e-12)
+    counts, _ = np.histogram(om[:, 2], np.linspace(-1, 1, 17))
+    assert stats.chisquare(counts).pvalue > 0.01
+    az = np.arctan2(om[:, 1], om[:, 0])
+    counts, _ = np.histogram(az, np.linspace(-np.pi, np.pi, 17))
+    assert stats.chisquare(counts).pvalue > 0.01
