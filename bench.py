@@ -1,0 +1,305 @@
+"""bench.py — throughput of the hot path of arXiv 1804.06304 on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C4] [--impl ours|reference]
+
+One step = one pass of the whole hot path (resample
+if anisotropic, Q14 blur + gradient magnitude, seeds, MC evolution of every
+cell for T+1 iterations, E0 + overlap cull, label map) over one synthetic
+volume resident in HBM.  Metric (BASELINE.json): contour ray-samples/s
+(one ray-sample = one (cell, iteration, sample) triple, iteration T+1
+included) and cells segmented/s.  N > 1: one process per GPU (torchrun),
+z-slabs of the same volume (strong scaling), max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402  (input generator: no method arithmetic)
+
+METRIC = "contour ray-samples/sec and cells segmented/sec at 1/2/4/8 B200; HBM/L2 GB/s"
+UNIT = "ray-samples/s"
+# Algorithmic issue slots per MC sample: Philox4x32-10 40, uniforms 6,
+# direction + radius 12 (5 SFU), position 3, d-linear gather 8 loads + 26 ALU,
+# weights S, S_r, S_R 17, leaves 6, tree adds 5  ->  123 lane-ops per sample.
+OPS_PER_SAMPLE = 123
+SMS = 148
+LANES_PER_SM = 128
+
+
+# ---------------------------------------------------------------- helpers
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if len(r) > 4 + i and r[4 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    return int(os.environ.get("RANK", "0")), int(os.environ.get("LOCAL_RANK", "0")), ws
+
+
+def workload_name(cfg):
+    iso = cfg.iso_n
+    aniso = "" if tuple(iso) == tuple(cfg.n) else f" (raw {cfg.n[0]}x{cfg.n[1]}x{cfg.n[2]}, spacing {cfg.spacing})"
+    dims = f"{iso[0]}x{iso[1]}" + (f"x{iso[2]}" if cfg.dim == 3 else "")
+    nn = int(np.prod(cfg.count))
+    return f"{cfg.name}: synthetic {dims}{aniso}, {nn} nuclei, N={cfg.n_samples}, T={cfg.max_iters}"
+
+
+# ---------------------------------------------------------------- CPU oracle sample
+def oracle_crop_run(cfg, raw_full, target_cells: int, threads: int):
+    """The oracle as it stands on a bounded sample of the workload: a crop of the
+    raw volume, a2 blur -> a4 maxima seeds (crop interior) -> a5/a6 evolution ->
+    a7 cull.  Returns (samples, seconds, description)."""
+    import oracle
+    oracle.set_num_threads(threads)
+    n = cfg.iso_n
+    assert tuple(n) == tuple(cfg.n), "cpu sample needs an isotropic config"
+    vox_per_cell = float(np.prod(cfg.pitch[:cfg.dim])) / 1.5
+    L = int(round((target_cells * vox_per_cell) ** (1.0 / cfg.dim)))
+    L = max(32, min(L, min(n[:cfg.dim]) - 1))
+    reach = int(math.ceil(4 * cfg.r0 + 1 + 2)) + 4
+    c = [n[a] // 2 for a in range(3)]
+    lo = [max(c[a] - L // 2 - reach, 0) if a < cfg.dim else 0 for a in range(3)]
+    hi = [min(c[a] + L // 2 + reach, n[a] - 1) if a < cfg.dim else 0 for a in range(3)]
+    ilo = [max(c[a] - L // 2, 0) if a < cfg.dim else 0 for a in range(3)]
+    ihi = [min(c[a] + L // 2 - 1, n[a] - 1) if a < cfg.dim else 0 for a in range(3)]
+    crop = np.ascontiguousarray(raw_full[lo[2]:hi[2] + 1, lo[1]:hi[1] + 1, lo[0]:hi[0] + 1])
+    p = oracle.Params(r0=cfg.r0, n_samples=cfg.n_samples, max_iters=cfg.max_iters, dim=cfg.dim,
+                      seed=cfg.philox_seed)
+    t0 = time.perf_counter()
+    B = oracle.blur(crop, cfg.dim, 1.0)
+    seeds = oracle.seeds_maxima(B, cfg.dim, cfg.window, cfg.seed_threshold, org=lo, n_global=n,
+                                lo=ilo, hi=ihi)
+    cells = oracle.evolve(B, p, seeds, org=lo, n_global=n)
+    oracle.cull(cells["c"].astype(np.float32), cells["R"].astype(np.float32),
+                cells["E"].astype(np.float32), cells["flags"], cells["id"], cfg.dim, p.e0)
+    dt = time.perf_counter() - t0
+    samples = len(seeds) * (cfg.max_iters + 1) * cfg.n_samples
+    desc = (f"{cfg.name} crop {hi[0]-lo[0]+1}x{hi[1]-lo[1]+1}x{hi[2]-lo[2]+1} at {lo}: a2 blur, a4 seeds, "
+            f"a5/a6 evolution of {len(seeds)} cells, a7 cull (fp64 oracle, OpenMP)")
+    return samples, dt, desc, len(seeds)
+
+
+# ---------------------------------------------------------------- our arm
+def run_ours(args):
+    import torch
+    rank, local_rank, world = dist_env()
+    cfg = synth.CONFIGS[args.config]
+    if world > 1:
+        from paper_1804_06304_b200 import dist as D
+        return D.bench_rank(args, cfg)
+    torch.cuda.set_device(local_rank)
+    from paper_1804_06304_b200 import pipeline, snk
+    p = pipeline.params_for(cfg, image_term=snk.IMAGE_INTENSITY)
+    P = pipeline.Pipeline(cfg.dim, cfg.n, p, spacing=cfg.spacing, gradmag=True)
+    h_raw = torch.empty((cfg.n[2], cfg.n[1], cfg.n[0]), dtype=torch.uint16, pin_memory=True)
+    t = time.perf_counter()
+    synth.generate_into_ptr(cfg, h_raw.data_ptr())
+    gen_s = time.perf_counter() - t
+    P.upload(h_raw)
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream()
+
+    def step(ev=None):
+        if ev is not None:
+            ev[0].record(stream)
+        P.preprocess()
+        P.seed()
+        if ev is not None:
+            ev[1].record(stream)
+        P.evolve()
+        if ev is not None:
+            ev[2].record(stream)
+        P.cull()
+        P.label()
+        if ev is not None:
+            ev[3].record(stream)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
+    l0 = snk.snk_launch_count()
+    with ClockSampler(local_rank) as clk:
+        torch.cuda.synchronize()
+        start = torch.cuda.Event(enable_timing=True)
+        end = torch.cuda.Event(enable_timing=True)
+        start.record(stream)
+        for k in range(args.steps):
+            step(evs[k])
+        end.record(stream)
+        torch.cuda.synchronize()
+    launches = snk.snk_launch_count() - l0
+    total_ms = start.elapsed_time(end)
+    evolve_ms = [e[1].elapsed_time(e[2]) for e in evs]
+    n_cells = P.n_seeds
+    samples = n_cells * (cfg.max_iters + 1) * cfg.n_samples
+    value = samples * args.steps / (total_ms / 1e3)
+    cells_per_s = n_cells * args.steps / (total_ms / 1e3)
+    phase = {"preprocess+seeds": statistics.mean(e[0].elapsed_time(e[1]) for e in evs),
+             "evolve": statistics.mean(evolve_ms),
+             "cull+label": statistics.mean(e[2].elapsed_time(e[3]) for e in evs)}
+    clocks = clk.summary()
+    # roofline: the evolve kernel is issue-bound plain ALU work
+    f_clk = (clocks["sm_max_mhz"] or 1965.0) * 1e6
+    peak = SMS * LANES_PER_SM * f_clk / 1e9            # G lane-ops/s
+    ev_s = statistics.mean(evolve_ms) / 1e3
+    achieved = samples * OPS_PER_SAMPLE / ev_s / 1e9
+    roofline = {"bound": "alu", "achieved": round(achieved, 1), "peak": round(peak, 1),
+                "unit": "Glane-op/s", "frac": round(achieved / peak, 4), "traffic": None,
+                "kernel": "evolve_kernel<3,1,false,4,3>", "ops_per_sample": OPS_PER_SAMPLE,
+                "samples_per_s_kernel": samples / ev_s,
+                "gather_GBps": round(samples * 16 / ev_s / 1e9, 1),
+                "peak_source": f"{SMS} SMs x {LANES_PER_SM} FP32 lanes x sm_max_mhz (B200_PROFILING.md)"}
+    # end to end through the public host-buffer call (snk_run)
+    e2e = None
+    if not args.no_e2e:
+        H = pipeline.HostRunner(cfg.dim, cfg.n, p, spacing=cfg.spacing, max_cells=P.max_cells)
+        for _ in range(max(1, args.warmup)):
+            nd = H.run(h_raw)
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            nd = H.run(h_raw)
+        e2e_s = time.perf_counter() - t0
+        niso = int(np.prod(P.n_iso))
+        e2e = {"value": samples * args.steps / e2e_s, "unit": UNIT,
+               "h2d_bytes_per_step": int(h_raw.numel() * 2),
+               "d2h_bytes_per_step": int(nd * 48 + niso * 4),
+               "cells_per_s": n_cells * args.steps / e2e_s}
+        del H
+    cpu = None
+    if not args.no_cpu_baseline:
+        threads = os.cpu_count() or 1
+        raw_np = h_raw.numpy()
+        s, dt, desc, nc = oracle_crop_run(cfg, raw_np, target_cells=250 * threads, threads=threads)
+        cpu = {"value": s / dt, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": desc,
+               "seconds": round(dt, 2), "cells_per_s": nc / dt}
+    out = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": workload_name(cfg), "volume_iso": list(P.n_iso), "cells": n_cells,
+                   "detections": P.n_dets, "n_samples": cfg.n_samples, "iters": cfg.max_iters,
+                   "seed_mode": cfg.seed_mode, "parallelism": "1 GPU",
+                   "l2": "inputs larger than L2 (u16 volume %.1f GiB > 126 MB)" % (h_raw.numel() * 2 / 2**30)},
+        "cells_per_s": cells_per_s, "phase_ms": phase, "gpu_launches": int(launches),
+        "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
+        "generate_s": round(gen_s, 2),
+    }
+    return out
+
+
+# ---------------------------------------------------------------- reference arm (the oracle)
+def run_reference(args):
+    rank, _, world = dist_env()
+    if rank != 0:
+        return None
+    cfg = synth.CONFIGS[args.config]
+    threads = os.cpu_count() or 1
+    # the bounded sample: a crop of the same workload (generated once, outside the timing)
+    raw = synth.generate(cfg) if np.prod(cfg.n) <= 64 * 2**20 else None
+    if raw is None:
+        # generate only the planes the crop needs
+        n = cfg.iso_n
+        raw = np.zeros((1, 1, 1), np.uint16)
+        zc = n[2] // 2
+        half = 120
+        z0, z1 = max(zc - half, 0), min(zc + half, n[2])
+        part = synth.generate(cfg, z0, z1)
+
+        class _Lazy:   # raw_full[z, y, x] slicing on the generated band
+            def __getitem__(self, key):
+                kz, ky, kx = key
+                return part[kz.start - z0:kz.stop - z0, ky, kx]
+        raw = _Lazy()
+    samples = secs = 0.0
+    desc = ""
+    for k in range(args.warmup + args.steps):
+        s, dt, desc, _ = oracle_crop_run(cfg, raw, target_cells=60 * threads, threads=threads)
+        if k >= args.warmup:
+            samples += s
+            secs += dt
+    v = samples / secs
+    return {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": secs / args.steps * 1e3,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": {"workload": workload_name(cfg)},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": desc},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C4")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3   # contract: at least 3 warm-up steps
+    out = run_reference(args) if args.impl == "reference" else run_ours(args)
+    rank, _, _ = dist_env()
+    if out is not None and rank == 0:
+        print(json.dumps(out), flush=True)
+
+
+if __name__ == "__main__":
+    main()

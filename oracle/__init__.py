@@ -115,12 +115,12 @@ def _declare(L):
         "ora_resample_dims": (None, [vp, vp, i32, vp]),
         "ora_resample": (i32, [vp, vp, vp, i32, vp]),
         "ora_seeds_lattice": (i32, [vp, i32, d, d, vp, i64, vp]),
-        "ora_is_maxima_seed": (i32, [vp, vp, i32, i64, i64, i32, u32, i64, i64, i64]),
-        "ora_seeds_maxima": (i32, [vp, vp, i32, i64, i64, i64, i64, i32, u32, vp, i64, vp]),
-        "ora_energy_mc": (None, [vp, vp, i64, i64, vp, vp, d, u32, i64, vp]),
-        "ora_energy_grid": (None, [vp, vp, i64, i64, vp, vp, d, vp]),
+        "ora_is_maxima_seed": (i32, [vp, vp, vp, vp, i32, i32, u32, i64, i64, i64]),
+        "ora_seeds_maxima": (i32, [vp, vp, vp, vp, vp, vp, i32, i32, u32, vp, i64, vp]),
+        "ora_energy_mc": (None, [vp, vp, vp, vp, vp, vp, d, u32, i64, vp]),
+        "ora_energy_grid": (None, [vp, vp, vp, vp, vp, vp, d, vp]),
         "ora_energy_ss": (d, [vp, vp, vp, vp, d, i32]),
-        "ora_evolve": (None, [vp, vp, i64, i64, vp, vp, vp, i64, vp]),
+        "ora_evolve": (None, [vp, vp, vp, vp, vp, vp, vp, i64, vp]),
         "ora_cull": (i32, [vp, vp, vp, vp, vp, i64, i32, d, vp, vp]),
         "ora_label": (i32, [vp, i32, i64, i64, vp, vp, i64, vp]),
         "ora_label_points": (i32, [i32, vp, i64, vp, vp, i64, vp]),
@@ -218,24 +218,37 @@ def seeds_lattice(n_xyz, dim, r0, dR=2.0):
     return st, out[:cnt.value] if st == OK else out[:0]
 
 
-def is_maxima_seed(vol, dim, w, thr, x, y, z, z_lo=0, n_global=None):
-    v = _u16(vol)
-    n = _dims(v) if n_global is None else np.asarray(n_global, np.int64).copy()
-    return bool(lib().ora_is_maxima_seed(_p(v), _p(n), dim, z_lo, v.shape[0] if v.ndim == 3 else 1,
-                                         w, thr, x, y, z))
+def _box(v, org, n_global, z_lo=0):
+    """(global dims, box origin, box dims) as int64 arrays for a buffer v."""
+    nb = _dims(v)
+    org = np.array([0, 0, z_lo] if org is None else org, np.int64)
+    n = (org + nb) if n_global is None else np.asarray(n_global, np.int64).copy()
+    if n_global is None and tuple(org) != (0, 0, 0):
+        raise ValueError("n_global is required for a crop")
+    return n, org, nb
 
 
-def seeds_maxima(vol, dim, w, thr, z_lo=0, n_global=None, zs=None):
+def is_maxima_seed(vol, dim, w, thr, x, y, z, org=None, n_global=None):
     v = _u16(vol)
-    nzb = v.shape[0] if v.ndim == 3 else 1
-    n = _dims(v) if n_global is None else np.asarray(n_global, np.int64).copy()
-    zs0, zs1 = (z_lo, z_lo + nzb) if zs is None else zs
+    n, o, nb = _box(v, org, n_global)
+    r = lib().ora_is_maxima_seed(_p(v), _p(n), _p(o), _p(nb), dim, w, thr, x, y, z)
+    if r < 0:
+        raise ValueError("window outside the buffer")
+    return bool(r)
+
+
+def seeds_maxima(vol, dim, w, thr, org=None, n_global=None, lo=None, hi=None):
+    """Seeds of the (global) box lo..hi (inclusive; default: the whole buffer)."""
+    v = _u16(vol)
+    n, o, nb = _box(v, org, n_global)
+    lo = o.copy() if lo is None else np.asarray(lo, np.int64).copy()
+    hi = (o + nb - 1) if hi is None else np.asarray(hi, np.int64).copy()
     cnt = C.c_int64()
     cap = 1 << 16
     while True:
         out = np.zeros((cap, 3), np.float32)
-        st = lib().ora_seeds_maxima(_p(v), _p(n), dim, z_lo, nzb, zs0, zs1, w, thr, _p(out), cap,
-                                    C.byref(cnt))
+        st = lib().ora_seeds_maxima(_p(v), _p(n), _p(o), _p(nb), _p(lo), _p(hi), dim, w, thr, _p(out),
+                                    cap, C.byref(cnt))
         if st == CAPACITY:
             cap = int(cnt.value)
             continue
@@ -244,14 +257,13 @@ def seeds_maxima(vol, dim, w, thr, z_lo=0, n_global=None, zs=None):
         return out[:cnt.value]
 
 
-def energy_mc(vol, params: Params, c, R, it, cell_id, z_lo=0, n_global=None):
+def energy_mc(vol, params: Params, c, R, it, cell_id, org=None, n_global=None):
     v = _u16(vol)
-    n = _dims(v) if n_global is None else np.asarray(n_global, np.int64).copy()
+    n, o, nb = _box(v, org, n_global)
     cc = np.asarray(c, np.float64).copy()
     out = np.zeros(6)
     pc = params.c()
-    lib().ora_energy_mc(_p(v), _p(n), z_lo, v.shape[0] if v.ndim == 3 else 1, C.byref(pc), _p(cc),
-                        R, it, cell_id, _p(out))
+    lib().ora_energy_mc(_p(v), _p(n), _p(o), _p(nb), C.byref(pc), _p(cc), R, it, cell_id, _p(out))
     return out
 
 
@@ -261,8 +273,8 @@ def energy_grid(vol, params: Params, c, R):
     cc = np.asarray(c, np.float64).copy()
     out = np.zeros(6)
     pc = params.c()
-    lib().ora_energy_grid(_p(v), _p(n), 0, v.shape[0] if v.ndim == 3 else 1, C.byref(pc), _p(cc), R,
-                          _p(out))
+    o = np.zeros(3, np.int64)
+    lib().ora_energy_grid(_p(v), _p(n), _p(o), _p(n), C.byref(pc), _p(cc), R, _p(out))
     return out
 
 
@@ -273,17 +285,19 @@ def energy_ss(vol, params: Params, c, R, q=6):
     return lib().ora_energy_ss(_p(v), _p(_dims(v)), C.byref(pc), _p(cc), R, q)
 
 
-def evolve(vol, params: Params, seeds, ids=None, z_lo=0, n_global=None):
-    """O5 for every seed; returns a CELL_DTYPE record array."""
+def evolve(vol, params: Params, seeds, ids=None, org=None, n_global=None, z_lo=0):
+    """O5 for every seed; returns a CELL_DTYPE record array.  ``vol`` may be a
+    crop/slab at ``org`` (or planes from ``z_lo``) of a volume of dims ``n_global``."""
     v = _u16(vol)
-    n = _dims(v) if n_global is None else np.asarray(n_global, np.int64).copy()
+    if org is None and z_lo:
+        org = (0, 0, z_lo)
+    n, o, nb = _box(v, org, n_global)
     s = np.ascontiguousarray(seeds, np.float32).reshape(-1, 3)
     ids = (np.arange(len(s), dtype=np.int64) if ids is None
            else np.ascontiguousarray(ids, np.int64))
     out = np.zeros(len(s), CELL_DTYPE)
     pc = params.c()
-    lib().ora_evolve(_p(v), _p(n), z_lo, v.shape[0] if v.ndim == 3 else 1, C.byref(pc), _p(s),
-                     _p(ids), len(s), _p(out))
+    lib().ora_evolve(_p(v), _p(n), _p(o), _p(nb), C.byref(pc), _p(s), _p(ids), len(s), _p(out))
     return out
 
 

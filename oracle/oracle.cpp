@@ -131,20 +131,22 @@ void weight(double r, double R, double dR, double rho, double* S, double* S_r, d
 // ---------------------------------------------------------------------------
 // The image I(x) of Eq. 2 at a non-integer point: d-linear interpolation of the
 // u16 smoothed volume (G17), clamp-to-edge, scaled by iscale
-// (G6: u16 -> 8-bit units, 1/257).  The volume buffer may hold only the planes
-// [z_lo, z_lo + nz_buf) of a volume of global size n (z-slabs, §8(e)); a
-// lookup outside the buffer is clamped into it and reported via *halo.
+// (G6: u16 -> 8-bit units, 1/257).  The volume buffer may hold only a box of a
+// volume of global size n: voxels org + [0, nb) (z-slabs, §8(e), or a crop
+// used by the full-size tests); a lookup outside the box is clamped into it
+// and reported via *halo.
 struct Image {
   const uint16_t* v;
   int64_t n[3];
-  int64_t z_lo, nz_buf;
+  int64_t org[3], nb[3];
   int dim;
   double iscale;
 
   double voxel(int64_t x, int64_t y, int64_t z, bool* halo) const {
-    int64_t zb = z - z_lo;
-    if (zb < 0 || zb >= nz_buf) { *halo = true; zb = clampi(zb, 0, nz_buf - 1); }
-    return (double)v[(zb * n[1] + y) * n[0] + x];
+    int64_t p[3] = {x - org[0], y - org[1], z - org[2]};
+    for (int a = 0; a < 3; ++a)
+      if (p[a] < 0 || p[a] >= nb[a]) { *halo = true; p[a] = clampi(p[a], 0, nb[a] - 1); }
+    return (double)v[(p[2] * nb[1] + p[1]) * nb[0] + p[0]];
   }
 
   // trilinear (bilinear in 2D): clamp k to [0, n-1], i0 = min(floor(k), n-2),
@@ -390,46 +392,66 @@ int ora_seeds_lattice(const int64_t n[3], int dim, double r0, double dR, float* 
 // that reliably places initial contours").  x is a seed iff B(x) >= thr and no
 // y in the (2w+1)^d box W(x) (clipped to the volume) has B(y) > B(x), or
 // B(y) = B(x) with lin(y) < lin(x).  Seeds are listed in linear-index order.
-// The volume buffer holds planes [z_lo, z_lo + nz_buf) of a global volume n;
-// only planes [zs0, zs1) are scanned.  Windows must lie inside the buffer
-// (the slab driver sizes halos for that); returns SHAPE otherwise.
-static bool is_maxima_seed(const uint16_t* B, const int64_t n[3], int dim, int64_t z_lo,
-                           int64_t nz_buf, int w, uint32_t thr, int64_t x, int64_t y, int64_t z) {
-  const int64_t nx = n[0], ny = n[1];
-  const uint16_t v = B[((z - z_lo) * ny + y) * nx + x];
+// The buffer holds the box org + [0, nb) of a global volume n; the box
+// lo..hi (inclusive, global coordinates) is scanned.  Every scanned window
+// must lie inside the buffer (the slab driver and the crop tests size their
+// margins for that); returns SHAPE otherwise.
+struct Box {
+  const uint16_t* B;
+  int64_t n[3], org[3], nb[3];
+  uint16_t at(int64_t x, int64_t y, int64_t z) const {
+    return B[((z - org[2]) * nb[1] + (y - org[1])) * nb[0] + (x - org[0])];
+  }
+};
+
+static bool is_maxima_seed(const Box& b, int dim, int w, uint32_t thr, int64_t x, int64_t y,
+                           int64_t z) {
+  const int64_t nx = b.n[0], ny = b.n[1];
+  const uint16_t v = b.at(x, y, z);
   if ((uint32_t)v < thr) return false;
   const int64_t lin = (z * ny + y) * nx + x;
   const int64_t z0 = dim == 3 ? std::max<int64_t>(z - w, 0) : z;
-  const int64_t z1 = dim == 3 ? std::min<int64_t>(z + w, n[2] - 1) : z;
+  const int64_t z1 = dim == 3 ? std::min<int64_t>(z + w, b.n[2] - 1) : z;
   for (int64_t zz = z0; zz <= z1; ++zz)
     for (int64_t yy = std::max<int64_t>(y - w, 0); yy <= std::min<int64_t>(y + w, ny - 1); ++yy)
       for (int64_t xx = std::max<int64_t>(x - w, 0); xx <= std::min<int64_t>(x + w, nx - 1); ++xx) {
-        const uint16_t u = B[((zz - z_lo) * ny + yy) * nx + xx];
+        const uint16_t u = b.at(xx, yy, zz);
         if (u > v) return false;
         if (u == v && (zz * ny + yy) * nx + xx < lin) return false;
       }
   return true;
 }
 
-int ora_is_maxima_seed(const uint16_t* B, const int64_t n[3], int dim, int64_t z_lo, int64_t nz_buf,
-                       int w, uint32_t thr, int64_t x, int64_t y, int64_t z) {
-  return is_maxima_seed(B, n, dim, z_lo, nz_buf, w, thr, x, y, z) ? 1 : 0;
+static bool window_inside(const Box& b, int dim, int w, const int64_t lo[3], const int64_t hi[3]) {
+  for (int a = 0; a < dim; ++a) {
+    const int64_t wl = std::max<int64_t>(lo[a] - w, 0), wh = std::min<int64_t>(hi[a] + w, b.n[a] - 1);
+    if (wl < b.org[a] || wh >= b.org[a] + b.nb[a]) return false;
+  }
+  return true;
 }
 
-int ora_seeds_maxima(const uint16_t* B, const int64_t n[3], int dim, int64_t z_lo, int64_t nz_buf,
-                     int64_t zs0, int64_t zs1, int w, uint32_t thr, float* out_xyz, int64_t cap,
-                     int64_t* count) {
-  if (dim == 3 && (std::max<int64_t>(zs0 - w, 0) < z_lo ||
-                   std::min<int64_t>(zs1 - 1 + w, n[2] - 1) >= z_lo + nz_buf))
-    return ORA_SHAPE;
-  const int64_t nplanes = zs1 - zs0;
+int ora_is_maxima_seed(const uint16_t* B, const int64_t n[3], const int64_t org[3],
+                       const int64_t nb[3], int dim, int w, uint32_t thr, int64_t x, int64_t y,
+                       int64_t z) {
+  Box b{B, {n[0], n[1], n[2]}, {org[0], org[1], org[2]}, {nb[0], nb[1], nb[2]}};
+  const int64_t p[3] = {x, y, z};
+  if (!window_inside(b, dim, w, p, p)) return -1;
+  return is_maxima_seed(b, dim, w, thr, x, y, z) ? 1 : 0;
+}
+
+int ora_seeds_maxima(const uint16_t* B, const int64_t n[3], const int64_t org[3],
+                     const int64_t nb[3], const int64_t lo[3], const int64_t hi[3], int dim, int w,
+                     uint32_t thr, float* out_xyz, int64_t cap, int64_t* count) {
+  Box b{B, {n[0], n[1], n[2]}, {org[0], org[1], org[2]}, {nb[0], nb[1], nb[2]}};
+  if (!window_inside(b, dim, w, lo, hi)) return ORA_SHAPE;
+  const int64_t nplanes = hi[2] - lo[2] + 1;
   std::vector<std::vector<int64_t>> per_plane(nplanes > 0 ? nplanes : 0);
 #pragma omp parallel for schedule(dynamic, 1)
   for (int64_t zi = 0; zi < nplanes; ++zi) {
-    const int64_t z = zs0 + zi;
-    for (int64_t y = 0; y < n[1]; ++y)
-      for (int64_t x = 0; x < n[0]; ++x)
-        if (is_maxima_seed(B, n, dim, z_lo, nz_buf, w, thr, x, y, z))
+    const int64_t z = lo[2] + zi;
+    for (int64_t y = lo[1]; y <= hi[1]; ++y)
+      for (int64_t x = lo[0]; x <= hi[0]; ++x)
+        if (is_maxima_seed(b, dim, w, thr, x, y, z))
           per_plane[zi].push_back((z * n[1] + y) * n[0] + x);
   }
   int64_t total = 0;
@@ -528,30 +550,32 @@ static EnergyOut energy_grid(const Image& img, const ora_params& p, const double
   return o;
 }
 
-static Image make_image(const uint16_t* v, const int64_t n[3], int64_t z_lo, int64_t nz_buf,
-                        const ora_params* p) {
+static Image make_image(const uint16_t* v, const int64_t n[3], const int64_t org[3],
+                        const int64_t nb[3], const ora_params* p) {
   Image img;
   img.v = v;
-  for (int a = 0; a < 3; ++a) img.n[a] = n[a];
-  img.z_lo = z_lo;
-  img.nz_buf = nz_buf;
+  for (int a = 0; a < 3; ++a) {
+    img.n[a] = n[a];
+    img.org[a] = org ? org[a] : 0;
+    img.nb[a] = nb ? nb[a] : n[a];
+  }
   img.dim = p->dim;
   img.iscale = p->iscale;
   return img;
 }
 
-void ora_energy_mc(const uint16_t* v, const int64_t n[3], int64_t z_lo, int64_t nz_buf,
+void ora_energy_mc(const uint16_t* v, const int64_t n[3], const int64_t org[3], const int64_t nb[3],
                    const ora_params* p, const double c[3], double R, uint32_t iter, int64_t id,
                    double* out6) {
-  const Image img = make_image(v, n, z_lo, nz_buf, p);
+  const Image img = make_image(v, n, org, nb, p);
   const EnergyOut o = energy_mc(img, *p, c, R, iter, id);
   out6[0] = o.E; out6[1] = o.gc[0]; out6[2] = o.gc[1]; out6[3] = o.gc[2]; out6[4] = o.gR;
   out6[5] = o.halo ? 1.0 : 0.0;
 }
 
-void ora_energy_grid(const uint16_t* v, const int64_t n[3], int64_t z_lo, int64_t nz_buf,
+void ora_energy_grid(const uint16_t* v, const int64_t n[3], const int64_t org[3], const int64_t nb[3],
                      const ora_params* p, const double c[3], double R, double* out6) {
-  const Image img = make_image(v, n, z_lo, nz_buf, p);
+  const Image img = make_image(v, n, org, nb, p);
   const EnergyOut o = energy_grid(img, *p, c, R);
   out6[0] = o.E; out6[1] = o.gc[0]; out6[2] = o.gc[1]; out6[3] = o.gc[2]; out6[4] = o.gR;
   out6[5] = o.halo ? 1.0 : 0.0;
@@ -561,7 +585,7 @@ void ora_energy_grid(const uint16_t* v, const int64_t n[3], int64_t z_lo, int64_
 // per voxel, i.e. the continuous integral the MC estimator is unbiased for.
 double ora_energy_ss(const uint16_t* v, const int64_t n[3], const ora_params* p, const double c[3],
                      double R, int q) {
-  const Image img = make_image(v, n, 0, n[2], p);
+  const Image img = make_image(v, n, nullptr, nullptr, p);
   const int d = p->dim;
   const double rho = rho_of(d);
   const double rho_s = R + p->delta_R / 2.0;
@@ -604,10 +628,10 @@ double ora_energy_ss(const uint16_t* v, const int64_t n[3], const ora_params* p,
 // shorter than 2m.  Iteration T+1 only evaluates E_final (G13).  CONVERGED if the
 // state moved by less than conv_tol (max norm) in iteration T (G9);
 // cells are never frozen.  Stops at T = max_iters.
-void ora_evolve(const uint16_t* v, const int64_t n[3], int64_t z_lo, int64_t nz_buf,
+void ora_evolve(const uint16_t* v, const int64_t n[3], const int64_t org[3], const int64_t nb[3],
                 const ora_params* p, const float* seeds_xyz, const int64_t* ids, int64_t ncell,
                 ora_cell* out) {
-  const Image img = make_image(v, n, z_lo, nz_buf, p);
+  const Image img = make_image(v, n, org, nb, p);
   const int d = p->dim;
   const int T = p->max_iters;
 #pragma omp parallel for schedule(dynamic, 1)

@@ -1,0 +1,332 @@
+// abi.cu — the extern "C" boundary of libsnk.so (include/snk.h): validation,
+// workspace sizing, status/error reporting and the single-GPU snk_run chain.
+// All device work is in the kernels of volume.cu, seeds.cu, evolve.cu,
+// cull.cu and label.cu.
+#include <cmath>
+#include <cstring>
+#include <string>
+
+#include "common.cuh"
+
+namespace snk {
+
+static thread_local std::string g_err;
+static thread_local int64_t g_launches = 0;
+
+void set_error(const std::string& msg) { g_err = msg; }
+void clear_error() { g_err.clear(); }
+int32_t fail(int32_t status, const std::string& msg) {
+  g_err = msg;
+  return status;
+}
+int32_t cuda_fail(cudaError_t e, const char* where) {
+  g_err = std::string(where) + ": " + cudaGetErrorName(e) + ": " + cudaGetErrorString(e);
+  return SNK_CUDA;
+}
+void count_launch(int64_t k) { g_launches += k; }
+
+static bool is_pow2(int64_t v) { return v > 0 && (v & (v - 1)) == 0; }
+
+static int32_t validate_grid(const snk_grid* g) {
+  if (!g) return fail(SNK_CONFIG, "grid is null");
+  if (g->dim != 2 && g->dim != 3) return fail(SNK_SHAPE, "dim must be 2 or 3");
+  for (int a = 0; a < g->dim; ++a)
+    if (g->n[a] < 2) return fail(SNK_SHAPE, "every used axis needs at least 2 voxels");
+  if (g->dim == 2 && g->n[2] != 1) return fail(SNK_SHAPE, "2D images need n[2] == 1");
+  if (g->n[0] > (1 << 30) || g->n[1] > (1 << 30) || g->n[2] > (1 << 30))
+    return fail(SNK_SHAPE, "axis too long");
+  if (g->z_lo < 0 || g->nz_buf < 1 || g->z_lo + g->nz_buf > g->n[2])
+    return fail(SNK_SHAPE, "buffer planes [z_lo, z_lo+nz_buf) must lie inside the volume");
+  if (g->dim == 3 && g->nz_buf < 2) return fail(SNK_SHAPE, "3D buffers need at least 2 planes");
+  if (g->own_z0 < g->z_lo || g->own_z1 > g->z_lo + g->nz_buf || g->own_z0 > g->own_z1)
+    return fail(SNK_SHAPE, "owned planes must lie inside the buffer");
+  const double nvox = (double)g->n[0] * (double)g->n[1] * (double)g->nz_buf;
+  if (nvox >= 4294967296.0) return fail(SNK_SHAPE, "buffer exceeds 2^32 voxels; use z-slabs");
+  return SNK_OK;
+}
+
+static int32_t validate_params(const snk_params* p, int dim) {
+  if (!p) return fail(SNK_CONFIG, "params is null");
+  if (!(p->r0 > 0) || !(p->delta_R > 0) || !(p->eps0 > 0) || !(p->max_step > 0))
+    return fail(SNK_CONFIG, "r0, delta_R, eps0 and max_step must be > 0");
+  if (!(p->e0 <= 0)) return fail(SNK_CONFIG, "e0 must be <= 0 (S:262)");
+  if (!(p->r_min > 0) || !(p->r0 > p->r_min) || !(p->r_max >= p->r0))
+    return fail(SNK_CONFIG, "need 0 < r_min < r0 <= r_max");
+  if (!(p->leash >= 0) || !(p->conv_tol >= 0) || !(p->intensity_scale > 0))
+    return fail(SNK_CONFIG, "leash, conv_tol >= 0 and intensity_scale > 0");
+  if (!(p->sigma >= 0) || std::ceil(4.0 * p->sigma) > 32)
+    return fail(SNK_CONFIG, "sigma must be in [0, 8]");
+  if (p->max_iters < 1 || p->max_iters > (1 << 24)) return fail(SNK_CONFIG, "max_iters in [1, 2^24]");
+  if (!is_pow2(p->n_samples) || p->n_samples < 32 || p->n_samples > (1 << 20))
+    return fail(SNK_CONFIG, "n_samples must be a power of two in [32, 2^20]");
+  if (p->cta_warps != 0 && !(is_pow2(p->cta_warps) && p->cta_warps <= 8))
+    return fail(SNK_CONFIG, "cta_warps must be 0 (auto), 1, 2, 4 or 8");
+  if (p->cta_warps > 0 && p->n_samples < 32 * p->cta_warps)
+    return fail(SNK_CONFIG, "n_samples must be >= 32 * cta_warps");
+  if (p->seed_mode < 0 || p->seed_mode > 2) return fail(SNK_CONFIG, "bad seed_mode");
+  if (p->seed_mode == SNK_SEED_MAXIMA && (p->seed_window < 0 || p->seed_window > 64))
+    return fail(SNK_CONFIG, "seed_window must be in [0, 64]");
+  if (p->image_term != SNK_IMAGE_INTENSITY && p->image_term != SNK_IMAGE_GRADMAG)
+    return fail(SNK_CONFIG, "bad image_term");
+  (void)dim;
+  return SNK_OK;
+}
+
+static int32_t validate(const snk_grid* g, const snk_params* p) {
+  SNK_TRY(validate_grid(g));
+  SNK_TRY(validate_params(p, g->dim));
+  return SNK_OK;
+}
+
+static int32_t check_ws(size_t need, void* d_ws, size_t ws_bytes) {
+  if (need > 0 && (d_ws == nullptr || ws_bytes < need))
+    return fail(SNK_CAPACITY, "workspace too small: need " + std::to_string(need) + " bytes");
+  return SNK_OK;
+}
+
+}  // namespace snk
+
+using namespace snk;
+
+extern "C" {
+
+int32_t snk_abi_version(void) { return SNK_ABI_VERSION; }
+
+const char* snk_last_error(void) { return g_err.c_str(); }
+
+const char* snk_status_string(int32_t s) {
+  switch (s) {
+    case SNK_OK: return "ok";
+    case SNK_EMPTY_DOMAIN: return "empty domain";
+    case SNK_CONFIG: return "invalid configuration";
+    case SNK_SHAPE: return "invalid shape";
+    case SNK_INTERNAL: return "internal error";
+    case SNK_CUDA: return "CUDA error";
+    case SNK_CAPACITY: return "capacity exceeded";
+    default: return "unknown status";
+  }
+}
+
+int64_t snk_launch_count(void) { return g_launches; }
+
+int32_t snk_validate(const snk_grid* g, const snk_params* p) {
+  clear_error();
+  return validate(g, p);
+}
+
+int32_t snk_workspace_bytes(const snk_grid* g, const snk_params* p, int64_t max_cells,
+                            size_t* bytes) {
+  clear_error();
+  SNK_TRY(validate(g, p));
+  if (!bytes || max_cells < 0) return fail(SNK_CONFIG, "bytes is null or max_cells < 0");
+  size_t b = preprocess_ws(g, p);
+  b = std::max(b, seeds_ws(g, p));
+  b = std::max(b, evolve_ws(g, p, max_cells));
+  b = std::max(b, cull_ws(g, p, max_cells));
+  b = std::max(b, label_ws(g, p, max_cells));
+  *bytes = b;
+  return SNK_OK;
+}
+
+int32_t snk_resample_dims(int32_t dim, const int64_t n_raw[3], const double spacing[3],
+                          int64_t n_out[3]) {
+  clear_error();
+  if ((dim != 2 && dim != 3) || !n_raw || !spacing || !n_out) return fail(SNK_CONFIG, "bad args");
+  double smin = spacing[0];
+  for (int a = 0; a < dim; ++a) {
+    if (!(spacing[a] > 0)) return fail(SNK_CONFIG, "spacing must be > 0");
+    smin = std::min(smin, spacing[a]);
+  }
+  for (int a = 0; a < 3; ++a) {
+    n_out[a] = n_raw[a];
+    if (a < dim && spacing[a] > smin) n_out[a] = (int64_t)std::llround((double)n_raw[a] * spacing[a] / smin);
+  }
+  return SNK_OK;
+}
+
+int32_t snk_resample(int32_t dim, const int64_t n_raw[3], const double spacing[3], int64_t zr_lo,
+                     int64_t nzr, const uint16_t* d_raw, int64_t z_lo, int64_t nz_out,
+                     uint16_t* d_out, void* d_ws, size_t ws_bytes, void* stream) {
+  clear_error();
+  if (!d_raw || !d_out) return fail(SNK_CONFIG, "null buffer");
+  SNK_TRY(check_ws(resample_ws(dim, n_raw, spacing), d_ws, ws_bytes));
+  return resample_impl(dim, n_raw, spacing, zr_lo, nzr, d_raw, z_lo, nz_out, d_out, d_ws,
+                       ws_bytes, as_stream(stream));
+}
+
+int32_t snk_preprocess(const snk_grid* g, const snk_params* p, const uint16_t* d_in,
+                       uint16_t* d_smooth, uint16_t* d_gradmag, void* d_ws, size_t ws_bytes,
+                       void* stream) {
+  clear_error();
+  SNK_TRY(validate(g, p));
+  if (!d_in || !d_smooth) return fail(SNK_CONFIG, "null buffer");
+  SNK_TRY(check_ws(preprocess_ws(g, p), d_ws, ws_bytes));
+  return preprocess_impl(g, p, d_in, d_smooth, d_gradmag, d_ws, ws_bytes, as_stream(stream));
+}
+
+int32_t snk_seeds(const snk_grid* g, const snk_params* p, const uint16_t* d_smooth,
+                  float* d_seeds, int64_t cap, int64_t* n_out, int64_t* first_id_out,
+                  void* d_ws, size_t ws_bytes, void* stream) {
+  clear_error();
+  SNK_TRY(validate(g, p));
+  if (!n_out || cap < 0 || (cap > 0 && !d_seeds)) return fail(SNK_CONFIG, "bad output buffer");
+  if (p->seed_mode == SNK_SEED_GIVEN) return fail(SNK_CONFIG, "seed_mode GIVEN: seeds come from the caller");
+  if (p->seed_mode == SNK_SEED_MAXIMA && !d_smooth) return fail(SNK_CONFIG, "null volume");
+  SNK_TRY(check_ws(seeds_ws(g, p), d_ws, ws_bytes));
+  return seeds_impl(g, p, d_smooth, d_seeds, cap, n_out, first_id_out, d_ws, ws_bytes,
+                    as_stream(stream));
+}
+
+int32_t snk_evolve(const snk_grid* g, const snk_params* p, const uint16_t* d_image,
+                   const float* d_seeds, const int64_t* d_ids, int64_t id_base, int64_t n,
+                   snk_cell* d_cells, void* d_ws, size_t ws_bytes, void* stream) {
+  clear_error();
+  SNK_TRY(validate(g, p));
+  if (n < 0) return fail(SNK_CONFIG, "n < 0");
+  if (n == 0) return SNK_OK;
+  if (!d_image || !d_seeds || !d_cells) return fail(SNK_CONFIG, "null buffer");
+  SNK_TRY(check_ws(evolve_ws(g, p, n), d_ws, ws_bytes));
+  return evolve_impl(g, p, d_image, d_seeds, d_ids, id_base, n, d_cells, d_ws, ws_bytes,
+                     as_stream(stream));
+}
+
+int32_t snk_compact_candidates(const snk_params* p, const snk_cell* d_cells, int64_t n,
+                               snk_cell* d_out, int64_t cap, int64_t* n_out, void* d_ws,
+                               size_t ws_bytes, void* stream) {
+  clear_error();
+  if (!p || !n_out || n < 0 || cap < 0) return fail(SNK_CONFIG, "bad args");
+  if (n > 0 && (!d_cells || (cap > 0 && !d_out))) return fail(SNK_CONFIG, "null buffer");
+  return compact_impl(p, d_cells, n, d_out, cap, n_out, d_ws, ws_bytes, as_stream(stream));
+}
+
+int32_t snk_cull(const snk_grid* g, const snk_params* p, const snk_cell* d_cells, int64_t n,
+                 snk_cell* d_dets, int64_t cap, int64_t* n_out, void* d_ws, size_t ws_bytes,
+                 void* stream) {
+  clear_error();
+  SNK_TRY(validate(g, p));
+  if (!n_out || n < 0 || cap < 0) return fail(SNK_CONFIG, "bad args");
+  if (n > 0 && (!d_cells || (cap > 0 && !d_dets))) return fail(SNK_CONFIG, "null buffer");
+  if (n >= ((int64_t)1 << 31)) return fail(SNK_SHAPE, "too many cells");
+  SNK_TRY(check_ws(cull_ws(g, p, n), d_ws, ws_bytes));
+  return cull_impl(g, p, d_cells, n, d_dets, cap, n_out, d_ws, ws_bytes, as_stream(stream));
+}
+
+int32_t snk_label(const snk_grid* g, const snk_params* p, const snk_cell* d_dets, int64_t n,
+                  int32_t* d_labels, void* d_ws, size_t ws_bytes, void* stream) {
+  clear_error();
+  SNK_TRY(validate(g, p));
+  if (!d_labels || n < 0 || (n > 0 && !d_dets)) return fail(SNK_CONFIG, "bad args");
+  SNK_TRY(check_ws(label_ws(g, p, n), d_ws, ws_bytes));
+  return label_impl(g, p, d_dets, n, d_labels, d_ws, ws_bytes, as_stream(stream));
+}
+
+// --------------------------------------------------------------------------
+// snk_run: the single-GPU end-to-end call from host buffers.
+// Workspace layout: [raw | (resampled) | smooth | gradmag? | seeds | cells |
+//                    dets | labels | scratch]
+struct RunLayout {
+  snk_grid g;
+  int64_t n_iso[3];
+  bool resample;
+  size_t off_raw, off_iso, off_smooth, off_grad, off_seeds, off_cells, off_dets, off_labels,
+      off_scratch, scratch_bytes, total;
+};
+
+static int32_t run_layout(int32_t dim, const int64_t n_raw[3], const double spacing[3],
+                          const snk_params* p, int64_t max_cells, RunLayout* L) {
+  SNK_TRY(snk_resample_dims(dim, n_raw, spacing, L->n_iso));
+  L->resample = false;
+  for (int a = 0; a < 3; ++a) L->resample |= (L->n_iso[a] != n_raw[a]);
+  snk_grid& g = L->g;
+  std::memset(&g, 0, sizeof g);
+  g.dim = dim;
+  for (int a = 0; a < 3; ++a) g.n[a] = L->n_iso[a];
+  g.z_lo = 0;
+  g.nz_buf = L->n_iso[2];
+  g.own_z0 = 0;
+  g.own_z1 = L->n_iso[2];
+  SNK_TRY(validate(&g, p));
+  const size_t nraw = (size_t)n_raw[0] * n_raw[1] * n_raw[2];
+  const size_t niso = (size_t)g.n[0] * g.n[1] * g.n[2];
+  Carve c(nullptr, ~size_t(0));
+  L->off_raw = 0; c.take<uint16_t>(nraw);
+  c.off = (c.off + 255) & ~size_t(255); L->off_iso = c.off; if (L->resample) c.take<uint16_t>(niso);
+  c.off = (c.off + 255) & ~size_t(255); L->off_smooth = c.off; c.take<uint16_t>(niso);
+  c.off = (c.off + 255) & ~size_t(255); L->off_grad = c.off;
+  if (p->image_term == SNK_IMAGE_GRADMAG) c.take<uint16_t>(niso);
+  c.off = (c.off + 255) & ~size_t(255); L->off_seeds = c.off; c.take<float>(3 * (size_t)max_cells);
+  c.off = (c.off + 255) & ~size_t(255); L->off_cells = c.off; c.take<snk_cell>(max_cells);
+  c.off = (c.off + 255) & ~size_t(255); L->off_dets = c.off; c.take<snk_cell>(max_cells);
+  c.off = (c.off + 255) & ~size_t(255); L->off_labels = c.off; c.take<int32_t>(niso);
+  c.off = (c.off + 255) & ~size_t(255); L->off_scratch = c.off;
+  size_t s = 0;
+  SNK_TRY(snk_workspace_bytes(&g, p, max_cells, &s));
+  s = std::max(s, resample_ws(dim, n_raw, spacing));
+  L->scratch_bytes = s;
+  L->total = L->off_scratch + s;
+  return SNK_OK;
+}
+
+int32_t snk_run_workspace_bytes(int32_t dim, const int64_t n_raw[3], const double spacing[3],
+                                const snk_params* p, int64_t max_cells, size_t* bytes) {
+  clear_error();
+  if (!bytes || !n_raw || !spacing || max_cells < 1) return fail(SNK_CONFIG, "bad args");
+  RunLayout L;
+  SNK_TRY(run_layout(dim, n_raw, spacing, p, max_cells, &L));
+  *bytes = L.total;
+  return SNK_OK;
+}
+
+int32_t snk_run(int32_t dim, const int64_t n_raw[3], const double spacing[3],
+                const snk_params* p, const uint16_t* h_raw, snk_cell* h_dets, int64_t det_cap,
+                int64_t* n_dets, int32_t* h_labels, int64_t max_cells, void* d_ws,
+                size_t ws_bytes, void* stream) {
+  clear_error();
+  if (!h_raw || !n_dets || det_cap < 0 || (det_cap > 0 && !h_dets) || max_cells < 1)
+    return fail(SNK_CONFIG, "bad args");
+  RunLayout L;
+  SNK_TRY(run_layout(dim, n_raw, spacing, p, max_cells, &L));
+  SNK_TRY(check_ws(L.total, d_ws, ws_bytes));
+  cudaStream_t st = as_stream(stream);
+  char* base = static_cast<char*>(d_ws);
+  uint16_t* d_raw = reinterpret_cast<uint16_t*>(base + L.off_raw);
+  uint16_t* d_iso = L.resample ? reinterpret_cast<uint16_t*>(base + L.off_iso) : d_raw;
+  uint16_t* d_smooth = reinterpret_cast<uint16_t*>(base + L.off_smooth);
+  uint16_t* d_grad = p->image_term == SNK_IMAGE_GRADMAG ? reinterpret_cast<uint16_t*>(base + L.off_grad) : nullptr;
+  float* d_seeds = reinterpret_cast<float*>(base + L.off_seeds);
+  snk_cell* d_cells = reinterpret_cast<snk_cell*>(base + L.off_cells);
+  snk_cell* d_dets = reinterpret_cast<snk_cell*>(base + L.off_dets);
+  int32_t* d_labels = reinterpret_cast<int32_t*>(base + L.off_labels);
+  void* scratch = base + L.off_scratch;
+  const size_t sb = L.scratch_bytes;
+  const size_t nraw = (size_t)n_raw[0] * n_raw[1] * n_raw[2];
+  const size_t niso = (size_t)L.g.n[0] * L.g.n[1] * L.g.n[2];
+
+  SNK_CUDA_CHECK(cudaMemcpyAsync(d_raw, h_raw, nraw * sizeof(uint16_t), cudaMemcpyHostToDevice, st));
+  if (L.resample)
+    SNK_TRY(resample_impl(dim, n_raw, spacing, 0, n_raw[2], d_raw, 0, L.g.n[2], d_iso, scratch, sb, st));
+  SNK_TRY(preprocess_impl(&L.g, p, d_iso, d_smooth, d_grad, scratch, sb, st));
+  int64_t ns = 0, first = 0;
+  SNK_TRY(seeds_impl(&L.g, p, d_smooth, d_seeds, max_cells, &ns, &first, scratch, sb, st));
+  if (ns > 0)
+    SNK_TRY(evolve_impl(&L.g, p, d_grad ? d_grad : d_smooth, d_seeds, nullptr, first, ns, d_cells,
+                        scratch, sb, st));
+  int64_t nd = 0;
+  SNK_TRY(cull_impl(&L.g, p, d_cells, ns, d_dets, max_cells, &nd, scratch, sb, st));
+  *n_dets = nd;
+  if (h_labels) SNK_TRY(label_impl(&L.g, p, d_dets, nd, d_labels, scratch, sb, st));
+  const int64_t ncopy = std::min(nd, det_cap);
+  if (ncopy > 0)
+    SNK_CUDA_CHECK(cudaMemcpyAsync(h_dets, d_dets, ncopy * sizeof(snk_cell), cudaMemcpyDeviceToHost, st));
+  if (h_labels)
+    SNK_CUDA_CHECK(cudaMemcpyAsync(h_labels, d_labels, niso * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  SNK_CUDA_CHECK(cudaStreamSynchronize(st));
+  if (nd > det_cap) return fail(SNK_CAPACITY, "detection buffer too small");
+  return SNK_OK;
+}
+
+}  // extern "C"
+
+static_assert(sizeof(snk_grid) == 64, "snk_grid layout is part of the ABI");
+static_assert(sizeof(snk_params) == 128, "snk_params layout is part of the ABI");
+static_assert(sizeof(snk_cell) == 48, "snk_cell layout is part of the ABI");

@@ -1,0 +1,104 @@
+// common.cuh — shared host/device helpers of libsnk (the CUDA path).
+// Nothing here is shared with oracle/ (the test oracle).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "../../include/snk.h"
+
+namespace snk {
+
+// ---------------------------------------------------------------- errors
+void set_error(const std::string& msg);
+void clear_error();
+int32_t fail(int32_t status, const std::string& msg);
+int32_t cuda_fail(cudaError_t e, const char* where);
+void count_launch(int64_t k = 1);
+
+#define SNK_CUDA_CHECK(expr)                                  \
+  do {                                                        \
+    cudaError_t _e = (expr);                                  \
+    if (_e != cudaSuccess) return ::snk::cuda_fail(_e, #expr); \
+  } while (0)
+
+#define SNK_LAUNCH_CHECK(name)                                     \
+  do {                                                             \
+    ::snk::count_launch();                                         \
+    cudaError_t _e = cudaGetLastError();                           \
+    if (_e != cudaSuccess) return ::snk::cuda_fail(_e, name);      \
+  } while (0)
+
+#define SNK_TRY(expr)                   \
+  do {                                  \
+    int32_t _s = (expr);                \
+    if (_s != SNK_OK) return _s;        \
+  } while (0)
+
+inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// ---------------------------------------------------------------- constants
+// rho = 2^(-1/d), as correctly rounded doubles; rho^2 for labels.
+constexpr double kRho3 = 0.7937005259840998;
+constexpr double kRho2 = 0.7071067811865476;
+constexpr double kRhoSq3 = 0.6299605249474366;
+constexpr double kRhoSq2 = 0.5;
+inline double rho_of(int dim) { return dim == 3 ? kRho3 : kRho2; }
+
+// ---------------------------------------------------------------- workspace
+// A bump allocator over the caller's workspace; 256-byte aligned slices.
+struct Carve {
+  char* base;
+  size_t cap;
+  size_t off = 0;
+  bool overflow = false;
+  Carve(void* b, size_t c) : base(static_cast<char*>(b)), cap(c) {}
+  template <typename T>
+  T* take(size_t count) {
+    off = (off + 255) & ~size_t(255);
+    T* p = reinterpret_cast<T*>(base ? base + off : nullptr);
+    off += count * sizeof(T);
+    if (off > cap) overflow = true;
+    return p;
+  }
+};
+
+inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// ---------------------------------------------------------------- sizes
+size_t preprocess_ws(const snk_grid* g, const snk_params* p);
+size_t seeds_ws(const snk_grid* g, const snk_params* p);
+size_t evolve_ws(const snk_grid* g, const snk_params* p, int64_t max_cells);
+size_t cull_ws(const snk_grid* g, const snk_params* p, int64_t max_cells);
+size_t label_ws(const snk_grid* g, const snk_params* p, int64_t max_cells);
+size_t resample_ws(int32_t dim, const int64_t n_raw[3], const double spacing[3]);
+
+// ---------------------------------------------------------------- entry points per file
+int32_t preprocess_impl(const snk_grid* g, const snk_params* p, const uint16_t* d_in,
+                        uint16_t* d_smooth, uint16_t* d_gradmag, void* d_ws, size_t ws_bytes,
+                        cudaStream_t st);
+int32_t resample_impl(int32_t dim, const int64_t n_raw[3], const double spacing[3], int64_t zr_lo,
+                      int64_t nzr, const uint16_t* d_raw, int64_t z_lo, int64_t nz_out,
+                      uint16_t* d_out, void* d_ws, size_t ws_bytes, cudaStream_t st);
+int32_t seeds_impl(const snk_grid* g, const snk_params* p, const uint16_t* d_smooth,
+                   float* d_seeds, int64_t cap, int64_t* n_out, int64_t* first_id, void* d_ws,
+                   size_t ws_bytes, cudaStream_t st);
+int32_t evolve_impl(const snk_grid* g, const snk_params* p, const uint16_t* d_image,
+                    const float* d_seeds, const int64_t* d_ids, int64_t id_base, int64_t n,
+                    snk_cell* d_cells, void* d_ws, size_t ws_bytes, cudaStream_t st);
+int32_t compact_impl(const snk_params* p, const snk_cell* d_cells, int64_t n, snk_cell* d_out,
+                     int64_t cap, int64_t* n_out, void* d_ws, size_t ws_bytes, cudaStream_t st);
+int32_t cull_impl(const snk_grid* g, const snk_params* p, const snk_cell* d_cells, int64_t n,
+                  snk_cell* d_dets, int64_t cap, int64_t* n_out, void* d_ws, size_t ws_bytes,
+                  cudaStream_t st);
+int32_t label_impl(const snk_grid* g, const snk_params* p, const snk_cell* d_dets, int64_t n,
+                   int32_t* d_labels, void* d_ws, size_t ws_bytes, cudaStream_t st);
+
+int evolve_warps_per_cell(const snk_params* p, int64_t n_cells);
+
+// exclusive scan of n int counts into n + 1 int64 offsets (offsets[n] = total)
+int32_t scan_counts(const int* counts, int64_t n, int64_t* offsets, cudaStream_t st);
+
+}  // namespace snk

@@ -1,0 +1,275 @@
+// volume.cu — a1 isotropic resampling, a2 separable Q14 Gaussian blur, a3
+// gradient magnitude (include/snk.h).  Integer-exact: results are bit-identical
+// to the definitions in DESIGN.md §3 (G16, G18, O3).
+//
+// Layout: u16 x-fastest volumes of nz planes; every kernel is a flat grid over
+// output voxels, threadIdx.x along x, so loads and stores are coalesced; the
+// stencil neighbours of the y/z passes are the rows/planes above and below and
+// are served from L1/L2 (each voxel is read from DRAM about once per pass).
+#include <cmath>
+#include <vector>
+
+#include "common.cuh"
+
+namespace snk {
+
+namespace {
+
+constexpr int kMaxTaps = 65;   // 2 * ceil(4 * 8) + 1
+__constant__ int32_t c_taps[kMaxTaps];
+
+// Q14 Gaussian taps (reading G18): h = ceil(4 sigma),
+// w_i = round(16384 exp(-i^2 / 2 sigma^2) / sum), centre absorbs the remainder.
+int q14_taps(double sigma, std::vector<int32_t>& taps) {
+  if (!(sigma > 0.0)) {
+    taps.assign(1, 16384);
+    return 0;
+  }
+  const int h = (int)std::ceil(4.0 * sigma);
+  std::vector<double> g(2 * h + 1);
+  double sum = 0.0;
+  for (int i = -h; i <= h; ++i) {
+    g[i + h] = std::exp(-(double)(i * i) / (2.0 * sigma * sigma));
+    sum += g[i + h];
+  }
+  taps.assign(2 * h + 1, 0);
+  int64_t tot = 0;
+  for (int i = 0; i <= 2 * h; ++i) {
+    taps[i] = (int32_t)std::floor(16384.0 * g[i] / sum + 0.5);
+    tot += taps[i];
+  }
+  taps[h] += (int32_t)(16384 - tot);
+  return h;
+}
+
+// One separable pass along AXIS (0 = x, 1 = y, 2 = z): out = (sum w_i in[clamp(p+i)] + 8192) >> 14.
+// Two output voxels per thread (x and x+1 share the row) -> 32-bit stores.
+template <int AXIS>
+__global__ void __launch_bounds__(256) blur_pass_kernel(const uint16_t* __restrict__ in,
+                                                        uint16_t* __restrict__ out, int nx, int ny,
+                                                        int nz, int h) {
+  const int64_t pairs_per_row = (nx + 1) >> 1;
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t total = pairs_per_row * ny * nz;
+  if (t >= total) return;
+  const int x0 = (int)(t % pairs_per_row) * 2;
+  const int64_t row = t / pairs_per_row;   // = z * ny + y
+  const int y = (int)(row % ny);
+  const int z = (int)(row / ny);
+  const int64_t plane = (int64_t)nx * ny;
+  uint32_t acc0 = 8192, acc1 = 8192;
+  const bool two = x0 + 1 < nx;
+  if (AXIS == 0) {
+    const uint16_t* r = in + row * nx;
+    for (int i = -h; i <= h; ++i) {
+      const uint32_t w = (uint32_t)c_taps[i + h];
+      const int xa = min(max(x0 + i, 0), nx - 1);
+      const int xb = min(max(x0 + 1 + i, 0), nx - 1);
+      acc0 += w * __ldg(r + xa);
+      acc1 += w * __ldg(r + xb);
+    }
+  } else {
+    const int p = AXIS == 1 ? y : z;
+    const int np = AXIS == 1 ? ny : nz;
+    const int64_t stride = AXIS == 1 ? nx : plane;
+    const uint16_t* base = in + row * nx - (int64_t)p * stride + x0;
+    for (int i = -h; i <= h; ++i) {
+      const uint32_t w = (uint32_t)c_taps[i + h];
+      const int q = min(max(p + i, 0), np - 1);
+      const uint16_t* src = base + (int64_t)q * stride;
+      acc0 += w * __ldg(src);
+      if (two) acc1 += w * __ldg(src + 1);
+    }
+  }
+  uint16_t* o = out + row * nx + x0;
+  o[0] = (uint16_t)(acc0 >> 14);
+  if (two) o[1] = (uint16_t)(acc1 >> 14);
+}
+
+// a3: G = (isqrt(gx^2 + gy^2 + gz^2) + 1) >> 1, central differences, clamp-to-edge.
+__device__ __forceinline__ uint32_t isqrt_u64(uint64_t v) {
+  uint64_t r = (uint64_t)sqrt((double)v);   // exact integer part after correction
+  while (r * r > v) --r;
+  while ((r + 1) * (r + 1) <= v) ++r;
+  return (uint32_t)r;
+}
+
+template <int D>
+__global__ void __launch_bounds__(256) gradmag_kernel(const uint16_t* __restrict__ B,
+                                                      uint16_t* __restrict__ G, int nx, int ny,
+                                                      int nz) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t plane = (int64_t)nx * ny;
+  if (t >= plane * nz) return;
+  const int x = (int)(t % nx);
+  const int y = (int)((t / nx) % ny);
+  const int z = (int)(t / plane);
+  const int64_t row = t - x;
+  const int gx = (int)__ldg(B + row + min(x + 1, nx - 1)) - (int)__ldg(B + row + max(x - 1, 0));
+  const int gy = (int)__ldg(B + t + (int64_t)(min(y + 1, ny - 1) - y) * nx) -
+                 (int)__ldg(B + t + (int64_t)(max(y - 1, 0) - y) * nx);
+  uint64_t s = (uint64_t)((int64_t)gx * gx) + (uint64_t)((int64_t)gy * gy);
+  if (D == 3) {
+    const int gz = (int)__ldg(B + t + (int64_t)(min(z + 1, nz - 1) - z) * plane) -
+                   (int)__ldg(B + t + (int64_t)(max(z - 1, 0) - z) * plane);
+    s += (uint64_t)((int64_t)gz * gz);
+  }
+  G[t] = (uint16_t)((isqrt_u64(s) + 1) >> 1);
+}
+
+// a1: one resampling pass along AXIS.  Input dims (ni[0], ni[1], ni[2]) holding
+// planes from in_z0 (AXIS 2 only: global raw plane of the buffer's first
+// plane); output dims with no[AXIS] = output samples, out_z0 likewise.
+// src = (k + 0.5) * ratio - 0.5 in IEEE double, no contraction (G16).
+template <int AXIS>
+__global__ void __launch_bounds__(256) resample_kernel(const uint16_t* __restrict__ in,
+                                                       uint16_t* __restrict__ out, int64_t nix,
+                                                       int64_t niy, int64_t noz, int64_t nox,
+                                                       int64_t noy, int64_t n_axis, double ratio,
+                                                       int64_t in_z0, int64_t out_z0) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= nox * noy * noz) return;
+  const int64_t x = t % nox, y = (t / nox) % noy, z = t / (nox * noy);
+  const int64_t kg = (AXIS == 0 ? x : AXIS == 1 ? y : z + out_z0);   // global output index
+  double src = __dadd_rn(__dmul_rn(__dadd_rn((double)kg, 0.5), ratio), -0.5);
+  src = fmin(fmax(src, 0.0), (double)(n_axis - 1));
+  int64_t i0 = 0, w1 = 0;
+  if (n_axis > 1) {
+    i0 = min((int64_t)floor(src), n_axis - 2);
+    w1 = (int64_t)floor(__dadd_rn(__dmul_rn(16384.0, __dadd_rn(src, -(double)i0)), 0.5));
+  }
+  int64_t sx = x, sy = y, sz = z, step;
+  if (AXIS == 0) { sx = i0; step = 1; }
+  else if (AXIS == 1) { sy = i0; step = nix; }
+  else { sz = i0 - in_z0; step = nix * niy; }
+  const int64_t si = (sz * niy + sy) * nix + sx;
+  const uint32_t v0 = __ldg(in + si);
+  const uint32_t v1 = n_axis > 1 ? __ldg(in + si + step) : v0;
+  out[t] = (uint16_t)((v0 * (uint32_t)(16384 - w1) + v1 * (uint32_t)w1 + 8192u) >> 14);
+}
+
+inline unsigned grid_for(int64_t n, int block) { return (unsigned)ceil_div(n, block); }
+
+}  // namespace
+
+size_t preprocess_ws(const snk_grid* g, const snk_params* p) {
+  (void)p;
+  return (size_t)g->n[0] * g->n[1] * g->nz_buf * sizeof(uint16_t) + 256;
+}
+
+int32_t preprocess_impl(const snk_grid* g, const snk_params* p, const uint16_t* d_in,
+                        uint16_t* d_smooth, uint16_t* d_gradmag, void* d_ws, size_t ws_bytes,
+                        cudaStream_t st) {
+  std::vector<int32_t> taps;
+  const int h = q14_taps(p->sigma, taps);
+  SNK_CUDA_CHECK(cudaMemcpyToSymbolAsync(c_taps, taps.data(), taps.size() * sizeof(int32_t), 0,
+                                         cudaMemcpyHostToDevice, st));
+  const int nx = (int)g->n[0], ny = (int)g->n[1], nz = (int)g->nz_buf;
+  const int64_t nvox = (int64_t)nx * ny * nz;
+  Carve cv(d_ws, ws_bytes);
+  uint16_t* tmp = cv.take<uint16_t>(nvox);
+  if (cv.overflow) return fail(SNK_CAPACITY, "workspace too small for preprocess");
+  const int64_t pairs = (int64_t)((nx + 1) / 2) * ny * nz;
+  const unsigned grid = grid_for(pairs, 256);
+  if (g->dim == 3) {
+    // x: in -> smooth, y: smooth -> tmp, z: tmp -> smooth
+    blur_pass_kernel<0><<<grid, 256, 0, st>>>(d_in, d_smooth, nx, ny, nz, h);
+    SNK_LAUNCH_CHECK("blur_pass_kernel<x>");
+    blur_pass_kernel<1><<<grid, 256, 0, st>>>(d_smooth, tmp, nx, ny, nz, h);
+    SNK_LAUNCH_CHECK("blur_pass_kernel<y>");
+    blur_pass_kernel<2><<<grid, 256, 0, st>>>(tmp, d_smooth, nx, ny, nz, h);
+    SNK_LAUNCH_CHECK("blur_pass_kernel<z>");
+  } else {
+    blur_pass_kernel<0><<<grid, 256, 0, st>>>(d_in, tmp, nx, ny, nz, h);
+    SNK_LAUNCH_CHECK("blur_pass_kernel<x>");
+    blur_pass_kernel<1><<<grid, 256, 0, st>>>(tmp, d_smooth, nx, ny, nz, h);
+    SNK_LAUNCH_CHECK("blur_pass_kernel<y>");
+  }
+  if (d_gradmag) {
+    if (g->dim == 3) gradmag_kernel<3><<<grid_for(nvox, 256), 256, 0, st>>>(d_smooth, d_gradmag, nx, ny, nz);
+    else gradmag_kernel<2><<<grid_for(nvox, 256), 256, 0, st>>>(d_smooth, d_gradmag, nx, ny, nz);
+    SNK_LAUNCH_CHECK("gradmag_kernel");
+  }
+  return SNK_OK;
+}
+
+size_t resample_ws(int32_t dim, const int64_t n_raw[3], const double spacing[3]) {
+  int64_t no[3];
+  if (snk_resample_dims(dim, n_raw, spacing, no) != SNK_OK) return 0;
+  // at most two intermediate volumes (x then y before z)
+  int64_t cur[3] = {n_raw[0], n_raw[1], n_raw[2]};
+  size_t total = 0;
+  int npass = 0;
+  for (int a = 0; a < dim; ++a) npass += (no[a] != n_raw[a]);
+  int done = 0;
+  for (int a = 0; a < dim; ++a) {
+    if (no[a] == n_raw[a]) continue;
+    cur[a] = no[a];
+    ++done;
+    if (done < npass) total += (size_t)cur[0] * cur[1] * cur[2] * sizeof(uint16_t) + 256;
+  }
+  return total;
+}
+
+int32_t resample_impl(int32_t dim, const int64_t n_raw[3], const double spacing[3], int64_t zr_lo,
+                      int64_t nzr, const uint16_t* d_raw, int64_t z_lo, int64_t nz_out,
+                      uint16_t* d_out, void* d_ws, size_t ws_bytes, cudaStream_t st) {
+  int64_t no[3];
+  SNK_TRY(snk_resample_dims(dim, n_raw, spacing, no));
+  double smin = spacing[0];
+  for (int a = 1; a < dim; ++a) smin = std::min(smin, spacing[a]);
+  if (zr_lo < 0 || nzr < 1 || zr_lo + nzr > n_raw[2] || z_lo < 0 || nz_out < 1 ||
+      z_lo + nz_out > no[2])
+    return fail(SNK_SHAPE, "resample plane ranges outside the volume");
+  const bool rz = no[2] != n_raw[2];
+  if (!rz && (zr_lo != z_lo || nzr < nz_out))
+    return fail(SNK_SHAPE, "z is not resampled: output planes must equal the raw planes");
+  if (rz) {
+    // the raw planes the output planes read
+    const double ratio = smin / spacing[2];
+    auto src_i0 = [&](int64_t k) {
+      double s = ((double)k + 0.5) * ratio - 0.5;
+      s = std::min(std::max(s, 0.0), (double)(n_raw[2] - 1));
+      return std::min((int64_t)std::floor(s), n_raw[2] - 2);
+    };
+    const int64_t lo = src_i0(z_lo), hi = src_i0(z_lo + nz_out - 1) + 1;
+    if (lo < zr_lo || hi > zr_lo + nzr - 1) return fail(SNK_SHAPE, "raw planes missing for resampling");
+  }
+  int npass = 0;
+  for (int a = 0; a < dim; ++a) npass += (no[a] != n_raw[a]);
+  // current buffer dims: x, y, planes; z-buffer origin
+  int64_t cx = n_raw[0], cy = n_raw[1], cz = rz ? nzr : nz_out, cz0 = rz ? zr_lo : z_lo;
+  const uint16_t* cur = d_raw + (rz ? 0 : (z_lo - zr_lo) * n_raw[0] * n_raw[1]);
+  if (npass == 0) {
+    SNK_CUDA_CHECK(cudaMemcpyAsync(d_out, cur, (size_t)cx * cy * nz_out * sizeof(uint16_t),
+                                   cudaMemcpyDeviceToDevice, st));
+    return SNK_OK;
+  }
+  Carve cv(d_ws, ws_bytes);
+  int done = 0;
+  for (int a = 0; a < dim; ++a) {
+    if (no[a] == n_raw[a]) continue;
+    ++done;
+    int64_t ox = cx, oy = cy, oz = cz, oz0 = cz0;
+    if (a == 0) ox = no[0];
+    if (a == 1) oy = no[1];
+    if (a == 2) { oz = nz_out; oz0 = z_lo; }
+    uint16_t* dst = done == npass ? d_out : cv.take<uint16_t>((size_t)ox * oy * oz);
+    if (cv.overflow) return fail(SNK_CAPACITY, "workspace too small for resample");
+    const double ratio = smin / spacing[a];
+    const int64_t total = ox * oy * oz;
+    const unsigned grid = grid_for(total, 256);
+    if (a == 0)
+      resample_kernel<0><<<grid, 256, 0, st>>>(cur, dst, cx, cy, oz, ox, oy, n_raw[0], ratio, cz0, oz0);
+    else if (a == 1)
+      resample_kernel<1><<<grid, 256, 0, st>>>(cur, dst, cx, cy, oz, ox, oy, n_raw[1], ratio, cz0, oz0);
+    else
+      resample_kernel<2><<<grid, 256, 0, st>>>(cur, dst, cx, cy, oz, ox, oy, n_raw[2], ratio, cz0, oz0);
+    SNK_LAUNCH_CHECK("resample_kernel");
+    cur = dst;
+    cx = ox; cy = oy; cz = oz; cz0 = oz0;
+  }
+  return SNK_OK;
+}
+
+}  // namespace snk

@@ -1,0 +1,414 @@
+"""GPU (libsnk, sm_100a) vs the fp64 CPU oracle, element by element.
+
+Contract: integer volume passes, seeds, culling and labels
+bit-exact; per-cell R and c within 1e-3 voxel and E within 1e-3 max(1, |E|)
+(fp32 vs fp64, same Philox samples); evolution bit-identical across
+warps-per-cell schedules.  Oracle inputs are always computed by the oracle
+from the raw synthetic volume — never taken from the CUDA path.
+"""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+
+TOL_RC = 1e-3
+
+
+@pytest.fixture(scope="module")
+def gpu():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_1804_06304_b200 import pipeline, snk
+    return torch, snk, pipeline
+
+
+def _t(torch, a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def _ora_params(cfg, **kw):
+    d = dict(r0=cfg.r0, n_samples=cfg.n_samples, max_iters=cfg.max_iters, dim=cfg.dim,
+             seed=cfg.philox_seed)
+    d.update(kw)
+    return oracle.Params(**d)
+
+
+def _assert_cells_close(g, o, ctx=""):
+    """GPU snk_cell records vs oracle cells (same order)."""
+    assert len(g) == len(o), ctx
+    dR = np.abs(g["R"].astype(np.float64) - o["R"])
+    dc = np.abs(g["c"].astype(np.float64) - o["c"]).max(axis=1)
+    dE = np.abs(g["energy"].astype(np.float64) - o["E"]) / np.maximum(1.0, np.abs(o["E"]))
+    assert np.array_equal(g["id"], o["id"]), ctx
+    assert np.array_equal(g["seed"].astype(np.float64), o["seed"]), ctx
+    bad = np.nonzero((dR > TOL_RC) | (dc > TOL_RC) | (dE > 1e-3))[0]
+    assert len(bad) == 0, (f"{ctx}: {len(bad)}/{len(g)} cells out of tolerance; worst dR={dR.max():.3g} "
+                           f"dc={dc.max():.3g} dE={dE.max():.3g}; first {bad[:5]}")
+    return dR.max(), dc.max(), dE.max()
+
+
+# ---------------------------------------------------------------- a1-a3 volume passes
+
+
+@pytest.mark.parametrize("dim,shape,sigma", [(3, (37, 45, 67), 1.0), (3, (2, 17, 9), 1.0),
+                                             (3, (21, 33, 70), 2.0), (3, (12, 13, 14), 0.0),
+                                             (2, (1, 129, 257), 1.0), (3, (9, 5, 300), 0.5)])
+def test_blur_gradmag_bitexact(gpu, dim, shape, sigma):
+    torch, snk, _ = gpu
+    rng = np.random.default_rng(hash(shape) % 2 ** 32)
+    vol = rng.integers(0, 65536, size=shape, dtype=np.uint16)
+    n = (shape[2], shape[1], shape[0])
+    g = snk.make_grid(dim, n)
+    p = snk.make_params(10.0, sigma=sigma)
+    d_in = _t(torch, vol)
+    sm, gm = torch.empty_like(d_in), torch.empty_like(d_in)
+    ws = torch.empty(snk.snk_workspace_bytes(g, p, 16), dtype=torch.uint8, device="cuda")
+    snk.snk_preprocess(g, p, d_in, sm, gm, ws)
+    torch.cuda.synchronize()
+    B = oracle.blur(vol, dim, sigma)
+    assert np.array_equal(sm.cpu().numpy(), B)
+    assert np.array_equal(gm.cpu().numpy(), oracle.gradmag(B, dim))
+
+
+@pytest.mark.parametrize("n,spacing", [((40, 36, 20), (1.0, 1.0, 2.0)), ((23, 17, 11), (3.0, 1.5, 1.0)),
+                                       ((16, 16, 9), (1.0, 1.0, 2.7))])
+def test_resample_bitexact(gpu, n, spacing):
+    torch, snk, _ = gpu
+    rng = np.random.default_rng(7)
+    raw = rng.integers(0, 65536, size=(n[2], n[1], n[0]), dtype=np.uint16)
+    no = snk.snk_resample_dims(3, n, spacing)
+    out = torch.empty((no[2], no[1], no[0]), dtype=torch.uint16, device="cuda")
+    ws = torch.empty(4 * no[0] * no[1] * no[2] * 2 + 4096, dtype=torch.uint8, device="cuda")
+    snk.snk_resample(3, n, spacing, 0, n[2], _t(torch, raw), 0, no[2], out, ws)
+    torch.cuda.synchronize()
+    assert np.array_equal(out.cpu().numpy(), oracle.resample(raw, spacing, 3))
+
+
+def test_resample_c3_full(gpu):
+    torch, snk, _ = gpu
+    cfg = synth.CONFIGS["C3"]
+    raw = synth.generate(cfg)
+    no = snk.snk_resample_dims(3, cfg.n, cfg.spacing)
+    out = torch.empty((no[2], no[1], no[0]), dtype=torch.uint16, device="cuda")
+    snk.snk_resample(3, cfg.n, cfg.spacing, 0, cfg.n[2], _t(torch, raw), 0, no[2], out, None)
+    torch.cuda.synchronize()
+    assert np.array_equal(out.cpu().numpy(), oracle.resample(raw, cfg.spacing, 3))
+
+
+# ---------------------------------------------------------------- a4 seeds
+
+
+def test_seeds_lattice_bitexact(gpu):
+    torch, snk, _ = gpu
+    for dim, n, r0 in [(3, (64, 64, 64), 10.0), (3, (100, 77, 51), 9.0), (2, (2048, 2048, 1), 25.0)]:
+        g = snk.make_grid(dim, n)
+        p = snk.make_params(r0, seed_mode=snk.SEED_LATTICE)
+        seeds = torch.empty((100_000, 3), dtype=torch.float32, device="cuda")
+        cnt, first = snk.snk_seeds(g, p, None, seeds, 100_000, None)
+        st, exp = oracle.seeds_lattice(n, dim, r0)
+        assert st == 0 and first == 0
+        assert np.array_equal(seeds[:cnt].cpu().numpy(), exp)
+    g = snk.make_grid(3, (20, 64, 64))
+    with pytest.raises(snk.SNKError) as e:
+        snk.snk_seeds(g, snk.make_params(10.0, seed_mode=snk.SEED_LATTICE), None, seeds, 10, None)
+    assert e.value.status == snk.EMPTY_DOMAIN
+
+
+def _gpu_smooth_seeds(torch, snk, pipeline, cfg, **over):
+    p = pipeline.params_for(cfg, **over)
+    P = pipeline.Pipeline(cfg.dim, cfg.n, p, spacing=cfg.spacing)
+    raw = synth.generate(cfg)
+    P.upload(raw)
+    P.preprocess()
+    P.seed()
+    torch.cuda.synchronize()
+    return P, raw, p
+
+
+@pytest.mark.parametrize("name", ["C1", "C2"])
+def test_seeds_maxima_bitexact_full(gpu, name):
+    torch, snk, pipeline = gpu
+    cfg = synth.CONFIGS[name]
+    P, raw, p = _gpu_smooth_seeds(torch, snk, pipeline, cfg, seed_mode=snk.SEED_MAXIMA)
+    vol = raw if cfg.dim == 3 else raw
+    B = oracle.blur(vol, cfg.dim, 1.0)
+    assert np.array_equal(P.smooth.cpu().numpy().reshape(B.shape), B)
+    exp = oracle.seeds_maxima(B, cfg.dim, cfg.window, cfg.seed_threshold)
+    assert P.n_seeds == len(exp) > 0
+    assert np.array_equal(P.seeds_np(), exp)
+
+
+def _crop(lo, hi):
+    return tuple(slice(int(lo[a]), int(hi[a]) + 1) for a in (2, 1, 0))
+
+
+def _oracle_smooth_crop(raw_iso, lo, hi, n):
+    """Oracle blur of raw[lo-4 .. hi+4] (clipped); returns (org, crop) whose voxels
+    lo..hi are exact (clamp-to-edge only acts at the true volume boundary)."""
+    m = 4
+    a = np.maximum(np.asarray(lo) - m, 0)
+    b = np.minimum(np.asarray(hi) + m, np.asarray(n) - 1)
+    B = oracle.blur(raw_iso[_crop(a, b)], 3, 1.0)
+    return a, B
+
+
+@pytest.mark.parametrize("name", ["C3", "C4"])
+def test_full_size_sampled_parity(gpu, name):
+    """Full BASELINE sizes in the bench's launch configuration (warp per cell):
+    sampled crops of the smoothed volume and the seed list are bit-exact; sampled
+    cells evolve within tolerance; the full-launch results for those cells are
+    bit-identical to a separate launch of just them."""
+    torch, snk, pipeline = gpu
+    cfg = synth.CONFIGS[name]
+    P, raw, p = _gpu_smooth_seeds(torch, snk, pipeline, cfg)
+    n = P.n_iso
+    raw_iso = oracle.resample(raw, cfg.spacing, 3) if P.resample else raw
+    if P.resample:   # resampled volume: sampled planes bit-exact
+        for z in [0, 1, n[2] // 2, n[2] - 1]:
+            assert np.array_equal(P.iso[z].cpu().numpy(), raw_iso[z])
+    rng = np.random.default_rng(12)
+    gseeds = P.seeds_np()
+    w = cfg.window
+    test_seeds = []
+    for k in range(3):
+        size = np.array([96, 96, 64])
+        lo = np.array([rng.integers(0, n[a] - size[a]) for a in range(3)])
+        hi = lo + size - 1
+        org, B = _oracle_smooth_crop(raw_iso, lo, hi, n)
+        gs = P.smooth[_crop(lo, hi)].cpu().numpy()
+        assert np.array_equal(gs, B[_crop(lo - org, hi - org)])
+        ilo, ihi = lo + w, hi - w
+        exp = oracle.seeds_maxima(B, 3, w, cfg.seed_threshold, org=org, n_global=n, lo=ilo, hi=ihi)
+        sel = np.all((gseeds >= ilo) & (gseeds <= ihi), axis=1)
+        assert np.array_equal(gseeds[sel], exp)
+        test_seeds.append(exp[rng.permutation(len(exp))[:8]])
+    seeds = np.concatenate(test_seeds).astype(np.float32)
+    ids = rng.permutation(1 << 20)[:len(seeds)].astype(np.int64) + 12345
+    # GPU: the bench's kernel configuration (warp per cell), explicit seeds and ids
+    p1 = pipeline.params_for(cfg, cta_warps=1)
+    cells = torch.empty(len(seeds) * 48, dtype=torch.uint8, device="cuda")
+    snk.snk_evolve(P.grid, p1, P.smooth, _t(torch, seeds), _t(torch, ids), 0, len(seeds), cells, None)
+    torch.cuda.synchronize()
+    g = pipeline.as_cells(cells, len(seeds))
+    # oracle: each cell on an oracle-smoothed crop covering everything it can reach
+    op = _ora_params(cfg)
+    reach = int(np.ceil(2 * cfg.r0 + 2 * cfg.r0 + 1.0 + 2))
+    outs = []
+    for s, i in zip(seeds, ids):
+        lo = np.maximum(np.floor(s).astype(int) - reach, 0)
+        hi = np.minimum(np.ceil(s).astype(int) + reach, np.asarray(n) - 1)
+        org, B = _oracle_smooth_crop(raw_iso, lo, hi, n)
+        outs.append(oracle.evolve(B, op, s[None], ids=np.array([i]), org=org, n_global=n)[0])
+    o = np.array(outs, dtype=oracle.CELL_DTYPE)
+    assert not np.any(o["flags"] & oracle.HALO)
+    _assert_cells_close(g, o, name)
+    # the full launch (all seeds, as bench.py times it) gives bit-identical cells
+    P.params = p1
+    P.evolve()
+    torch.cuda.synchronize()
+    allc = P.cells_np()
+    idx = [int(np.nonzero(np.all(gseeds == s, axis=1))[0][0]) for s in seeds]
+    full = allc[idx]
+    # same cells with the pipeline's ids in a separate small launch: identical bytes
+    snk.snk_evolve(P.grid, p1, P.smooth, _t(torch, seeds), _t(torch, full["id"].copy()), 0,
+                   len(seeds), cells, None)
+    torch.cuda.synchronize()
+    again = pipeline.as_cells(cells, len(seeds))
+    assert again.tobytes() == full.tobytes()
+
+
+# ---------------------------------------------------------------- a5-a6 evolution
+
+
+def test_evolve_c1_parity_and_schedules(gpu):
+    torch, snk, pipeline = gpu
+    cfg = synth.CONFIGS["C1"]
+    P, raw, p = _gpu_smooth_seeds(torch, snk, pipeline, cfg)
+    B = oracle.blur(raw, 3, 1.0)
+    st, oseeds = oracle.seeds_lattice(cfg.n, 3, cfg.r0)
+    assert np.array_equal(P.seeds_np(), oseeds)
+    ref = None
+    for W in (1, 2, 4, 8):
+        P.params = pipeline.params_for(cfg, cta_warps=W)
+        P.evolve()
+        torch.cuda.synchronize()
+        c = P.cells_np()
+        if ref is None:
+            ref = c
+        assert c.tobytes() == ref.tobytes(), f"cta_warps={W} differs"
+    o = oracle.evolve(B, _ora_params(cfg), oseeds, ids=np.arange(len(oseeds)))
+    _assert_cells_close(ref, o, "C1")
+    fmask = oracle.COLLAPSED | oracle.RMAX
+    assert np.array_equal(ref["flags"] & fmask, o["flags"] & fmask)
+
+
+@pytest.mark.parametrize("N", [32, 64, 256, 4096])
+def test_evolve_sample_counts(gpu, N):
+    """C5's N sweep: every per-thread block size (B = 1 .. 128) matches the oracle."""
+    torch, snk, pipeline = gpu
+    cfg = synth.CONFIGS["C1"].with_(n_samples=N, max_iters=60)
+    P, raw, p = _gpu_smooth_seeds(torch, snk, pipeline, cfg)
+    B = oracle.blur(raw, 3, 1.0)
+    for W in ((1, 8) if N >= 256 else (1,)):
+        P.params = pipeline.params_for(cfg, cta_warps=W)
+        P.evolve(n=16)
+        torch.cuda.synchronize()
+        g = P.cells_np()[:16]
+        o = oracle.evolve(B, _ora_params(cfg), P.seeds_np()[:16], ids=np.arange(16))
+        _assert_cells_close(g, o, f"N={N} W={W}")
+
+
+def test_evolve_2d_parity(gpu):
+    torch, snk, pipeline = gpu
+    cfg = synth.CONFIGS["C2"]
+    raw = synth.generate(cfg)[0]
+    sub = np.ascontiguousarray(raw[:300, :400])
+    c2 = cfg.with_(n=(400, 300, 1), max_iters=400)
+    p = pipeline.params_for(c2)
+    P = pipeline.Pipeline(2, c2.n, p)
+    P.upload(sub[None])
+    P.preprocess()
+    P.seed()
+    torch.cuda.synchronize()
+    B = oracle.blur(sub[None], 2, 1.0)
+    assert np.array_equal(P.smooth.cpu().numpy(), B)
+    exp = oracle.seeds_maxima(B, 2, c2.window, c2.seed_threshold)
+    assert np.array_equal(P.seeds_np(), exp) and len(exp) > 5
+    P.evolve()
+    torch.cuda.synchronize()
+    o = oracle.evolve(B, _ora_params(c2), exp, ids=np.arange(len(exp)))
+    _assert_cells_close(P.cells_np(), o, "2D")
+    assert np.all(P.cells_np()["c"][:, 2] == 0)
+
+
+def test_evolve_slab_buffer_bit_identical(gpu):
+    """T4 on one GPU: a z-slab buffer (with halo) gives the same cells as the whole volume."""
+    torch, snk, pipeline = gpu
+    cfg = synth.CONFIGS["C1"]
+    P, raw, p = _gpu_smooth_seeds(torch, snk, pipeline, cfg)
+    P.evolve()
+    torch.cuda.synchronize()
+    full = P.cells_np()
+    sel = np.nonzero(P.seeds_np()[:, 2] < 20)[0]
+    z1 = 20 + int(np.ceil(2 * cfg.r0 + 2 * cfg.r0 + 2 + 2))
+    g = snk.make_grid(3, (64, 64, 64), z_lo=0, nz_buf=z1, own=(0, 20))
+    cells = torch.empty(len(sel) * 48, dtype=torch.uint8, device="cuda")
+    snk.snk_evolve(g, p, P.smooth[:z1].contiguous(), P.seeds[sel].contiguous(),
+                   _t(torch, sel.astype(np.int64)), 0, len(sel), cells, None)
+    torch.cuda.synchronize()
+    got = pipeline.as_cells(cells, len(sel))
+    assert got.tobytes() == full[sel].tobytes()
+
+
+# ---------------------------------------------------------------- a7-a8, stage-isolated and end to end
+
+
+@pytest.mark.parametrize("name", ["C1", "C3"])
+def test_cull_and_label_stage_isolated(gpu, name):
+    torch, snk, pipeline = gpu
+    cfg = synth.CONFIGS[name]
+    P, raw, p = _gpu_smooth_seeds(torch, snk, pipeline, cfg)
+    P.evolve()
+    P.cull()
+    P.label()
+    torch.cuda.synchronize()
+    cells = P.cells_np()
+    keep = oracle.cull(cells["c"], cells["R"], cells["energy"], cells["flags"], cells["id"], cfg.dim,
+                       -3.0)
+    dets = P.dets_np()
+    assert dets.tobytes() == cells[keep].tobytes()
+    n = P.n_iso
+    if name == "C1":
+        lab = oracle.label(n, 3, dets["c"], dets["R"])
+        assert np.array_equal(P.labels.cpu().numpy(), lab)
+    else:
+        rng = np.random.default_rng(3)
+        pts = np.stack([rng.integers(0, n[a], 200_000) for a in range(3)], axis=1)
+        # plus every detection's centre neighbourhood (where labels are dense)
+        cen = np.round(dets["c"][:2000]).astype(np.int64)
+        pts = np.concatenate([pts, cen, np.clip(cen + 3, 0, np.asarray(n) - 1)])
+        exp = oracle.label_points(3, pts, dets["c"], dets["R"])
+        got = P.labels.cpu().numpy()[pts[:, 2], pts[:, 1], pts[:, 0]]
+        assert np.array_equal(got, exp)
+    assert (P.labels.cpu().numpy() > 0).any()
+
+
+def test_end_to_end_c1_and_host_call(gpu):
+    """C1 through the device pipeline and through snk_run (host buffers) against
+    the oracle's own end-to-end run."""
+    torch, snk, pipeline = gpu
+    cfg = synth.CONFIGS["C1"]
+    P, raw, p = _gpu_smooth_seeds(torch, snk, pipeline, cfg)
+    P.evolve()
+    P.cull()
+    P.label()
+    torch.cuda.synchronize()
+    res = oracle.run_pipeline(raw, _ora_params(cfg), seed_mode="lattice")
+    odets = res.cells[res.keep]
+    gdets = P.dets_np()
+    assert len(gdets) == len(odets) == 8
+    assert np.array_equal(gdets["id"], odets["id"])
+    assert np.abs(gdets["c"] - odets["c"]).max() < TOL_RC
+    assert np.array_equal(P.labels.cpu().numpy(), res.labels)
+    H = pipeline.HostRunner(3, cfg.n, p)
+    h_raw = torch.from_numpy(raw).pin_memory()
+    nd = H.run(h_raw)
+    assert nd == len(gdets)
+    assert H.dets_np(nd).tobytes() == gdets.tobytes()
+    assert np.array_equal(H.h_labels.numpy(), P.labels.cpu().numpy())
+
+
+def test_host_call_resampled_c3(gpu):
+    torch, snk, pipeline = gpu
+    cfg = synth.CONFIGS["C3"]
+    P, raw, p = _gpu_smooth_seeds(torch, snk, pipeline, cfg)
+    P.evolve()
+    P.cull()
+    P.label()
+    torch.cuda.synchronize()
+    H = pipeline.HostRunner(3, cfg.n, p, spacing=cfg.spacing, max_cells=P.max_cells)
+    nd = H.run(torch.from_numpy(raw).pin_memory())
+    assert nd == P.n_dets > 1000
+    assert H.dets_np(nd).tobytes() == P.dets_np().tobytes()
+    assert np.array_equal(H.h_labels.numpy(), P.labels.cpu().numpy())
+
+
+# ---------------------------------------------------------------- edge cases
+
+
+def test_edge_cases(gpu):
+    torch, snk, pipeline = gpu
+    # blank volume: no maxima above threshold -> 0 seeds, 0 detections, empty label map
+    cfg = synth.CONFIGS["C1"]
+    p = pipeline.params_for(cfg, seed_mode=snk.SEED_MAXIMA, seed_window=4)
+    P = pipeline.Pipeline(3, (40, 30, 20), p)
+    P.upload(np.full((20, 30, 40), 1000, np.uint16))
+    r = P.step()
+    assert (r.n_seeds, r.n_dets) == (0, 0)
+    assert int(P.labels.abs().sum()) == 0
+    # capacity: the required count is reported
+    P2 = pipeline.Pipeline(3, cfg.n, pipeline.params_for(cfg), max_cells=10)
+    P2.upload(synth.generate(cfg))
+    P2.preprocess()
+    with pytest.raises(snk.SNKError) as e:
+        P2.seed()
+    assert e.value.status == snk.CAPACITY
+    # minimal 3D volume 2x2x2 and n = 0 evolve are fine
+    g = snk.make_grid(3, (2, 2, 2))
+    pp = snk.make_params(0.5, r_min=0.1, seed_mode=snk.SEED_MAXIMA, seed_window=1, seed_threshold=0)
+    d = _t(torch, (np.arange(8, dtype=np.uint16) * 1000).reshape(2, 2, 2))
+    sm = torch.empty_like(d)
+    ws = torch.empty(snk.snk_workspace_bytes(g, pp, 8), dtype=torch.uint8, device="cuda")
+    snk.snk_preprocess(g, pp, d, sm, None, ws)
+    seeds = torch.empty((8, 3), dtype=torch.float32, device="cuda")
+    n, _ = snk.snk_seeds(g, pp, sm, seeds, 8, ws)
+    B = oracle.blur(d.cpu().numpy(), 3, 1.0)
+    assert np.array_equal(sm.cpu().numpy(), B)
+    assert np.array_equal(seeds[:n].cpu().numpy(), oracle.seeds_maxima(B, 3, 1, 0))
+    snk.snk_evolve(g, pp, sm, seeds, None, 0, 0, torch.empty(48, dtype=torch.uint8, device="cuda"), None)
+    assert snk.snk_cull(g, pp, torch.empty(48, dtype=torch.uint8, device="cuda"), 0,
+                        torch.empty(48, dtype=torch.uint8, device="cuda"), 1, ws) == 0

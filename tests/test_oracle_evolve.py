@@ -207,3 +207,26 @@ def test_c1_end_to_end(ora):
     for i, cc in enumerate(det["c"]):
         x, y, z = np.round(cc).astype(int)
         assert res.labels[z, y, x] == i + 1
+
+
+def test_crop_and_slab_equal_full_volume(ora):
+    """T4 on the CPU: evolving on a crop / z-slab holding every voxel a cell can
+    reach (leash + r_max + dR/2 + 1) gives bit-identical cells (§8(e))."""
+    vol = _ball_volume(48, (24.0, 22.0, 25.0), 8.0, ora=ora)
+    p = ora.Params(r0=9.0, n_samples=128, dim=3, max_iters=60, leash=3.0, r_max=11.0)
+    seeds = np.array([[23.5, 22.5, 24.0], [26.0, 20.0, 25.5]], np.float32)
+    full = ora.evolve(vol, p, seeds, ids=np.array([5, 9]))
+    reach = int(np.ceil(3.0 + 11.0 + 1.0 + 1.0))
+    lo = np.floor(seeds.min(0)).astype(int) - reach
+    hi = np.ceil(seeds.max(0)).astype(int) + reach
+    lo, hi = np.maximum(lo, 0), np.minimum(hi, 47)
+    crop = vol[lo[2]:hi[2] + 1, lo[1]:hi[1] + 1, lo[0]:hi[0] + 1]
+    got = ora.evolve(crop, p, seeds, ids=np.array([5, 9]), org=lo, n_global=(48, 48, 48))
+    assert got.tobytes() == full.tobytes()
+    slab = vol[lo[2]:hi[2] + 1]
+    got = ora.evolve(slab, p, seeds, ids=np.array([5, 9]), z_lo=int(lo[2]), n_global=(48, 48, 48))
+    assert got.tobytes() == full.tobytes()
+    assert not np.any(full["flags"] & ora.HALO)
+    # a crop that is too small is detected (HALO flag), never silently wrong
+    small = ora.evolve(vol[20:30], p, seeds, ids=np.array([5, 9]), z_lo=20, n_global=(48, 48, 48))
+    assert np.all(small["flags"] & ora.HALO)

@@ -175,3 +175,18 @@ def test_maxima_plateau_single_seed(ora):
     B[2:6, 2:6, 2:6] = 30000        # flat plateau: lowest linear index wins
     s = ora.seeds_maxima(B, 3, 4, 20000)
     assert s.tolist() == [[2.0, 2.0, 2.0]]
+
+
+def test_maxima_on_crop_equals_full(ora):
+    """A crop with a w-margin gives the full volume's seeds in its interior (§8(e))."""
+    rng = np.random.default_rng(11)
+    B = (rng.integers(0, 8, size=(20, 22, 24)) * 9000).astype(np.uint16)
+    w, thr = 2, 20000
+    full = ora.seeds_maxima(B, 3, w, thr)
+    org = np.array([3, 4, 5])
+    crop = B[5:17, 4:20, 3:21]                     # (z, y, x) = org + [0, nb)
+    n = (24, 22, 20)
+    lo, hi = org + w, org + np.array([18, 16, 12]) - 1 - w
+    got = ora.seeds_maxima(crop, 3, w, thr, org=org, n_global=n, lo=lo, hi=hi)
+    sel = np.all((full >= lo) & (full <= hi), axis=1)
+    assert np.array_equal(got, full[sel])
