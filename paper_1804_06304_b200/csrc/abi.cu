@@ -68,6 +68,7 @@ static int32_t validate_params(const snk_params* p, int dim) {
     return fail(SNK_CONFIG, "seed_window must be in [0, 64]");
   if (p->image_term != SNK_IMAGE_INTENSITY && p->image_term != SNK_IMAGE_GRADMAG)
     return fail(SNK_CONFIG, "bad image_term");
+  if (p->kernel_variant > 2) return fail(SNK_CONFIG, "kernel_variant must be 0, 1 or 2");
   (void)dim;
   return SNK_OK;
 }

@@ -1,21 +1,35 @@
 // evolve.cu — a5 + a6: batched Monte-Carlo evolution of independent 3D (2D)
 // snakuscules (Eqs. 11-14), the ★ hot loop.
 //
-// Mapping (B200): a cell is owned by W warps (W = 1: warp-per-cell; W > 1:
-// the paper's block-per-contour of §II-F) for all T+1 iterations; the
-// cell state stays in registers.  Each iteration draws a FIXED number N of
-// samples per cell (no divergence), 32 W threads x B = N/(32 W)
-// samples each.  Per sample: Philox4x32-10 -> (omega, t) -> 8 u16 gathers ->
-// trilinear -> S, S_r, S_R -> 5 leaf products.  Sums follow one canonical
-// pairwise tree over the N sample positions (in-thread binary counter ->
-// xor-butterfly over lanes -> pairwise over warps), so results are
-// bit-identical for every W.  This file is compiled with
-// -fmad=false: every FMA is written explicitly, so no schedule can contract
-// differently.
+// Two kernels compute the same function, bit for bit:
+//
+//  * evolve_brick_kernel (default when the volume meets TMA's alignment rules):
+//    one CTA of W warps per cell (the paper's block-per-contour).  The
+//    cell's neighbourhood — an S^d brick of the u16 image containing the
+//    sampled ball — lives in shared memory, loaded by one TMA box copy
+//    (cp.async.bulk.tensor) and re-centred only when the ball leaves it, so
+//    the per-sample gathers are shared-memory loads with immediate offsets
+//    and L2/HBM see ~one brick per cell instead of 8 scattered taps per
+//    sample.  A sample ball that cannot fit the brick falls back to global
+//    loads for that iteration (same arithmetic).
+//  * evolve_warp_kernel (generic fallback, any shape): W warps per cell,
+//    gathers straight from global memory (L1/L2).
+//
+// Each iteration draws a FIXED number N of samples per cell (no
+// divergence), 32 W threads x B = N/(32 W) each.  Per sample: Philox4x32-10
+// -> (omega, t) -> 8 u16 taps -> trilinear -> S, S_r, S_R -> 5 leaf products.
+// Sums follow one canonical pairwise tree over the N sample positions
+// (in-thread binary counter -> xor butterfly over lanes -> pairwise over
+// warps), so every W and both kernels give bit-identical results (S:314,
+// S:317).  Compiled with -fmad=false: every FMA is explicit.
 //
 // Reading of the update (G3/G4/G8): E = gamma A0,
 // dE/dc = -gamma A_c, dE/dR = gamma (A_R - (d/R) A0), gamma = (2R)^-d;
 // (c, R) -= clip((eps0/sqrt(n))/2 * grad, +-max_step); R clamp, leash, domain.
+#include <cudaTypedefs.h>
+
+#include <mutex>
+
 #include "common.cuh"
 
 namespace snk {
@@ -54,9 +68,11 @@ __device__ __forceinline__ Acc acc_add(const Acc& l, const Acc& r) {
 // Per cell-iteration constants.
 struct CellIt {
   float cx, cy, cz;
-  float rho_s;        // R + dR/2: radius of the sampled ball
-  float a;            // -(R - dR/2)/dR: offset of both ramp coordinates
-  uint32_t p0, p1, p3;   // Philox round-1 words that depend only on (n, id)
+  float rho_s;          // R + dR/2: radius of the sampled ball
+  float a;              // -(R - dR/2)/dR: offset of both ramp coordinates
+  uint32_t p0, p1, p3;  // Philox round-1 words that depend only on (n, id)
+  // brick: magic-offset origin (2^23 + b) per axis, as integers
+  uint32_t ob[3];
 };
 
 __device__ __forceinline__ float sqrt_approx(float x) {
@@ -83,15 +99,6 @@ __device__ __forceinline__ float u01(uint32_t x) {
 // u16 value v as a float offset by 2^23 (exact).
 __device__ __forceinline__ float mag(uint32_t v) { return __uint_as_float(kMagicBits | v); }
 
-// clamp k to [0, n-1], i0 = min(floor(k), n-2) (magic-number floor: FADD.RM),
-// returns the fraction k - i0 and the integer i0.
-__device__ __forceinline__ float split_axis(float k, float n1, float m2, int* i0) {
-  k = fminf(fmaxf(k, 0.0f), n1);
-  const float r = fminf(__fadd_rd(k, kMagic), m2);
-  *i0 = (int)(__float_as_uint(r) - kMagicBits);
-  return __fsub_rn(k, __fsub_rn(r, kMagic));
-}
-
 __device__ __forceinline__ float lerp_mag(float A, float Bm, float f) {
   // A, Bm are values + 2^23: a + f (b - a), with b - a = Bm - A exact and a = A - 2^23 exact
   return __fmaf_rn(f, __fsub_rn(Bm, A), __fsub_rn(A, kMagic));
@@ -101,63 +108,64 @@ __device__ __forceinline__ float lerp(float a, float b, float f) {
   return __fmaf_rn(f, __fsub_rn(b, a), a);
 }
 
-template <int D, bool SLAB>
-__device__ __forceinline__ Acc sample_leaf(const EvoParams& P, const CellIt& C, uint32_t j,
-                                           uint32_t& halo) {
-  // ---- Philox4x32-10, ctr = {j, n, id_lo, id_hi}, key = seed (G11)
-  uint32_t c0 = C.p0, c1 = C.p1, c2 = __umulhi(kM0, j) ^ C.p3, c3 = kM0 * j;
+// One axis of the d-linear lookup: clamp k to [0, n-1] (unless the caller
+// knows it is inside), i0 = min(floor(k), n-2) by the magic-number floor
+// (FADD.RM, no conversions), fraction k - i0.  Returns r = 2^23 + i0 (as bits).
+template <bool CLAMP>
+__device__ __forceinline__ float split_axis(float k, float n1, float m2, uint32_t* rbits) {
+  if (CLAMP) k = fminf(fmaxf(k, 0.0f), n1);
+  float r = __fadd_rd(k, kMagic);
+  if (CLAMP) r = fminf(r, m2);
+  *rbits = __float_as_uint(r);
+  return __fsub_rn(k, __fsub_rn(r, kMagic));
+}
+
+struct Draw {
+  float ox, oy, oz, t;
+};
+
+// Philox4x32-10 with ctr = {j, n, id_lo, id_hi}, key = seed (G11) -> the
+// sample's direction (Archimedes, G10) and distance.
+template <int D>
+__device__ __forceinline__ Draw draw(const EvoParams& P, const CellIt& C, uint32_t j) {
+  const uint64_t pj = (uint64_t)kM0 * j;
+  uint32_t c0 = C.p0, c1 = C.p1, c2 = (uint32_t)(pj >> 32) ^ C.p3, c3 = (uint32_t)pj;
 #pragma unroll
   for (int r = 1; r < 10; ++r) {
-    const uint32_t hi0 = __umulhi(kM0, c0), lo0 = kM0 * c0;
-    const uint32_t hi1 = __umulhi(kM1, c2), lo1 = kM1 * c2;
-    const uint32_t n0 = hi1 ^ c1 ^ P.rk0[r], n2 = hi0 ^ c3 ^ P.rk1[r];
-    c0 = n0; c1 = lo1; c2 = n2; c3 = lo0;
+    const uint64_t p0 = (uint64_t)kM0 * c0;
+    const uint64_t p1 = (uint64_t)kM1 * c2;
+    const uint32_t n0 = (uint32_t)(p1 >> 32) ^ c1 ^ P.rk0[r];
+    const uint32_t n2 = (uint32_t)(p0 >> 32) ^ c3 ^ P.rk1[r];
+    c0 = n0;
+    c1 = (uint32_t)p1;
+    c2 = n2;
+    c3 = (uint32_t)p0;
   }
   const float u0 = u01(c0), u1 = u01(c1), u2 = u01(c2);
-  // ---- direction (Archimedes, G10) and distance
   float sn, cs;
   __sincosf(__fmul_rn(6.2831853071795865f, u1), &sn, &cs);
-  float ox, oy, oz, t;
+  Draw d;
   if (D == 3) {
-    oz = __fmaf_rn(-2.0f, u0, 1.0f);
+    d.oz = __fmaf_rn(-2.0f, u0, 1.0f);
     const float st = __fmul_rn(2.0f, sqrt_approx(__fmaf_rn(-u0, u0, u0)));
-    ox = __fmul_rn(st, cs);
-    oy = __fmul_rn(st, sn);
-    t = __fmul_rn(C.rho_s, ex2_approx(__fmul_rn(lg2_approx(u2), 0.333333343f)));
+    d.ox = __fmul_rn(st, cs);
+    d.oy = __fmul_rn(st, sn);
+    d.t = __fmul_rn(C.rho_s, ex2_approx(__fmul_rn(lg2_approx(u2), 0.333333343f)));
   } else {
-    ox = cs;
-    oy = sn;
-    oz = 0.0f;
-    t = __fmul_rn(C.rho_s, sqrt_approx(u2));
+    d.ox = cs;
+    d.oy = sn;
+    d.oz = 0.0f;
+    d.t = __fmul_rn(C.rho_s, sqrt_approx(u2));
   }
-  // ---- position k = c + t omega, trilinear (bilinear) gather, clamp-to-edge (G17)
-  int ix, iy, iz = 0;
-  const float fx = split_axis(__fmaf_rn(t, ox, C.cx), P.fnx1, P.mx2, &ix);
-  const float fy = split_axis(__fmaf_rn(t, oy, C.cy), P.fny1, P.my2, &iy);
-  float fz = 0.0f;
-  if (D == 3) {
-    fz = split_axis(__fmaf_rn(t, oz, C.cz), P.fnz1, P.mz2, &iz);
-    if (SLAB) {
-      iz -= P.z_lo;
-      if (iz < 0 || iz > P.nz_buf - 2) { halo = 1u; iz = min(max(iz, 0), P.nz_buf - 2); }
-    }
-  }
-  const uint32_t nx = (uint32_t)P.nx;
-  const uint32_t base = ((uint32_t)iz * (uint32_t)P.ny + (uint32_t)iy) * nx + (uint32_t)ix;
-  const uint16_t* p = P.img + base;
-  const float v00 = lerp_mag(mag(__ldg(p)), mag(__ldg(p + 1)), fx);
-  const float v10 = lerp_mag(mag(__ldg(p + nx)), mag(__ldg(p + nx + 1)), fx);
-  float tri = lerp(v00, v10, fy);
-  if (D == 3) {
-    const uint32_t pl = nx * (uint32_t)P.ny;
-    const float v01 = lerp_mag(mag(__ldg(p + pl)), mag(__ldg(p + pl + 1)), fx);
-    const float v11 = lerp_mag(mag(__ldg(p + pl + nx)), mag(__ldg(p + pl + nx + 1)), fx);
-    tri = lerp(tri, lerp(v01, v11, fy), fz);
-  }
-  // ---- weight S(t; R) and partials (G1): tau_o = (t - (R - dR/2))/dR,
-  //      tau_i = (t - rho (R - dR/2))/(rho dR) = t/(rho dR) + a
-  const float uo = __saturatef(__fmaf_rn(t, P.inv_dR, C.a));
-  const float ui = __saturatef(__fmaf_rn(t, P.inv_rho_dR, C.a));
+  return d;
+}
+
+// S(t; R) and partials (G1) -> the five leaves for image value tri.
+__device__ __forceinline__ Acc leaves(const EvoParams& P, const CellIt& C, const Draw& d, float tri,
+                                      bool three) {
+  // tau_o = (t - (R - dR/2))/dR,  tau_i = (t - rho (R - dR/2))/(rho dR) = t/(rho dR) + a
+  const float uo = __saturatef(__fmaf_rn(d.t, P.inv_dR, C.a));
+  const float ui = __saturatef(__fmaf_rn(d.t, P.inv_rho_dR, C.a));
   const float s3o = __fmul_rn(__fmul_rn(uo, uo), __fmaf_rn(-2.0f, uo, 3.0f));
   const float s3i = __fmul_rn(__fmul_rn(ui, ui), __fmaf_rn(-2.0f, ui, 3.0f));
   const float d3o = __fmul_rn(6.0f, __fmaf_rn(-uo, uo, uo));
@@ -165,43 +173,102 @@ __device__ __forceinline__ Acc sample_leaf(const EvoParams& P, const CellIt& C, 
   const float S = __fsub_rn(__fmaf_rn(2.0f, s3i, -s3o), 1.0f);             // (1-s3o) - 2(1-s3i)
   const float Sr = __fmaf_rn(__fmul_rn(2.0f, P.inv_rho_dR), d3i, __fmul_rn(-P.inv_dR, d3o));
   const float SR = __fmul_rn(__fmaf_rn(-2.0f, d3i, d3o), P.inv_dR);
-  // ---- leaves (iscale and V/N are applied once per iteration)
   const float w = __fmul_rn(Sr, tri);
   Acc a;
   a.a0 = __fmul_rn(S, tri);
-  a.cx = __fmul_rn(w, ox);
-  a.cy = __fmul_rn(w, oy);
-  a.cz = D == 3 ? __fmul_rn(w, oz) : 0.0f;
+  a.cx = __fmul_rn(w, d.ox);
+  a.cy = __fmul_rn(w, d.oy);
+  a.cz = three ? __fmul_rn(w, d.oz) : 0.0f;
   a.aR = __fmul_rn(SR, tri);
   return a;
 }
 
-// Pairwise sum over CH consecutive samples (CH a power of two).
-template <int D, bool SLAB, int CH>
-__device__ __forceinline__ Acc chunk_sum(const EvoParams& P, const CellIt& C, uint32_t j0,
-                                         uint32_t& halo) {
-  if constexpr (CH == 1) {
-    return sample_leaf<D, SLAB>(P, C, j0, halo);
+// Gather modes
+enum { G_GLOBAL = 0, G_GLOBAL_SLAB = 1, G_BRICK_CLAMP = 2, G_BRICK_FAST = 3 };
+
+template <int D, int MODE, int S>
+__device__ __forceinline__ Acc sample_leaf(const EvoParams& P, const CellIt& C, uint32_t j,
+                                           const uint16_t* brick, uint32_t& halo) {
+  const Draw d = draw<D>(P, C, j);
+  constexpr bool CLAMP = MODE != G_BRICK_FAST;
+  uint32_t rx, ry, rz = kMagicBits;
+  const float fx = split_axis<CLAMP>(__fmaf_rn(d.t, d.ox, C.cx), P.fnx1, P.mx2, &rx);
+  const float fy = split_axis<CLAMP>(__fmaf_rn(d.t, d.oy, C.cy), P.fny1, P.my2, &ry);
+  float fz = 0.0f;
+  if (D == 3) fz = split_axis<CLAMP>(__fmaf_rn(d.t, d.oz, C.cz), P.fnz1, P.mz2, &rz);
+  float v000, v100, v010, v110, v001 = 0, v101 = 0, v011 = 0, v111 = 0;
+  if (MODE == G_BRICK_CLAMP || MODE == G_BRICK_FAST) {
+    // brick-local index; strides S and S^2 are immediates
+    const uint32_t lx = rx - C.ob[0], ly = ry - C.ob[1];
+    uint32_t li = ly * S + lx;
+    if (D == 3) li += (rz - C.ob[2]) * (S * S);
+    const uint16_t* p = brick + li;
+    v000 = mag(p[0]);
+    v100 = mag(p[1]);
+    v010 = mag(p[S]);
+    v110 = mag(p[S + 1]);
+    if (D == 3) {
+      v001 = mag(p[S * S]);
+      v101 = mag(p[S * S + 1]);
+      v011 = mag(p[S * S + S]);
+      v111 = mag(p[S * S + S + 1]);
+    }
   } else {
-    const Acc l = chunk_sum<D, SLAB, CH / 2>(P, C, j0, halo);
-    const Acc r = chunk_sum<D, SLAB, CH / 2>(P, C, j0 + CH / 2, halo);
+    int iz = (int)(rz - kMagicBits);
+    if (MODE == G_GLOBAL_SLAB && D == 3) {
+      iz -= P.z_lo;
+      if (iz < 0 || iz > P.nz_buf - 2) {
+        halo = 1u;
+        iz = min(max(iz, 0), P.nz_buf - 2);
+      }
+    }
+    const uint32_t nx = (uint32_t)P.nx;
+    const uint32_t base = ((uint32_t)iz * (uint32_t)P.ny + (ry - kMagicBits)) * nx + (rx - kMagicBits);
+    const uint16_t* p = P.img + base;
+    v000 = mag(__ldg(p));
+    v100 = mag(__ldg(p + 1));
+    v010 = mag(__ldg(p + nx));
+    v110 = mag(__ldg(p + nx + 1));
+    if (D == 3) {
+      const uint32_t pl = nx * (uint32_t)P.ny;
+      v001 = mag(__ldg(p + pl));
+      v101 = mag(__ldg(p + pl + 1));
+      v011 = mag(__ldg(p + pl + nx));
+      v111 = mag(__ldg(p + pl + nx + 1));
+    }
+  }
+  // trilinear: x, then y, then z (G17)
+  float tri = lerp(lerp_mag(v000, v100, fx), lerp_mag(v010, v110, fx), fy);
+  if (D == 3) tri = lerp(tri, lerp(lerp_mag(v001, v101, fx), lerp_mag(v011, v111, fx), fy), fz);
+  return leaves(P, C, d, tri, D == 3);
+}
+
+// Pairwise sum over CH consecutive samples (CH a power of two).
+template <int D, int MODE, int S, int CH>
+__device__ __forceinline__ Acc chunk_sum(const EvoParams& P, const CellIt& C, uint32_t j0,
+                                         const uint16_t* brick, uint32_t& halo) {
+  if constexpr (CH == 1) {
+    return sample_leaf<D, MODE, S>(P, C, j0, brick, halo);
+  } else {
+    const Acc l = chunk_sum<D, MODE, S, CH / 2>(P, C, j0, brick, halo);
+    const Acc r = chunk_sum<D, MODE, S, CH / 2>(P, C, j0 + CH / 2, brick, halo);
     return acc_add(l, r);
   }
 }
 
 // Pairwise sum over CH << L consecutive samples: 2^L chunks combined by a
 // binary counter (stack of L partial sums) = a perfect pairwise tree.
-template <int D, bool SLAB, int CH, int L>
+template <int D, int MODE, int S, int CH, int L>
 __device__ __forceinline__ Acc lane_sum(const EvoParams& P, const CellIt& C, uint32_t j0,
-                                        uint32_t& halo) {
+                                        const uint16_t* brick, uint32_t& halo) {
   if constexpr (L == 0) {
-    return chunk_sum<D, SLAB, CH>(P, C, j0, halo);
+    return chunk_sum<D, MODE, S, CH>(P, C, j0, brick, halo);
   } else {
     Acc stk[L];
     Acc res{};
 #pragma unroll 1
     for (int i = 0; i < (1 << L); ++i) {
-      Acc x = chunk_sum<D, SLAB, CH>(P, C, j0 + (uint32_t)(i * CH), halo);
+      Acc x = chunk_sum<D, MODE, S, CH>(P, C, j0 + (uint32_t)(i * CH), brick, halo);
       bool carry = true;
 #pragma unroll
       for (int l = 0; l < L; ++l) {
@@ -216,169 +283,391 @@ __device__ __forceinline__ Acc lane_sum(const EvoParams& P, const CellIt& C, uin
   }
 }
 
+__device__ __forceinline__ Acc warp_butterfly(Acc s) {
+  // (l, l^1), (l, l^2), ... = pairwise over consecutive lane blocks
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    Acc q;
+    q.a0 = __shfl_xor_sync(0xffffffffu, s.a0, o);
+    q.cx = __shfl_xor_sync(0xffffffffu, s.cx, o);
+    q.cy = __shfl_xor_sync(0xffffffffu, s.cy, o);
+    q.cz = __shfl_xor_sync(0xffffffffu, s.cz, o);
+    q.aR = __shfl_xor_sync(0xffffffffu, s.aR, o);
+    s = acc_add(s, q);
+  }
+  return s;
+}
+
+template <int W>
+__device__ __forceinline__ Acc warp_tree(const Acc* v) {
+  Acc t[W];
+#pragma unroll
+  for (int w = 0; w < W; ++w) t[w] = v[w];
+#pragma unroll
+  for (int span = 1; span < W; span <<= 1)
+#pragma unroll
+    for (int w = 0; w + span < W; w += 2 * span) t[w] = acc_add(t[w], t[w + span]);
+  return t[0];
+}
+
 __device__ __forceinline__ float clampf(float v, float lo, float hi) { return fminf(fmaxf(v, lo), hi); }
 
+// The per-cell state and the iteration update, shared by both kernels.
+struct CellState {
+  float sx, sy, sz;     // seed
+  float cx, cy, cz, R, E;
+  uint32_t flags;
+  int64_t id;
+  uint32_t id_lo, id_hi;
+};
+
+__device__ __forceinline__ void cell_begin(const EvoParams& P, int64_t cell, int D, CellState& s) {
+  s.sx = P.seeds[3 * cell + 0];
+  s.sy = P.seeds[3 * cell + 1];
+  s.sz = D == 3 ? P.seeds[3 * cell + 2] : 0.0f;
+  s.id = P.ids ? P.ids[cell] : P.id_base + cell;
+  s.id_lo = (uint32_t)((uint64_t)s.id & 0xffffffffu);
+  s.id_hi = (uint32_t)((uint64_t)s.id >> 32);
+  s.cx = s.sx; s.cy = s.sy; s.cz = s.sz;
+  s.R = P.r0;
+  s.E = 0.0f;
+  s.flags = 0;
+}
+
+__device__ __forceinline__ CellIt cell_iter(const EvoParams& P, const CellState& s, int it) {
+  CellIt C;
+  C.cx = s.cx; C.cy = s.cy; C.cz = s.cz;
+  C.rho_s = __fadd_rn(s.R, P.half_dR);
+  C.a = __fmul_rn(-__fsub_rn(s.R, P.half_dR), P.inv_dR);
+  // Philox round 1: the words that come from c1 = n, c2 = id_lo, c3 = id_hi
+  const uint64_t p1 = (uint64_t)kM1 * s.id_lo;
+  C.p0 = (uint32_t)(p1 >> 32) ^ (uint32_t)it ^ P.rk0[0];
+  C.p1 = (uint32_t)p1;
+  C.p3 = s.id_hi ^ P.rk1[0];
+  C.ob[0] = C.ob[1] = C.ob[2] = kMagicBits;
+  return C;
+}
+
+// Energy, gradient and the clipped descent step; returns true after E_final.
+template <int D>
+__device__ __forceinline__ bool cell_update(const EvoParams& P, CellState& s, const CellIt& C,
+                                            const Acc& sum, int it) {
+  const float rs = C.rho_s;
+  const float vol = D == 3 ? __fmul_rn(__fmul_rn(rs, rs), rs) : __fmul_rn(rs, rs);
+  const float scale = __fmul_rn(P.vscale, vol);
+  const float A0 = __fmul_rn(sum.a0, scale);
+  const float twoR = __fmul_rn(2.0f, s.R);
+  const float gden = D == 3 ? __fmul_rn(__fmul_rn(twoR, twoR), twoR) : __fmul_rn(twoR, twoR);
+  const float gamma = __fdiv_rn(1.0f, gden);
+  const float gs = __fmul_rn(gamma, scale);
+  s.E = __fmul_rn(gamma, A0);
+  if (it == P.T + 1) return true;
+  const float gcx = -__fmul_rn(gs, sum.cx), gcy = -__fmul_rn(gs, sum.cy), gcz = -__fmul_rn(gs, sum.cz);
+  const float gR = __fmul_rn(gamma, __fsub_rn(__fmul_rn(sum.aR, scale),
+                                              __fmul_rn(__fdiv_rn(D == 3 ? 3.0f : 2.0f, s.R), A0)));
+  // step eps_n / 2 with eps_n = eps0 / sqrt(n), clipped (G8)
+  const float h = __fmul_rn(0.5f, __fdiv_rn(P.eps0, __fsqrt_rn((float)it)));
+  const float dcx = clampf(-__fmul_rn(h, gcx), -P.max_step, P.max_step);
+  const float dcy = clampf(-__fmul_rn(h, gcy), -P.max_step, P.max_step);
+  const float dcz = D == 3 ? clampf(-__fmul_rn(h, gcz), -P.max_step, P.max_step) : 0.0f;
+  const float dR = clampf(-__fmul_rn(h, gR), -P.max_step, P.max_step);
+  const float ox = s.cx, oy = s.cy, oz = s.cz, oR = s.R;
+  float cx = __fadd_rn(s.cx, dcx), cy = __fadd_rn(s.cy, dcy), cz = __fadd_rn(s.cz, dcz);
+  const float R = clampf(__fadd_rn(s.R, dR), P.r_min, P.r_max);
+  // leash
+  const float lx = clampf(cx, __fsub_rn(s.sx, P.leash), __fadd_rn(s.sx, P.leash));
+  const float ly = clampf(cy, __fsub_rn(s.sy, P.leash), __fadd_rn(s.sy, P.leash));
+  const float lz = clampf(cz, __fsub_rn(s.sz, P.leash), __fadd_rn(s.sz, P.leash));
+  const bool leashed = (lx != cx) || (ly != cy) || (lz != cz);
+  cx = lx; cy = ly; cz = lz;
+  // domain: c_a in [m, n_a - 1 - m], m = R + dR/2, or the axis centre
+  const float m = __fadd_rn(R, P.half_dR), m2 = __fmul_rn(2.0f, m);
+  const float dx = P.fnx1 < m2 ? __fmul_rn(0.5f, P.fnx1) : clampf(cx, m, __fsub_rn(P.fnx1, m));
+  const float dy = P.fny1 < m2 ? __fmul_rn(0.5f, P.fny1) : clampf(cy, m, __fsub_rn(P.fny1, m));
+  float dz = cz;
+  if (D == 3) dz = P.fnz1 < m2 ? __fmul_rn(0.5f, P.fnz1) : clampf(cz, m, __fsub_rn(P.fnz1, m));
+  const bool domained = (dx != cx) || (dy != cy) || (dz != cz);
+  s.cx = dx; s.cy = dy; s.cz = dz;
+  s.R = R;
+  if (it == P.T) {
+    float mv = fabsf(__fsub_rn(R, oR));
+    mv = fmaxf(mv, fabsf(__fsub_rn(s.cx, ox)));
+    mv = fmaxf(mv, fabsf(__fsub_rn(s.cy, oy)));
+    mv = fmaxf(mv, fabsf(__fsub_rn(s.cz, oz)));
+    if (mv < P.conv_tol) s.flags |= SNK_F_CONVERGED;
+    if (leashed) s.flags |= SNK_F_LEASHED;
+    if (domained) s.flags |= SNK_F_DOMAIN;
+  }
+  return false;
+}
+
+__device__ __forceinline__ void cell_finish(const EvoParams& P, CellState& s, int64_t cell) {
+  if (s.R <= P.r_min) s.flags |= SNK_F_COLLAPSED;
+  if (s.R >= P.r_max) s.flags |= SNK_F_RMAX;
+  snk_cell o;
+  o.c[0] = s.cx; o.c[1] = s.cy; o.c[2] = s.cz;
+  o.R = s.R;
+  o.seed[0] = s.sx; o.seed[1] = s.sy; o.seed[2] = s.sz;
+  o.energy = s.E;
+  o.flags = s.flags;
+  o.iters = P.T;
+  o.id = s.id;
+  P.out[cell] = o;
+}
+
+// =========================================================================
+// Generic kernel: W warps per cell, gathers from global memory.
 template <int D, int W, bool SLAB, int CH, int L>
 __global__ void __launch_bounds__(W >= 4 ? 32 * W : 128)
-    evolve_kernel(const __grid_constant__ EvoParams P) {
+    evolve_warp_kernel(const __grid_constant__ EvoParams P) {
   constexpr int CPB = W >= 4 ? 1 : 4 / W;   // cells per block
   constexpr int B = CH << L;                // samples per thread per iteration
+  constexpr int MODE = SLAB ? G_GLOBAL_SLAB : G_GLOBAL;
   __shared__ Acc xch[2][CPB][W];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int slot = warp / W, wsub = warp % W;
   const int64_t cell = (int64_t)blockIdx.x * CPB + slot;
   if (cell >= P.n) return;   // uniform per cell group (named barriers below)
-  const float sx = P.seeds[3 * cell + 0], sy = P.seeds[3 * cell + 1];
-  const float sz = D == 3 ? P.seeds[3 * cell + 2] : 0.0f;
-  const int64_t id = P.ids ? P.ids[cell] : P.id_base + cell;
-  const uint32_t id_lo = (uint32_t)((uint64_t)id & 0xffffffffu), id_hi = (uint32_t)((uint64_t)id >> 32);
-  float cx = sx, cy = sy, cz = sz, R = P.r0, E = 0.0f;
-  uint32_t flags = 0, halo = 0;
+  CellState s;
+  cell_begin(P, cell, D, s);
+  uint32_t halo = 0;
   const uint32_t j0 = (uint32_t)((wsub * 32 + lane) * B);
-  const float inv_d = D == 3 ? 3.0f : 2.0f;
   for (int it = 1; it <= P.T + 1; ++it) {
-    CellIt C;
-    C.cx = cx; C.cy = cy; C.cz = cz;
-    C.rho_s = __fadd_rn(R, P.half_dR);
-    C.a = __fmul_rn(-__fsub_rn(R, P.half_dR), P.inv_dR);
-    // Philox round 1: words from c1 = n, c2 = id_lo, c3 = id_hi
-    C.p0 = __umulhi(kM1, id_lo) ^ (uint32_t)it ^ P.rk0[0];
-    C.p1 = kM1 * id_lo;
-    C.p3 = id_hi ^ P.rk1[0];
-    Acc s = lane_sum<D, SLAB, CH, L>(P, C, j0, halo);
-    // butterfly over lanes: (l, l^1), (l, l^2), ... = pairwise over lane blocks
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      Acc q;
-      q.a0 = __shfl_xor_sync(0xffffffffu, s.a0, o);
-      q.cx = __shfl_xor_sync(0xffffffffu, s.cx, o);
-      q.cy = __shfl_xor_sync(0xffffffffu, s.cy, o);
-      q.cz = __shfl_xor_sync(0xffffffffu, s.cz, o);
-      q.aR = __shfl_xor_sync(0xffffffffu, s.aR, o);
-      s = acc_add(s, q);
-    }
+    const CellIt C = cell_iter(P, s, it);
+    Acc sum = warp_butterfly(lane_sum<D, MODE, 1, CH, L>(P, C, j0, nullptr, halo));
     if constexpr (W > 1) {
-      if (lane == 0) xch[it & 1][slot][wsub] = s;
+      if (lane == 0) xch[it & 1][slot][wsub] = sum;
       asm volatile("bar.sync %0, %1;" ::"r"(1 + slot), "r"(32 * W) : "memory");
-      Acc v[W];
-#pragma unroll
-      for (int w = 0; w < W; ++w) v[w] = xch[it & 1][slot][w];
-#pragma unroll
-      for (int span = 1; span < W; span <<= 1)
-#pragma unroll
-        for (int w = 0; w + span < W; w += 2 * span) v[w] = acc_add(v[w], v[w + span]);
-      s = v[0];
+      sum = warp_tree<W>(xch[it & 1][slot]);
     }
-    // ---- energy and gradient (Eqs. 5-10 in (c, R) form; gamma = (2R)^-d, G3)
-    const float rs = C.rho_s;
-    const float vol = D == 3 ? __fmul_rn(__fmul_rn(rs, rs), rs) : __fmul_rn(rs, rs);
-    const float scale = __fmul_rn(P.vscale, vol);
-    const float A0 = __fmul_rn(s.a0, scale);
-    const float twoR = __fmul_rn(2.0f, R);
-    const float gden = D == 3 ? __fmul_rn(__fmul_rn(twoR, twoR), twoR) : __fmul_rn(twoR, twoR);
-    const float gamma = __fdiv_rn(1.0f, gden);
-    const float gs = __fmul_rn(gamma, scale);
-    E = __fmul_rn(gamma, A0);
-    if (it == P.T + 1) break;
-    const float gcx = -__fmul_rn(gs, s.cx), gcy = -__fmul_rn(gs, s.cy), gcz = -__fmul_rn(gs, s.cz);
-    const float gR = __fmul_rn(gamma, __fsub_rn(__fmul_rn(s.aR, scale), __fmul_rn(__fdiv_rn(inv_d, R), A0)));
-    // ---- step eps_n / 2 with eps_n = eps0 / sqrt(n), clipped (G8)
-    const float h = __fmul_rn(0.5f, __fdiv_rn(P.eps0, __fsqrt_rn((float)it)));
-    const float dcx = clampf(-__fmul_rn(h, gcx), -P.max_step, P.max_step);
-    const float dcy = clampf(-__fmul_rn(h, gcy), -P.max_step, P.max_step);
-    const float dcz = D == 3 ? clampf(-__fmul_rn(h, gcz), -P.max_step, P.max_step) : 0.0f;
-    const float dR = clampf(-__fmul_rn(h, gR), -P.max_step, P.max_step);
-    const float ox = cx, oy = cy, oz = cz, oR = R;
-    cx = __fadd_rn(cx, dcx);
-    cy = __fadd_rn(cy, dcy);
-    cz = __fadd_rn(cz, dcz);
-    R = clampf(__fadd_rn(R, dR), P.r_min, P.r_max);
-    // leash
-    const float lx = clampf(cx, __fsub_rn(sx, P.leash), __fadd_rn(sx, P.leash));
-    const float ly = clampf(cy, __fsub_rn(sy, P.leash), __fadd_rn(sy, P.leash));
-    const float lz = clampf(cz, __fsub_rn(sz, P.leash), __fadd_rn(sz, P.leash));
-    const bool leashed = (lx != cx) || (ly != cy) || (lz != cz);
-    cx = lx; cy = ly; cz = lz;
-    // domain: c_a in [m, n_a - 1 - m], m = R + dR/2, or the axis centre
-    const float m = __fadd_rn(R, P.half_dR), m2 = __fmul_rn(2.0f, m);
-    const float dx = P.fnx1 < m2 ? __fmul_rn(0.5f, P.fnx1) : clampf(cx, m, __fsub_rn(P.fnx1, m));
-    const float dy = P.fny1 < m2 ? __fmul_rn(0.5f, P.fny1) : clampf(cy, m, __fsub_rn(P.fny1, m));
-    float dz = cz;
-    if (D == 3) dz = P.fnz1 < m2 ? __fmul_rn(0.5f, P.fnz1) : clampf(cz, m, __fsub_rn(P.fnz1, m));
-    const bool domained = (dx != cx) || (dy != cy) || (dz != cz);
-    cx = dx; cy = dy; cz = dz;
-    if (it == P.T) {
-      float mv = fabsf(__fsub_rn(R, oR));
-      mv = fmaxf(mv, fabsf(__fsub_rn(cx, ox)));
-      mv = fmaxf(mv, fabsf(__fsub_rn(cy, oy)));
-      mv = fmaxf(mv, fabsf(__fsub_rn(cz, oz)));
-      if (mv < P.conv_tol) flags |= SNK_F_CONVERGED;
-      if (leashed) flags |= SNK_F_LEASHED;
-      if (domained) flags |= SNK_F_DOMAIN;
-    }
+    if (cell_update<D>(P, s, C, sum, it)) break;
   }
-  if (R <= P.r_min) flags |= SNK_F_COLLAPSED;
-  if (R >= P.r_max) flags |= SNK_F_RMAX;
   if (SLAB) {
-    if (__any_sync(0xffffffffu, halo != 0)) flags |= SNK_F_HALO;
+    if (__any_sync(0xffffffffu, halo != 0)) s.flags |= SNK_F_HALO;
     if constexpr (W > 1) {
-      // combine the halo flag of every warp of the cell
       __shared__ uint32_t hf[CPB];
       if (wsub == 0 && lane == 0) hf[slot] = 0;
       asm volatile("bar.sync %0, %1;" ::"r"(1 + slot), "r"(32 * W) : "memory");
-      if (lane == 0 && (flags & SNK_F_HALO)) atomicOr(&hf[slot], SNK_F_HALO);
+      if (lane == 0 && (s.flags & SNK_F_HALO)) atomicOr(&hf[slot], SNK_F_HALO);
       asm volatile("bar.sync %0, %1;" ::"r"(1 + slot), "r"(32 * W) : "memory");
-      flags |= hf[slot];
+      s.flags |= hf[slot];
     }
   }
-  if (wsub == 0 && lane == 0) {
-    snk_cell o;
-    o.c[0] = cx; o.c[1] = cy; o.c[2] = cz;
-    o.R = R;
-    o.seed[0] = sx; o.seed[1] = sy; o.seed[2] = sz;
-    o.energy = E;
-    o.flags = flags;
-    o.iters = P.T;
-    o.id = id;
-    P.out[cell] = o;
+  if (wsub == 0 && lane == 0) cell_finish(P, s, cell);
+}
+
+// =========================================================================
+// Brick kernel: one CTA (W warps) per cell, S^d u16 brick in shared memory
+// loaded by TMA.
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+
+template <int D>
+__device__ __forceinline__ void tma_load_brick(uint16_t* dst, const CUtensorMap* map, int x, int y,
+                                               int z, uint64_t* bar) {
+  if (D == 3) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes "
+        "[%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
+        "l"(map), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
+        : "memory");
+  } else {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes "
+        "[%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(dst)),
+        "l"(map), "r"(x), "r"(y), "r"(smem_u32(bar))
+        : "memory");
   }
 }
 
+template <int D, int W, int S, bool SLAB, int CH, int L>
+__global__ void __launch_bounds__(32 * W)
+    evolve_brick_kernel(const __grid_constant__ EvoParams P, const __grid_constant__ CUtensorMap map) {
+  constexpr int B = CH << L;
+  constexpr uint32_t kBrickBytes = (D == 3 ? S * S * S : S * S) * 2;
+  extern __shared__ __align__(128) uint16_t brick[];
+  __shared__ Acc xch[2][W];
+  __shared__ __align__(8) uint64_t bar;
+  const int lane = threadIdx.x & 31, wsub = threadIdx.x >> 5;
+  const int64_t cell = blockIdx.x;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  CellState s;
+  cell_begin(P, cell, D, s);
+  uint32_t halo = 0, phase = 0;
+  int b[3] = {-(1 << 28), -(1 << 28), -(1 << 28)};   // brick origin (global voxels); none yet
+  const int n[3] = {P.nx, P.ny, P.nz};
+  // z range the brick may cover: the slab buffer
+  const int zlo = SLAB ? P.z_lo : 0, zhi = SLAB ? P.z_lo + P.nz_buf - 1 : P.nz - 1;
+  const uint32_t j0 = (uint32_t)((wsub * 32 + lane) * B);
+  for (int it = 1; it <= P.T + 1; ++it) {
+    CellIt C = cell_iter(P, s, it);
+    // bounding box of the sampled ball, with a margin for the fp32 rounding of t and k
+    const float ext = __fmaf_rn(C.rho_s, 1.0001f, 0.01f);
+    const float c[3] = {s.cx, s.cy, s.cz};
+    bool interior = true, fits = true, inside = true;
+    int lo[3], hi[3];
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+      lo[a] = (int)floorf(__fsub_rn(c[a], ext));
+      hi[a] = (int)floorf(__fadd_rn(c[a], ext)) + 1;
+      interior &= lo[a] >= 0 && hi[a] <= n[a] - 1;
+      lo[a] = max(lo[a], 0);
+      hi[a] = min(hi[a], n[a] - 1);
+      fits &= hi[a] - lo[a] + 1 <= S;
+      inside &= lo[a] >= b[a] && hi[a] <= b[a] + S - 1;
+    }
+    if (D == 3 && SLAB) fits &= lo[2] >= zlo && hi[2] <= zhi;
+    if (!inside && fits) {
+      // re-centre: the ball's box in the middle of the brick, clipped to the buffer
+#pragma unroll
+      for (int a = 0; a < D; ++a) {
+        const int amin = (a == 2) ? zlo : 0, amax = (a == 2) ? zhi : n[a] - 1;
+        int o = lo[a] - (S - (hi[a] - lo[a] + 1)) / 2;
+        o = min(o, amax + 1 - S);
+        o = max(o, amin);
+        b[a] = o;
+      }
+      // all reads of the previous brick finished at the last iteration's barrier
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        mbar_expect_tx(&bar, kBrickBytes);
+        tma_load_brick<D>(brick, &map, b[0], b[1], D == 3 ? b[2] - zlo : 0, &bar);
+      }
+      mbar_wait(&bar, phase);
+      phase ^= 1u;
+      inside = true;
+    }
+    Acc part;
+    if (inside) {
+#pragma unroll
+      for (int a = 0; a < D; ++a) C.ob[a] = kMagicBits + (uint32_t)b[a];
+      if (interior) part = lane_sum<D, G_BRICK_FAST, S, CH, L>(P, C, j0, brick, halo);
+      else part = lane_sum<D, G_BRICK_CLAMP, S, CH, L>(P, C, j0, brick, halo);
+    } else {
+      part = lane_sum<D, SLAB ? G_GLOBAL_SLAB : G_GLOBAL, S, CH, L>(P, C, j0, brick, halo);
+    }
+    Acc sum = warp_butterfly(part);
+    if constexpr (W > 1) {
+      if (lane == 0) xch[it & 1][wsub] = sum;
+      __syncthreads();
+      sum = warp_tree<W>(xch[it & 1]);
+    }
+    if (cell_update<D>(P, s, C, sum, it)) break;
+  }
+  if (SLAB && __syncthreads_or(halo != 0)) s.flags |= SNK_F_HALO;
+  if (threadIdx.x == 0) cell_finish(P, s, cell);
+}
+
+// ------------------------------------------------------------------ launching
 template <int D, int W, bool SLAB, int CH, int L>
-int32_t launch_one(const EvoParams& P, cudaStream_t st) {
+int32_t launch_warp(const EvoParams& P, cudaStream_t st) {
   constexpr int CPB = W >= 4 ? 1 : 4 / W;
-  const unsigned grid = (unsigned)ceil_div(P.n, CPB);
-  const unsigned block = 32 * W * CPB;
-  evolve_kernel<D, W, SLAB, CH, L><<<grid, block, 0, st>>>(P);
-  SNK_LAUNCH_CHECK("evolve_kernel");
+  evolve_warp_kernel<D, W, SLAB, CH, L><<<(unsigned)ceil_div(P.n, CPB), 32 * W * CPB, 0, st>>>(P);
+  SNK_LAUNCH_CHECK("evolve_warp_kernel");
   return SNK_OK;
 }
 
-// B samples per thread: B = 1, 2 (one chunk) or 4 << L (chunks of 4, L <= 5).
-template <int D, int W, bool SLAB>
-int32_t launch_B(const EvoParams& P, int B, cudaStream_t st) {
-  switch (B) {
-    case 1: return launch_one<D, W, SLAB, 1, 0>(P, st);
-    case 2: return launch_one<D, W, SLAB, 2, 0>(P, st);
-    case 4: return launch_one<D, W, SLAB, 4, 0>(P, st);
-    case 8: return launch_one<D, W, SLAB, 4, 1>(P, st);
-    case 16: return launch_one<D, W, SLAB, 4, 2>(P, st);
-    case 32: return launch_one<D, W, SLAB, 4, 3>(P, st);
-    case 64: return launch_one<D, W, SLAB, 4, 4>(P, st);
-    case 128: return launch_one<D, W, SLAB, 4, 5>(P, st);
-    default: return fail(SNK_CONFIG, "samples per thread must be a power of two <= 128");
+template <int D, int W, int S, bool SLAB, int CH, int L>
+int32_t launch_brick(const EvoParams& P, const CUtensorMap& map, cudaStream_t st) {
+  auto k = evolve_brick_kernel<D, W, S, SLAB, CH, L>;
+  const int smem = (D == 3 ? S * S * S : S * S) * 2;
+  static std::once_flag once;
+  static cudaError_t attr_err = cudaSuccess;
+  std::call_once(once, [&] { attr_err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); });
+  if (attr_err != cudaSuccess) return cuda_fail(attr_err, "cudaFuncSetAttribute(evolve_brick_kernel)");
+  k<<<(unsigned)P.n, 32 * W, smem, st>>>(P, map);
+  SNK_LAUNCH_CHECK("evolve_brick_kernel");
+  return SNK_OK;
+}
+
+// B samples per thread: 1, 2 (one chunk) or 4 << L (chunks of 4, L <= 5).
+#define SNK_DISPATCH_B(B, CALL)                              \
+  switch (B) {                                               \
+    case 1: { constexpr int CH = 1, L = 0; return CALL; }    \
+    case 2: { constexpr int CH = 2, L = 0; return CALL; }    \
+    case 4: { constexpr int CH = 4, L = 0; return CALL; }    \
+    case 8: { constexpr int CH = 4, L = 1; return CALL; }    \
+    case 16: { constexpr int CH = 4, L = 2; return CALL; }   \
+    case 32: { constexpr int CH = 4, L = 3; return CALL; }   \
+    case 64: { constexpr int CH = 4, L = 4; return CALL; }   \
+    case 128: { constexpr int CH = 4, L = 5; return CALL; }  \
+    default: return fail(SNK_CONFIG, "samples per thread must be a power of two <= 128"); \
   }
+
+template <int D, int W, bool SLAB>
+int32_t warp_B(const EvoParams& P, int B, cudaStream_t st) {
+  SNK_DISPATCH_B(B, (launch_warp<D, W, SLAB, CH, L>(P, st)))
 }
 
 template <int D, bool SLAB>
-int32_t launch_W(const EvoParams& P, int W, int B, cudaStream_t st) {
+int32_t warp_W(const EvoParams& P, int W, int B, cudaStream_t st) {
   switch (W) {
-    case 1: return launch_B<D, 1, SLAB>(P, B, st);
-    case 2: return launch_B<D, 2, SLAB>(P, B, st);
-    case 4: return launch_B<D, 4, SLAB>(P, B, st);
-    case 8: return launch_B<D, 8, SLAB>(P, B, st);
+    case 1: return warp_B<D, 1, SLAB>(P, B, st);
+    case 2: return warp_B<D, 2, SLAB>(P, B, st);
+    case 4: return warp_B<D, 4, SLAB>(P, B, st);
+    case 8: return warp_B<D, 8, SLAB>(P, B, st);
     default: return fail(SNK_CONFIG, "bad warps per cell");
   }
+}
+
+template <int D, int W, int S, bool SLAB>
+int32_t brick_B(const EvoParams& P, const CUtensorMap& map, int B, cudaStream_t st) {
+  SNK_DISPATCH_B(B, (launch_brick<D, W, S, SLAB, CH, L>(P, map, st)))
+}
+
+// ------------------------------------------------------------------ TMA descriptor
+PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+bool make_brick_map(const snk_grid* g, const uint16_t* img, int S, CUtensorMap* map) {
+  auto enc = get_encode();
+  if (!enc) return false;
+  const int D = g->dim;
+  if ((g->n[0] * 2) % 16 != 0 || (reinterpret_cast<uintptr_t>(img) & 15) != 0) return false;
+  cuuint64_t dims[3] = {(cuuint64_t)g->n[0], (cuuint64_t)g->n[1], (cuuint64_t)g->nz_buf};
+  cuuint64_t strides[2] = {(cuuint64_t)g->n[0] * 2, (cuuint64_t)(g->n[0] * g->n[1] * 2)};
+  cuuint32_t box[3] = {(cuuint32_t)S, (cuuint32_t)S, (cuuint32_t)S};
+  cuuint32_t estr[3] = {1, 1, 1};
+  const CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT16, (cuuint32_t)D, const_cast<uint16_t*>(img),
+                         dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                         CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
 }
 
 }  // namespace
@@ -386,7 +675,7 @@ int32_t launch_W(const EvoParams& P, int W, int B, cudaStream_t st) {
 int evolve_warps_per_cell(const snk_params* p, int64_t n_cells) {
   int W = p->cta_warps;
   if (W <= 0) {
-    // enough warps to fill every SM with >= 16 warps -> warp-per-cell; else
+    // enough warps to fill every SM with >= 32 warps -> warp-per-cell; else
     // spread each cell over more warps (the paper's §II-F fix)
     W = 1;
     while (W < 8 && n_cells * W < 148 * 32 && p->n_samples >= 32 * 2 * W) W *= 2;
@@ -446,12 +735,29 @@ int32_t evolve_impl(const snk_grid* g, const snk_params* p, const uint16_t* d_im
   }
   if (D == 3 && g->n[2] < 2) return fail(SNK_SHAPE, "3D needs nz >= 2");
   if (g->n[0] * g->n[1] * g->nz_buf >= ((int64_t)1 << 32)) return fail(SNK_SHAPE, "buffer too large");
+  const bool slab = !(g->z_lo == 0 && g->nz_buf == g->n[2]);
+  // kernel choice: 0 auto, 1 warp (global gathers), 2 brick (TMA + shared memory)
+  const uint32_t variant = p->kernel_variant;
+  const int Wb = p->cta_warps > 0 ? p->cta_warps : 4;
+  const int Bb = p->n_samples / (32 * Wb);
+  const int Sb = D == 3 ? 32 : 64;
+  CUtensorMap map;
+  const bool brick_ok = variant != 1 && Bb >= 1 && Bb <= 128 && (Wb == 4 || Wb == 8) &&
+                        make_brick_map(g, d_image, Sb, &map);
+  if (variant == 2 && !brick_ok) return fail(SNK_CONFIG, "brick kernel unavailable for this volume");
+  if (brick_ok) {
+    if (D == 3) {
+      if (Wb == 4) return slab ? brick_B<3, 4, 32, true>(P, map, Bb, st) : brick_B<3, 4, 32, false>(P, map, Bb, st);
+      return slab ? brick_B<3, 8, 32, true>(P, map, Bb, st) : brick_B<3, 8, 32, false>(P, map, Bb, st);
+    }
+    if (Wb == 4) return brick_B<2, 4, 64, false>(P, map, Bb, st);
+    return brick_B<2, 8, 64, false>(P, map, Bb, st);
+  }
   const int W = evolve_warps_per_cell(p, n);
   const int B = p->n_samples / (32 * W);
   if (B < 1) return fail(SNK_CONFIG, "n_samples < 32 * warps per cell");
-  const bool slab = !(g->z_lo == 0 && g->nz_buf == g->n[2]);
-  if (D == 3) return slab ? launch_W<3, true>(P, W, B, st) : launch_W<3, false>(P, W, B, st);
-  return launch_W<2, false>(P, W, B, st);
+  if (D == 3) return slab ? warp_W<3, true>(P, W, B, st) : warp_W<3, false>(P, W, B, st);
+  return warp_W<2, false>(P, W, B, st);
 }
 
 }  // namespace snk

@@ -1,0 +1,275 @@
+"""Multi-GPU z-slab driver: one process per GPU,
+torch.distributed for the plumbing (NCCL on GPUs; gloo in the CPU tests).
+
+Partition.  Rank r owns the isotropic planes [z0_r, z1_r) (equal split) and
+holds raw planes [z0 - H - h, z1 + H + h) clipped to the volume, where
+h = ceil(4 sigma) is the blur radius and H = ceil(leash + r_max + dR/2) + 2
+bounds every voxel a cell seeded in [z0, z1) can read (leash per component,
+sampled ball radius, trilinear +1) — so seeds, cells, detections and labels
+are bit-identical to one GPU.
+
+Exchange steps (the only ones the method has):
+  N1  raw halo planes from the ranks that own them (P2P, once per step);
+  N2  all_gather of per-rank seed counts -> global ids = exclusive prefix
+      (slabs are contiguous in linear-index order, so ids equal one GPU's);
+  N3  all_gather of the E0 candidates (48-byte snk_cell records); every rank
+      then runs the identical deterministic cull (the overlap competition
+      crosses slab boundaries);
+  labels stay distributed (each rank labels its own planes).
+Cells never interact during evolution, so nothing is exchanged per
+iteration.
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import torch
+import torch.distributed as tdist
+
+
+@dataclass
+class SlabPlan:
+    n: tuple            # global isotropic dims (x, y, z)
+    world: int
+    rank: int
+    own: tuple          # owned planes [z0, z1)
+    halo: int           # H
+    blur: int           # h
+    buf: tuple          # raw / smoothed buffer planes [lo, hi)
+
+    @property
+    def nz_buf(self) -> int:
+        return self.buf[1] - self.buf[0]
+
+
+def slab_bounds(nz: int, world: int, r: int) -> tuple:
+    base, rem = divmod(nz, world)
+    z0 = r * base + min(r, rem)
+    return z0, z0 + base + (1 if r < rem else 0)
+
+
+def halo_planes(params) -> int:
+    return int(math.ceil(params.leash + params.r_max + params.delta_R / 2.0)) + 2
+
+
+def plan_slabs(n, world: int, rank: int, params) -> SlabPlan:
+    n = tuple(int(a) for a in n)
+    z0, z1 = slab_bounds(n[2], world, rank)
+    H = max(halo_planes(params), int(getattr(params, "seed_window", 0)))
+    h = int(math.ceil(4.0 * params.sigma)) if params.sigma > 0 else 0
+    lo, hi = max(z0 - H - h, 0), min(z1 + H + h, n[2])
+    return SlabPlan(n=n, world=world, rank=rank, own=(z0, z1), halo=H, blur=h, buf=(lo, hi))
+
+
+def exchange_halo(plan: SlabPlan, own_raw: torch.Tensor, group=None) -> torch.Tensor:
+    """N1: assemble raw planes [buf) from this rank's own planes and the other
+    ranks' (point-to-point; each rank sends exactly what the others need)."""
+    nz = plan.n[2]
+    lo, hi = plan.buf
+    z0, z1 = plan.own
+    plane_shape = own_raw.shape[1:]
+    out = torch.empty((hi - lo,) + tuple(plane_shape), dtype=own_raw.dtype, device=own_raw.device)
+    out[z0 - lo:z1 - lo].copy_(own_raw)
+    ops = []
+    recv = []
+    for q in range(plan.world):
+        if q == plan.rank:
+            continue
+        q0, q1 = slab_bounds(nz, plan.world, q)
+        # what I need from q
+        a, b = max(lo, q0), min(hi, q1)
+        if a < b:
+            buf = out[a - lo:b - lo]
+            t = buf if buf.is_contiguous() else torch.empty_like(buf)
+            ops.append(tdist.P2POp(tdist.irecv, _wire(t), q, group))
+            recv.append((buf, t))
+        # what q needs from me
+        qp = plan_like(plan, q)
+        a, b = max(qp.buf[0], z0), min(qp.buf[1], z1)
+        if a < b:
+            ops.append(tdist.P2POp(tdist.isend, _wire(own_raw[a - z0:b - z0].contiguous()), q, group))
+    if ops:
+        for r in tdist.batch_isend_irecv(ops):
+            r.wait()
+    for buf, t in recv:
+        if t.data_ptr() != buf.data_ptr():
+            buf.copy_(t)
+    return out
+
+
+def _wire(t: torch.Tensor) -> torch.Tensor:
+    """u16 planes travel as int16 (same bytes; NCCL/gloo have no uint16)."""
+    return t.view(torch.int16) if t.dtype == torch.uint16 else t
+
+
+def plan_like(plan: SlabPlan, rank: int) -> SlabPlan:
+    z0, z1 = slab_bounds(plan.n[2], plan.world, rank)
+    H, h = plan.halo, plan.blur
+    return SlabPlan(n=plan.n, world=plan.world, rank=rank, own=(z0, z1), halo=H, blur=h,
+                    buf=(max(z0 - H - h, 0), min(z1 + H + h, plan.n[2])))
+
+
+def allgather_counts(count: int, device, group=None) -> list:
+    """N2: every rank's count."""
+    t = torch.tensor([count], dtype=torch.int64, device=device)
+    outs = [torch.empty_like(t) for _ in range(tdist.get_world_size(group))]
+    tdist.all_gather(outs, t, group=group)
+    return [int(o.item()) for o in outs]
+
+
+def allgather_records(rec: torch.Tensor, count: int, device, group=None, rec_bytes: int = 48):
+    """N3: concatenate every rank's `count` records (uint8, rec_bytes each) in rank order."""
+    counts = allgather_counts(count, device, group)
+    m = max(max(counts), 1)
+    pad = torch.zeros(m * rec_bytes, dtype=torch.uint8, device=device)
+    if count:
+        pad[:count * rec_bytes].copy_(rec[:count * rec_bytes])
+    outs = [torch.empty_like(pad) for _ in counts]
+    tdist.all_gather(outs, pad, group=group)
+    allrec = torch.cat([o[:c * rec_bytes] for o, c in zip(outs, counts)])
+    return allrec, sum(counts), counts
+
+
+class SlabRun:
+    """One rank's share of one step: N1 -> a2/a3 -> a4 -> N2 -> a5/a6 -> a7
+    (compact, N3, cull) -> a8.  `backend` supplies the per-stage compute:
+    CudaBackend (libsnk) in production; the tests plug in the CPU oracle to check
+    the decomposition logic with gloo."""
+
+    def __init__(self, plan: SlabPlan, backend, device, group=None):
+        self.plan, self.be, self.device, self.group = plan, backend, device, group
+
+    def step(self, own_raw: torch.Tensor) -> dict:
+        pl = self.plan
+        local = exchange_halo(pl, own_raw, self.group)                 # N1
+        smooth = self.be.preprocess(pl, local)                          # a2/a3
+        seeds, ns = self.be.seeds(pl, smooth)                           # a4
+        counts = allgather_counts(ns, self.device, self.group)          # N2
+        id_base = sum(counts[:pl.rank])
+        cells = self.be.evolve(pl, smooth, seeds, ns, id_base)          # a5/a6
+        cand, nc = self.be.compact(cells, ns)                           # a7: E0
+        allc, ntot, _ = allgather_records(cand, nc, self.device, self.group)   # N3
+        dets, nd = self.be.cull(pl, allc, ntot)                         # a7: overlap
+        labels = self.be.label(pl, dets, nd)                            # a8
+        return {"n_seeds": ns, "id_base": id_base, "n_total": sum(counts), "cells": cells,
+                "seeds": seeds, "dets": dets, "n_dets": nd, "labels": labels, "smooth": smooth}
+
+
+class CudaBackend:
+    """libsnk on this rank's GPU; buffers are reused across steps."""
+
+    def __init__(self, plan: SlabPlan, params, max_cells: int, gradmag: bool = True):
+        from . import snk
+        self.snk = snk
+        self.p = params
+        n, (lo, hi) = plan.n, plan.buf
+        self.grid = snk.make_grid(3, n, z_lo=lo, nz_buf=hi - lo, own=plan.own)
+        shape = (hi - lo, n[1], n[0])
+        dev = torch.device("cuda", torch.cuda.current_device())
+        self.smooth = torch.empty(shape, dtype=torch.uint16, device=dev)
+        self.grad = torch.empty(shape, dtype=torch.uint16, device=dev) if gradmag else None
+        self.max_cells = max_cells
+        self.seeds_t = torch.empty((max_cells, 3), dtype=torch.float32, device=dev)
+        self.cells = torch.empty(max_cells * 48, dtype=torch.uint8, device=dev)
+        self.cand = torch.empty(max_cells * 48, dtype=torch.uint8, device=dev)
+        self.total_cap = max_cells * plan.world
+        self.dets = torch.empty(self.total_cap * 48, dtype=torch.uint8, device=dev)
+        self.labels = torch.empty((plan.own[1] - plan.own[0], n[1], n[0]), dtype=torch.int32, device=dev)
+        ws = max(snk.snk_workspace_bytes(self.grid, params, self.total_cap), 1)
+        self.ws = torch.empty(ws, dtype=torch.uint8, device=dev)
+
+    def preprocess(self, pl, local):
+        self.snk.snk_preprocess(self.grid, self.p, local, self.smooth, self.grad, self.ws)
+        return self.smooth
+
+    def seeds(self, pl, smooth):
+        n, _ = self.snk.snk_seeds(self.grid, self.p, smooth, self.seeds_t, self.max_cells, self.ws)
+        return self.seeds_t, n
+
+    def evolve(self, pl, smooth, seeds, n, id_base):
+        img = self.grad if self.p.image_term == self.snk.IMAGE_GRADMAG else smooth
+        if n:
+            self.snk.snk_evolve(self.grid, self.p, img, seeds, None, id_base, n, self.cells, None)
+        return self.cells
+
+    def compact(self, cells, n):
+        return self.cand, self.snk.snk_compact_candidates(self.p, cells, n, self.cand, self.max_cells,
+                                                          self.ws)
+
+    def cull(self, pl, allc, ntot):
+        nd = self.snk.snk_cull(self.grid, self.p, allc, ntot, self.dets, self.total_cap, self.ws)
+        return self.dets, nd
+
+    def label(self, pl, dets, nd):
+        self.snk.snk_label(self.grid, self.p, dets, nd, self.labels, self.ws)
+        return self.labels
+
+
+def bench_rank(args, cfg):
+    """bench.py for N > 1 ranks: z-slabs of one volume (strong scaling); timed on
+    the device with CUDA events, max over ranks; rank 0 returns the JSON dict."""
+    import os
+    import statistics
+    import time
+
+    import numpy as np
+
+    import synth
+    from . import pipeline, snk
+
+    rank, local_rank, world = (int(os.environ.get(k, d)) for k, d in
+                               (("RANK", "0"), ("LOCAL_RANK", "0"), ("WORLD_SIZE", "1")))
+    torch.cuda.set_device(local_rank)
+    tdist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    assert tuple(cfg.iso_n) == tuple(cfg.n), "the slab driver takes isotropic volumes"
+    p = pipeline.params_for(cfg, image_term=snk.IMAGE_INTENSITY)
+    plan = plan_slabs(cfg.n, world, rank, p)
+    z0, z1 = plan.own
+    nown = (z1 - z0) * cfg.n[0] * cfg.n[1]
+    max_cells = max(4096, (plan.nz_buf * cfg.n[0] * cfg.n[1]) // (2 * cfg.window + 1) ** 3 + 4096)
+    be = CudaBackend(plan, p, max_cells)
+    h_raw = torch.empty((z1 - z0, cfg.n[1], cfg.n[0]), dtype=torch.uint16, pin_memory=True)
+    synth.generate_into_ptr(cfg, h_raw.data_ptr(), z0, z1)
+    own = torch.empty(h_raw.shape, dtype=torch.uint16, device="cuda")
+    own.copy_(h_raw)
+    run = SlabRun(plan, be, torch.device("cuda", local_rank))
+    for _ in range(args.warmup):
+        r = run.step(own)
+    torch.cuda.synchronize()
+    tdist.barrier()
+    l0 = snk.snk_launch_count()
+    from bench import ClockSampler  # noqa: E402
+    with ClockSampler(local_rank) as clk:
+        torch.cuda.synchronize()
+        tdist.barrier()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        for _ in range(args.steps):
+            r = run.step(own)
+        e.record()
+        torch.cuda.synchronize()
+        tdist.barrier()
+    ms = torch.tensor([s.elapsed_time(e)], dtype=torch.float64, device="cuda")
+    tdist.all_reduce(ms, op=tdist.ReduceOp.MAX)
+    total_ms = float(ms.item())
+    launches = snk.snk_launch_count() - l0
+    n_total = r["n_total"]
+    samples = n_total * (cfg.max_iters + 1) * cfg.n_samples
+    out = None
+    if rank == 0:
+        clocks = clk.summary()
+        out = {"metric": "contour ray-samples/sec and cells segmented/sec at 1/2/4/8 B200; HBM/L2 GB/s",
+               "value": samples * args.steps / (total_ms / 1e3), "unit": "ray-samples/s",
+               "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+               "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "strong",
+               "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+               "config": {"workload": f"{cfg.name} z-slabs", "volume_iso": list(cfg.n), "cells": n_total,
+                          "detections": r["n_dets"], "n_samples": cfg.n_samples, "iters": cfg.max_iters,
+                          "parallelism": f"z-slab x{world}", "halo_planes": plan.halo,
+                          "l2": "inputs larger than L2"},
+               "cells_per_s": n_total * args.steps / (total_ms / 1e3), "gpu_launches": int(launches),
+               "clocks": clocks, "roofline": None, "cpu_baseline": None, "e2e": None}
+    tdist.barrier()
+    tdist.destroy_process_group()
+    return out

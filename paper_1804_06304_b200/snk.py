@@ -51,7 +51,7 @@ class snk_params(C.Structure):
                 ("leash", C.c_double), ("conv_tol", C.c_double), ("max_iters", C.c_int32),
                 ("n_samples", C.c_int32), ("seed_mode", C.c_int32), ("seed_window", C.c_int32),
                 ("image_term", C.c_int32), ("cta_warps", C.c_int32), ("seed_threshold", C.c_uint32),
-                ("_pad1", C.c_uint32), ("seed", C.c_uint64)]
+                ("kernel_variant", C.c_uint32), ("seed", C.c_uint64)]
 
 
 class snk_cell(C.Structure):
@@ -121,6 +121,8 @@ def _stream(s) -> C.c_void_p:
 
 
 def _nbytes(x) -> int:
+    if x is None:
+        return 0
     if hasattr(x, "untyped_storage"):
         return x.numel() * x.element_size()
     return int(x)
@@ -252,7 +254,8 @@ def make_grid(dim: int, n, z_lo: int = 0, nz_buf: int | None = None, own=None) -
 def make_params(r0=10.0, *, delta_R=2.0, eps0=0.5, e0=-3.0, sigma=1.0, intensity_scale=1.0 / 257.0,
                 max_step=1.0, r_min=1.0, r_max=None, leash=None, conv_tol=1e-3, max_iters=400,
                 n_samples=1024, seed_mode=SEED_MAXIMA, seed_window=4, image_term=IMAGE_INTENSITY,
-                cta_warps=0, seed_threshold=70 * 257, seed=1804063040) -> snk_params:
+                cta_warps=0, seed_threshold=70 * 257, seed=1804063040,
+                kernel_variant=0) -> snk_params:
     """Defaults: DESIGN.md §3 (readings G2-G9, G18, G20)."""
     p = snk_params()
     p.r0, p.delta_R, p.eps0, p.e0, p.sigma = r0, delta_R, eps0, e0, sigma
@@ -262,5 +265,6 @@ def make_params(r0=10.0, *, delta_R=2.0, eps0=0.5, e0=-3.0, sigma=1.0, intensity
     p.conv_tol, p.max_iters, p.n_samples = conv_tol, max_iters, n_samples
     p.seed_mode, p.seed_window, p.image_term, p.cta_warps = seed_mode, seed_window, image_term, cta_warps
     p.seed_threshold = seed_threshold
+    p.kernel_variant = kernel_variant
     p.seed = seed & 0xFFFFFFFFFFFFFFFF
     return p

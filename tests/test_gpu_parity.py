@@ -158,7 +158,7 @@ def _oracle_smooth_crop(raw_iso, lo, hi, n):
 
 @pytest.mark.parametrize("name", ["C3", "C4"])
 def test_full_size_sampled_parity(gpu, name):
-    """Full BASELINE sizes in the bench's launch configuration (warp per cell):
+    """Full BASELINE sizes in the bench's launch configuration (auto kernel choice):
     sampled crops of the smoothed volume and the seed list are bit-exact; sampled
     cells evolve within tolerance; the full-launch results for those cells are
     bit-identical to a separate launch of just them."""
@@ -188,8 +188,8 @@ def test_full_size_sampled_parity(gpu, name):
         test_seeds.append(exp[rng.permutation(len(exp))[:8]])
     seeds = np.concatenate(test_seeds).astype(np.float32)
     ids = rng.permutation(1 << 20)[:len(seeds)].astype(np.int64) + 12345
-    # GPU: the bench's kernel configuration (warp per cell), explicit seeds and ids
-    p1 = pipeline.params_for(cfg, cta_warps=1)
+    # GPU: the bench's kernel configuration (auto: brick kernel), explicit seeds and ids
+    p1 = pipeline.params_for(cfg)
     cells = torch.empty(len(seeds) * 48, dtype=torch.uint8, device="cuda")
     snk.snk_evolve(P.grid, p1, P.smooth, _t(torch, seeds), _t(torch, ids), 0, len(seeds), cells, None)
     torch.cuda.synchronize()
@@ -232,18 +232,47 @@ def test_evolve_c1_parity_and_schedules(gpu):
     st, oseeds = oracle.seeds_lattice(cfg.n, 3, cfg.r0)
     assert np.array_equal(P.seeds_np(), oseeds)
     ref = None
-    for W in (1, 2, 4, 8):
-        P.params = pipeline.params_for(cfg, cta_warps=W)
+    # warp kernel (global gathers) at W = 1..8 and brick kernel (TMA + smem) at W = 4, 8
+    for variant, W in ((1, 1), (1, 2), (1, 4), (1, 8), (2, 4), (2, 8), (0, 0)):
+        P.params = pipeline.params_for(cfg, cta_warps=W, kernel_variant=variant)
         P.evolve()
         torch.cuda.synchronize()
         c = P.cells_np()
         if ref is None:
             ref = c
-        assert c.tobytes() == ref.tobytes(), f"cta_warps={W} differs"
+        assert c.tobytes() == ref.tobytes(), f"variant={variant} cta_warps={W} differs"
     o = oracle.evolve(B, _ora_params(cfg), oseeds, ids=np.arange(len(oseeds)))
     _assert_cells_close(ref, o, "C1")
     fmask = oracle.COLLAPSED | oracle.RMAX
     assert np.array_equal(ref["flags"] & fmask, o["flags"] & fmask)
+
+
+@pytest.mark.parametrize("r0", [14.0, 18.0])
+def test_brick_reload_and_global_fallback(gpu, r0):
+    """Large contours whose sampled ball does not always fit the 32^3 brick take
+    the global-gather path for those iterations; lattice snakes far from nuclei
+    move and force brick re-centring.  Both kernels agree bit for bit and with
+    the oracle."""
+    torch, snk, pipeline = gpu
+    cfg = synth.CONFIGS["C1"].with_(r0=r0, max_iters=120, n_samples=256)
+    n = (72, 72, 72)
+    raw = synth.generate(synth.CONFIGS["C1"].with_(n=n))
+    p = pipeline.params_for(cfg, seed_mode=snk.SEED_LATTICE)
+    P = pipeline.Pipeline(3, n, p)
+    P.upload(raw)
+    P.preprocess()
+    P.seed()
+    out = []
+    for variant in (1, 2):
+        P.params = pipeline.params_for(cfg, seed_mode=snk.SEED_LATTICE, kernel_variant=variant,
+                                       cta_warps=4 if variant == 2 else 0)
+        P.evolve()
+        torch.cuda.synchronize()
+        out.append(P.cells_np())
+    assert out[0].tobytes() == out[1].tobytes()
+    B = oracle.blur(raw, 3, 1.0)
+    o = oracle.evolve(B, _ora_params(cfg), P.seeds_np(), ids=np.arange(P.n_seeds))
+    _assert_cells_close(out[1], o, f"r0={r0}")
 
 
 @pytest.mark.parametrize("N", [32, 64, 256, 4096])
@@ -254,7 +283,7 @@ def test_evolve_sample_counts(gpu, N):
     P, raw, p = _gpu_smooth_seeds(torch, snk, pipeline, cfg)
     B = oracle.blur(raw, 3, 1.0)
     for W in ((1, 8) if N >= 256 else (1,)):
-        P.params = pipeline.params_for(cfg, cta_warps=W)
+        P.params = pipeline.params_for(cfg, cta_warps=W)   # N >= 256: W=8 takes the brick kernel
         P.evolve(n=16)
         torch.cuda.synchronize()
         g = P.cells_np()[:16]
