@@ -145,7 +145,8 @@ def run_ours(args):
         return D.bench_rank(args, cfg)
     torch.cuda.set_device(local_rank)
     from paper_1804_06304_b200 import pipeline, snk
-    p = pipeline.params_for(cfg, image_term=snk.IMAGE_INTENSITY)
+    p = pipeline.params_for(cfg, image_term=snk.IMAGE_INTENSITY, cta_warps=args.cta_warps,
+                            kernel_variant=args.kernel_variant)
     P = pipeline.Pipeline(cfg.dim, cfg.n, p, spacing=cfg.spacing, gradmag=True)
     h_raw = torch.empty((cfg.n[2], cfg.n[1], cfg.n[0]), dtype=torch.uint16, pin_memory=True)
     t = time.perf_counter()
@@ -202,7 +203,7 @@ def run_ours(args):
     achieved = samples * OPS_PER_SAMPLE / ev_s / 1e9
     roofline = {"bound": "alu", "achieved": round(achieved, 1), "peak": round(peak, 1),
                 "unit": "Glane-op/s", "frac": round(achieved / peak, 4), "traffic": None,
-                "kernel": "evolve_kernel<3,1,false,4,3>", "ops_per_sample": OPS_PER_SAMPLE,
+                "kernel": "evolve_brick_kernel" if args.kernel_variant != 1 else "evolve_warp_kernel", "ops_per_sample": OPS_PER_SAMPLE,
                 "samples_per_s_kernel": samples / ev_s,
                 "gather_GBps": round(samples * 16 / ev_s / 1e9, 1),
                 "peak_source": f"{SMS} SMs x {LANES_PER_SM} FP32 lanes x sm_max_mhz (B200_PROFILING.md)"}
@@ -292,6 +293,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cta-warps", type=int, default=0, help="warps per cell (0: auto)")
+    ap.add_argument("--kernel-variant", type=int, default=0, help="evolve kernel: 0 auto, 1 warp, 2 brick")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3   # contract: at least 3 warm-up steps

@@ -85,13 +85,13 @@ typedef struct snk_grid {
  *   max_iters T (400)                            n_samples N per cell-iteration, a power of 2
  *   seed_mode LATTICE | MAXIMA | GIVEN                  seed_window w, seed_threshold thr (G20)
  *   image_term INTENSITY | GRADMAG                      cta_warps warps per cell: 0 auto, 1, 2, 4, 8
- *   kernel_variant  0 auto (brick when the volume suits TMA), 1 warp kernel, 2 brick kernel
+ *   kernel_variant  0 auto (brick kernel when nx is even), 1 warp kernel, 2 brick kernel
  *   seed      Philox key (G11) */
 typedef struct snk_params {
   double r0, delta_R, eps0, e0, sigma, intensity_scale, max_step, r_min, r_max, leash, conv_tol;
   int32_t max_iters, n_samples, seed_mode, seed_window, image_term, cta_warps;
   uint32_t seed_threshold;
-  uint32_t kernel_variant; /* evolve kernel: 0 auto, 1 warp (global gathers), 2 brick (TMA + smem) */
+  uint32_t kernel_variant; /* evolve kernel: 0 auto, 1 warp (global gathers), 2 brick (shared memory) */
   uint64_t seed;
 } snk_params;
 

@@ -98,7 +98,9 @@ int32_t label_impl(const snk_grid* g, const snk_params* p, const snk_cell* d_det
 
 int evolve_warps_per_cell(const snk_params* p, int64_t n_cells);
 
-// exclusive scan of n int counts into n + 1 int64 offsets (offsets[n] = total)
-int32_t scan_counts(const int* counts, int64_t n, int64_t* offsets, cudaStream_t st);
+// exclusive scan of n int counts into n + 1 int64 offsets (offsets[n] = total);
+// tmp: scan_ws(n) bytes of scratch (nullptr: single-block scan)
+size_t scan_ws(int64_t n);
+int32_t scan_counts(const int* counts, int64_t n, int64_t* offsets, cudaStream_t st, void* tmp);
 
 }  // namespace snk

@@ -185,8 +185,9 @@ __global__ void mis_round_kernel(SortedCells S, int64_t nc, BinGrid G, const int
   else atomicAdd(undecided, 1ull);
 }
 
-// exclusive scan of int counts -> int64 offsets (+ total at [n]); one block
-__global__ void __launch_bounds__(1024) scan_kernel(const int* counts, int64_t n, int64_t* offsets) {
+// exclusive scan of counts -> int64 offsets (+ total at [n]); one block
+template <typename T>
+__global__ void __launch_bounds__(1024) scan_any_kernel(const T* counts, int64_t n, int64_t* offsets) {
   __shared__ int64_t part[1024];
   const int t = threadIdx.x;
   const int64_t per = (n + 1023) / 1024;
@@ -208,6 +209,8 @@ __global__ void __launch_bounds__(1024) scan_kernel(const int* counts, int64_t n
   }
   if (t == 1023) offsets[n] = part[1023];
 }
+#define scan_kernel scan_any_kernel<int>
+#define scan_i64_kernel scan_any_kernel<int64_t>
 
 // order-preserving compaction, 1024 elements per block
 template <typename Pred>
@@ -289,9 +292,87 @@ size_t bins_cap(int64_t max_cells) { return (size_t)(4 * std::max<int64_t>(max_c
 
 }  // namespace
 
-int32_t scan_counts(const int* counts, int64_t n, int64_t* offsets, cudaStream_t st) {
-  scan_kernel<<<1, 1024, 0, st>>>(counts, n, offsets);
-  SNK_LAUNCH_CHECK("scan_kernel");
+namespace {
+
+constexpr int kScanThreads = 1024, kScanPer = 4, kScanTile = kScanThreads * kScanPer;
+
+__device__ __forceinline__ int64_t block_scan_excl(int64_t v, int64_t* total) {
+  __shared__ int64_t wsum[kScanThreads / 32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int64_t x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int64_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) wsum[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    int64_t s = wsum[lane];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int64_t y = __shfl_up_sync(0xffffffffu, s, o);
+      if (lane >= o) s += y;
+    }
+    wsum[lane] = s;
+  }
+  __syncthreads();
+  *total = wsum[31];
+  return (warp > 0 ? wsum[warp - 1] : 0) + x - v;
+}
+
+__global__ void __launch_bounds__(kScanThreads) tile_sum_kernel(const int* counts, int64_t n, int64_t* sums) {
+  const int64_t base = (int64_t)blockIdx.x * kScanTile + (int64_t)threadIdx.x * kScanPer;
+  int64_t s = 0;
+#pragma unroll
+  for (int k = 0; k < kScanPer; ++k)
+    if (base + k < n) s += counts[base + k];
+  int64_t total;
+  block_scan_excl(s, &total);
+  if (threadIdx.x == 0) sums[blockIdx.x] = total;
+}
+
+__global__ void __launch_bounds__(kScanThreads) tile_scan_kernel(const int* counts, int64_t n,
+                                                                 const int64_t* tile_off, int64_t* offsets) {
+  const int64_t base = (int64_t)blockIdx.x * kScanTile + (int64_t)threadIdx.x * kScanPer;
+  int c[kScanPer];
+  int64_t s = 0;
+#pragma unroll
+  for (int k = 0; k < kScanPer; ++k) {
+    c[k] = base + k < n ? counts[base + k] : 0;
+    s += c[k];
+  }
+  int64_t total;
+  int64_t run = tile_off[blockIdx.x] + block_scan_excl(s, &total);
+#pragma unroll
+  for (int k = 0; k < kScanPer; ++k) {
+    if (base + k < n) offsets[base + k] = run;
+    run += c[k];
+  }
+  if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) offsets[n] = tile_off[blockIdx.x] + total;
+}
+
+}  // namespace
+
+size_t scan_ws(int64_t n) { return (size_t)(ceil_div(std::max<int64_t>(n, 1), kScanTile) + 1) * sizeof(int64_t) * 2 + 512; }
+
+// Exclusive scan of int counts.  Small n: one block.  Large n: per-tile sums ->
+// one-block scan of the tile sums (into `tmp`, scan_ws(n) bytes) -> per-tile scans.
+int32_t scan_counts(const int* counts, int64_t n, int64_t* offsets, cudaStream_t st, void* tmp) {
+  if (n <= 4 * kScanTile || tmp == nullptr) {
+    scan_kernel<<<1, 1024, 0, st>>>(counts, n, offsets);
+    SNK_LAUNCH_CHECK("scan_kernel");
+    return SNK_OK;
+  }
+  const int64_t nt = ceil_div(n, kScanTile);
+  int64_t* sums = static_cast<int64_t*>(tmp);
+  int64_t* toff = sums + nt + 1;
+  tile_sum_kernel<<<(unsigned)nt, kScanThreads, 0, st>>>(counts, n, sums);
+  SNK_LAUNCH_CHECK("tile_sum_kernel");
+  scan_i64_kernel<<<1, 1024, 0, st>>>(sums, nt, toff);
+  SNK_LAUNCH_CHECK("scan_i64_kernel");
+  tile_scan_kernel<<<(unsigned)nt, kScanThreads, 0, st>>>(counts, n, toff, offsets);
+  SNK_LAUNCH_CHECK("tile_scan_kernel");
   return SNK_OK;
 }
 
@@ -305,6 +386,7 @@ size_t cull_ws(const snk_grid* g, const snk_params* p, int64_t max_cells) {
   b += 4 * (size_t)n * sizeof(float) + 1024;
   b += (size_t)n * sizeof(int) * 2 + 512;          // status, entries
   b += nbins * (sizeof(int) * 2 + sizeof(int64_t)) + sizeof(int64_t) + 1024;   // counts, cursor, offsets
+  b += scan_ws((int64_t)nbins) + 256;
   b += (size_t)(ceil_div(n, 1024) + 1) * (sizeof(int) + sizeof(int64_t)) + 512;
   b += 4096;
   return b;
@@ -347,6 +429,7 @@ int32_t cull_impl(const snk_grid* g, const snk_params* p, const snk_cell* d_cell
   int* bcount = cv.take<int>(nbins_cap);
   int* bcursor = cv.take<int>(nbins_cap);
   int64_t* boff = cv.take<int64_t>(nbins_cap + 1);
+  void* bscan = cv.take<char>(scan_ws(nbins_cap));
   const int64_t nblk = ceil_div(n, 1024);
   int* ccounts = cv.take<int>(nblk);
   int64_t* coffsets = cv.take<int64_t>(nblk + 1);
@@ -410,8 +493,7 @@ int32_t cull_impl(const snk_grid* g, const snk_params* p, const snk_cell* d_cell
   SNK_CUDA_CHECK(cudaMemsetAsync(status, 0, nc * sizeof(int), st));
   bin_count_kernel<<<(unsigned)ceil_div(nc, 256), 256, 0, st>>>(S, nc, G, bcount);
   SNK_LAUNCH_CHECK("bin_count_kernel");
-  scan_kernel<<<1, 1024, 0, st>>>(bcount, nbins, boff);
-  SNK_LAUNCH_CHECK("scan_kernel");
+  SNK_TRY(scan_counts(bcount, nbins, boff, st, bscan));
   bin_fill_kernel<<<(unsigned)ceil_div(nc, 256), 256, 0, st>>>(S, nc, G, boff, bcursor, entries);
   SNK_LAUNCH_CHECK("bin_fill_kernel");
   for (int round = 0;; ++round) {

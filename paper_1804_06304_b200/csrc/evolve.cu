@@ -3,15 +3,16 @@
 //
 // Two kernels compute the same function, bit for bit:
 //
-//  * evolve_brick_kernel (default when the volume meets TMA's alignment rules):
-//    one CTA of W warps per cell (the paper's block-per-contour).  The
-//    cell's neighbourhood — an S^d brick of the u16 image containing the
-//    sampled ball — lives in shared memory, loaded by one TMA box copy
-//    (cp.async.bulk.tensor) and re-centred only when the ball leaves it, so
-//    the per-sample gathers are shared-memory loads with immediate offsets
-//    and L2/HBM see ~one brick per cell instead of 8 scattered taps per
-//    sample.  A sample ball that cannot fit the brick falls back to global
-//    loads for that iteration (same arithmetic).
+//  * evolve_brick_kernel (default; needs an even x extent): one CTA of W warps
+//    per cell (the paper's block-per-contour).  The cell's
+//    neighbourhood — a (S+2) x S x S brick of the u16 image containing the
+//    sampled ball — lives in shared memory, filled by cp.async copies and
+//    re-centred only when the ball leaves it, so the per-sample gathers are
+//    shared-memory loads with immediate offsets and L2/HBM see a few bricks
+//    per cell instead of 8 scattered taps per sample (the warp kernel is
+//    L1-bound on C3 and DRAM-bound on C4, profiles/r1_baseline_evolve.md).  A
+//    sample ball that cannot fit the brick takes global loads for that
+//    iteration (same arithmetic).
 //  * evolve_warp_kernel (generic fallback, any shape): W warps per cell,
 //    gathers straight from global memory (L1/L2).
 //
@@ -26,8 +27,6 @@
 // Reading of the update (G3/G4/G8): E = gamma A0,
 // dE/dc = -gamma A_c, dE/dR = gamma (A_R - (d/R) A0), gamma = (2R)^-d;
 // (c, R) -= clip((eps0/sqrt(n))/2 * grad, +-max_step); R clamp, leash, domain.
-#include <cudaTypedefs.h>
-
 #include <mutex>
 
 #include "common.cuh"
@@ -198,20 +197,21 @@ __device__ __forceinline__ Acc sample_leaf(const EvoParams& P, const CellIt& C, 
   if (D == 3) fz = split_axis<CLAMP>(__fmaf_rn(d.t, d.oz, C.cz), P.fnz1, P.mz2, &rz);
   float v000, v100, v010, v110, v001 = 0, v101 = 0, v011 = 0, v111 = 0;
   if (MODE == G_BRICK_CLAMP || MODE == G_BRICK_FAST) {
-    // brick-local index; strides S and S^2 are immediates
+    // brick-local index; row stride SX = S + 2 and plane stride SX * S are immediates
+    constexpr int SX = S + 2, SP = SX * S;
     const uint32_t lx = rx - C.ob[0], ly = ry - C.ob[1];
-    uint32_t li = ly * S + lx;
-    if (D == 3) li += (rz - C.ob[2]) * (S * S);
+    uint32_t li = ly * SX + lx;
+    if (D == 3) li += (rz - C.ob[2]) * SP;
     const uint16_t* p = brick + li;
     v000 = mag(p[0]);
     v100 = mag(p[1]);
-    v010 = mag(p[S]);
-    v110 = mag(p[S + 1]);
+    v010 = mag(p[SX]);
+    v110 = mag(p[SX + 1]);
     if (D == 3) {
-      v001 = mag(p[S * S]);
-      v101 = mag(p[S * S + 1]);
-      v011 = mag(p[S * S + S]);
-      v111 = mag(p[S * S + S + 1]);
+      v001 = mag(p[SP]);
+      v101 = mag(p[SP + 1]);
+      v011 = mag(p[SP + SX]);
+      v111 = mag(p[SP + SX + 1]);
     }
   } else {
     int iz = (int)(rz - kMagicBits);
@@ -457,67 +457,48 @@ __global__ void __launch_bounds__(W >= 4 ? 32 * W : 128)
 }
 
 // =========================================================================
-// Brick kernel: one CTA (W warps) per cell, S^d u16 brick in shared memory
-// loaded by TMA.
+// Brick kernel: one CTA (W warps) per cell; the u16 neighbourhood of the cell
+// (x: S + 2 columns from an even origin, y and z: S rows/planes) lives in
+// shared memory, filled by 4-byte cp.async copies (LDGSTS) when the sampled
+// ball leaves it.
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
 }
 
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-               : "memory");
-}
-
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n"
-      "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-      "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
-      "r"(phase)
-      : "memory");
-}
-
-template <int D>
-__device__ __forceinline__ void tma_load_brick(uint16_t* dst, const CUtensorMap* map, int x, int y,
-                                               int z, uint64_t* bar) {
-  if (D == 3) {
-    asm volatile(
-        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes "
-        "[%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
-        "l"(map), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
-        : "memory");
-  } else {
-    asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes "
-        "[%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(dst)),
-        "l"(map), "r"(x), "r"(y), "r"(smem_u32(bar))
-        : "memory");
+template <int D, int S>
+__device__ __forceinline__ void load_brick(uint16_t* brick, const EvoParams& P, int bx, int by, int bz,
+                                           int zlo_buf) {
+  constexpr int SX = S + 2, WPR = SX / 2;          // u16 per row, 32-bit words per row
+  constexpr int ROWS = D == 3 ? S * S : S;
+  const int nw = min(WPR, (P.nx - bx + 1) / 2);     // words inside the volume (x)
+  const int ny = min(S, P.ny - by);
+  const int nzl = D == 3 ? min(S, P.z_lo + P.nz_buf - bz) : 1;
+  const uint32_t* src = reinterpret_cast<const uint32_t*>(P.img);
+  const uint32_t dst0 = smem_u32(brick);
+  for (int w = threadIdx.x; w < ROWS * WPR; w += blockDim.x) {
+    const int row = w / WPR, col = w % WPR;
+    const int ry = row % S, rz = row / S;
+    if (col >= nw || ry >= ny || rz >= nzl) continue;
+    const int64_t g = ((int64_t)(bz - zlo_buf + rz) * P.ny + (by + ry)) * P.nx + bx;   // even
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst0 + (uint32_t)w * 4u),
+                 "l"(src + g / 2 + col)
+                 : "memory");
   }
+  asm volatile("cp.async.wait_all;" ::: "memory");
+  __syncthreads();
 }
 
 template <int D, int W, int S, bool SLAB, int CH, int L>
-__global__ void __launch_bounds__(32 * W)
-    evolve_brick_kernel(const __grid_constant__ EvoParams P, const __grid_constant__ CUtensorMap map) {
+__global__ void __launch_bounds__(32 * W) evolve_brick_kernel(const __grid_constant__ EvoParams P) {
   constexpr int B = CH << L;
-  constexpr uint32_t kBrickBytes = (D == 3 ? S * S * S : S * S) * 2;
-  extern __shared__ __align__(128) uint16_t brick[];
+  constexpr int EXT[3] = {S + 2, S, S};             // brick extent per axis
+  extern __shared__ __align__(16) uint16_t brick[];
   __shared__ Acc xch[2][W];
-  __shared__ __align__(8) uint64_t bar;
   const int lane = threadIdx.x & 31, wsub = threadIdx.x >> 5;
   const int64_t cell = blockIdx.x;
-  if (threadIdx.x == 0) {
-    mbar_init(&bar, 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
   CellState s;
   cell_begin(P, cell, D, s);
-  uint32_t halo = 0, phase = 0;
+  uint32_t halo = 0;
   int b[3] = {-(1 << 28), -(1 << 28), -(1 << 28)};   // brick origin (global voxels); none yet
   const int n[3] = {P.nx, P.ny, P.nz};
   // z range the brick may cover: the slab buffer
@@ -538,28 +519,24 @@ __global__ void __launch_bounds__(32 * W)
       lo[a] = max(lo[a], 0);
       hi[a] = min(hi[a], n[a] - 1);
       fits &= hi[a] - lo[a] + 1 <= S;
-      inside &= lo[a] >= b[a] && hi[a] <= b[a] + S - 1;
+      inside &= lo[a] >= b[a] && hi[a] <= b[a] + EXT[a] - 1;
     }
     if (D == 3 && SLAB) fits &= lo[2] >= zlo && hi[2] <= zhi;
     if (!inside && fits) {
-      // re-centre: the ball's box in the middle of the brick, clipped to the buffer
+      // re-centre: the ball's box in the middle of the brick, clipped to the
+      // volume (z: the slab buffer); the x origin is even (4-byte copies)
 #pragma unroll
       for (int a = 0; a < D; ++a) {
         const int amin = (a == 2) ? zlo : 0, amax = (a == 2) ? zhi : n[a] - 1;
-        int o = lo[a] - (S - (hi[a] - lo[a] + 1)) / 2;
-        o = min(o, amax + 1 - S);
+        int o = lo[a] - (EXT[a] - (hi[a] - lo[a] + 1)) / 2;
+        if (a == 0) o &= ~1;
+        o = min(o, amax + 1 - EXT[a]);
+        if (a == 0) o &= ~1;
         o = max(o, amin);
         b[a] = o;
       }
-      // all reads of the previous brick finished at the last iteration's barrier
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        mbar_expect_tx(&bar, kBrickBytes);
-        tma_load_brick<D>(brick, &map, b[0], b[1], D == 3 ? b[2] - zlo : 0, &bar);
-      }
-      mbar_wait(&bar, phase);
-      phase ^= 1u;
+      // every read of the old brick finished before last iteration's barrier
+      load_brick<D, S>(brick, P, b[0], b[1], D == 3 ? b[2] : 0, zlo);
       inside = true;
     }
     Acc part;
@@ -572,11 +549,9 @@ __global__ void __launch_bounds__(32 * W)
       part = lane_sum<D, SLAB ? G_GLOBAL_SLAB : G_GLOBAL, S, CH, L>(P, C, j0, brick, halo);
     }
     Acc sum = warp_butterfly(part);
-    if constexpr (W > 1) {
-      if (lane == 0) xch[it & 1][wsub] = sum;
-      __syncthreads();
-      sum = warp_tree<W>(xch[it & 1]);
-    }
+    if (lane == 0) xch[it & 1][wsub] = sum;
+    __syncthreads();   // also: every brick read of this iteration is done
+    if constexpr (W > 1) sum = warp_tree<W>(xch[it & 1]);
     if (cell_update<D>(P, s, C, sum, it)) break;
   }
   if (SLAB && __syncthreads_or(halo != 0)) s.flags |= SNK_F_HALO;
@@ -593,14 +568,14 @@ int32_t launch_warp(const EvoParams& P, cudaStream_t st) {
 }
 
 template <int D, int W, int S, bool SLAB, int CH, int L>
-int32_t launch_brick(const EvoParams& P, const CUtensorMap& map, cudaStream_t st) {
+int32_t launch_brick(const EvoParams& P, cudaStream_t st) {
   auto k = evolve_brick_kernel<D, W, S, SLAB, CH, L>;
-  const int smem = (D == 3 ? S * S * S : S * S) * 2;
+  const int smem = (D == 3 ? (S + 2) * S * S : (S + 2) * S) * 2;
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [&] { attr_err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); });
   if (attr_err != cudaSuccess) return cuda_fail(attr_err, "cudaFuncSetAttribute(evolve_brick_kernel)");
-  k<<<(unsigned)P.n, 32 * W, smem, st>>>(P, map);
+  k<<<(unsigned)P.n, 32 * W, smem, st>>>(P);
   SNK_LAUNCH_CHECK("evolve_brick_kernel");
   return SNK_OK;
 }
@@ -636,38 +611,8 @@ int32_t warp_W(const EvoParams& P, int W, int B, cudaStream_t st) {
 }
 
 template <int D, int W, int S, bool SLAB>
-int32_t brick_B(const EvoParams& P, const CUtensorMap& map, int B, cudaStream_t st) {
-  SNK_DISPATCH_B(B, (launch_brick<D, W, S, SLAB, CH, L>(P, map, st)))
-}
-
-// ------------------------------------------------------------------ TMA descriptor
-PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
-  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-  static std::once_flag once;
-  std::call_once(once, [] {
-    void* p = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
-  });
-  return fn;
-}
-
-bool make_brick_map(const snk_grid* g, const uint16_t* img, int S, CUtensorMap* map) {
-  auto enc = get_encode();
-  if (!enc) return false;
-  const int D = g->dim;
-  if ((g->n[0] * 2) % 16 != 0 || (reinterpret_cast<uintptr_t>(img) & 15) != 0) return false;
-  cuuint64_t dims[3] = {(cuuint64_t)g->n[0], (cuuint64_t)g->n[1], (cuuint64_t)g->nz_buf};
-  cuuint64_t strides[2] = {(cuuint64_t)g->n[0] * 2, (cuuint64_t)(g->n[0] * g->n[1] * 2)};
-  cuuint32_t box[3] = {(cuuint32_t)S, (cuuint32_t)S, (cuuint32_t)S};
-  cuuint32_t estr[3] = {1, 1, 1};
-  const CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT16, (cuuint32_t)D, const_cast<uint16_t*>(img),
-                         dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                         CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
-                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  return r == CUDA_SUCCESS;
+int32_t brick_B(const EvoParams& P, int B, cudaStream_t st) {
+  SNK_DISPATCH_B(B, (launch_brick<D, W, S, SLAB, CH, L>(P, st)))
 }
 
 }  // namespace
@@ -736,22 +681,22 @@ int32_t evolve_impl(const snk_grid* g, const snk_params* p, const uint16_t* d_im
   if (D == 3 && g->n[2] < 2) return fail(SNK_SHAPE, "3D needs nz >= 2");
   if (g->n[0] * g->n[1] * g->nz_buf >= ((int64_t)1 << 32)) return fail(SNK_SHAPE, "buffer too large");
   const bool slab = !(g->z_lo == 0 && g->nz_buf == g->n[2]);
-  // kernel choice: 0 auto, 1 warp (global gathers), 2 brick (TMA + shared memory)
+  // kernel choice: 0 auto, 1 warp (global gathers), 2 brick (shared memory)
   const uint32_t variant = p->kernel_variant;
   const int Wb = p->cta_warps > 0 ? p->cta_warps : 4;
   const int Bb = p->n_samples / (32 * Wb);
-  const int Sb = D == 3 ? 32 : 64;
-  CUtensorMap map;
+  // the brick kernel copies 4-byte words from an even x origin: needs even nx
+  // and a 4-byte aligned image
   const bool brick_ok = variant != 1 && Bb >= 1 && Bb <= 128 && (Wb == 4 || Wb == 8) &&
-                        make_brick_map(g, d_image, Sb, &map);
+                        g->n[0] % 2 == 0 && (reinterpret_cast<uintptr_t>(d_image) & 3) == 0;
   if (variant == 2 && !brick_ok) return fail(SNK_CONFIG, "brick kernel unavailable for this volume");
   if (brick_ok) {
     if (D == 3) {
-      if (Wb == 4) return slab ? brick_B<3, 4, 32, true>(P, map, Bb, st) : brick_B<3, 4, 32, false>(P, map, Bb, st);
-      return slab ? brick_B<3, 8, 32, true>(P, map, Bb, st) : brick_B<3, 8, 32, false>(P, map, Bb, st);
+      if (Wb == 4) return slab ? brick_B<3, 4, 32, true>(P, Bb, st) : brick_B<3, 4, 32, false>(P, Bb, st);
+      return slab ? brick_B<3, 8, 32, true>(P, Bb, st) : brick_B<3, 8, 32, false>(P, Bb, st);
     }
-    if (Wb == 4) return brick_B<2, 4, 64, false>(P, map, Bb, st);
-    return brick_B<2, 8, 64, false>(P, map, Bb, st);
+    if (Wb == 4) return brick_B<2, 4, 64, false>(P, Bb, st);
+    return brick_B<2, 8, 64, false>(P, Bb, st);
   }
   const int W = evolve_warps_per_cell(p, n);
   const int B = p->n_samples / (32 * W);

@@ -5,10 +5,11 @@
 // Arithmetic is IEEE fp64 with explicit _rn intrinsics (no contraction), so the
 // map is bit-identical to the definition.
 //
-// Mapping: detections are binned onto 8x8x8 voxel tiles (16x16 in 2D) by the
-// bounding box of their inner ball; one CTA per tile stages the tile's list in
-// shared memory and each thread resolves one voxel.  Output: int32 planes
-// [own_z0, own_z1), coalesced 32-bit stores.
+// Mapping: detections are binned onto 32x8x8-voxel tiles (2D: 32x32) by the
+// bounding box of their inner ball; one CTA (256 threads) per tile stages the
+// tile's list in shared memory; thread (x, y) walks the tile's 8 z-planes,
+// re-using dx^2 + dy^2 across planes.  Each warp stores 32 consecutive int32
+// (128 B) per plane: the output is streamed once (4 B/voxel, HBM-bound).
 #include <cmath>
 
 #include "common.cuh"
@@ -16,6 +17,9 @@
 namespace snk {
 
 namespace {
+
+constexpr int kTX = 32, kTY = 8, kTZ3 = 8, kTY2 = 32, kThreads = 256;
+constexpr int kStage = 256;
 
 struct TileGrid {
   int tx, ty, tz;      // tile dims (voxels)
@@ -68,25 +72,33 @@ __global__ void tile_fill_kernel(const snk_cell* __restrict__ dets, int64_t n, T
       }
 }
 
-constexpr int kStage = 256;
-
+// D = 3: tile 32x8x8, thread (x, y) walks 8 planes.  D = 2: tile 32x32x1, thread
+// handles 4 rows (y, y+8, y+16, y+24).
 template <int D>
-__global__ void __launch_bounds__(512) label_kernel(const snk_cell* __restrict__ dets, TileGrid G,
-                                                    const int64_t* __restrict__ offsets,
-                                                    const int* __restrict__ entries,
-                                                    int32_t* __restrict__ labels) {
+__global__ void __launch_bounds__(kThreads) label_kernel(const snk_cell* __restrict__ dets, TileGrid G,
+                                                         const int64_t* __restrict__ offsets,
+                                                         const int* __restrict__ entries,
+                                                         int32_t* __restrict__ labels) {
+  constexpr int NV = D == 3 ? kTZ3 : kTY2 / kTY;   // voxels per thread
   __shared__ double s_c[3][kStage];
   __shared__ double s_thr[kStage];
   __shared__ int s_idx[kStage];
   const int64_t tile = blockIdx.x;
   const int tx = (int)(tile % G.nt[0]), ty = (int)((tile / G.nt[0]) % G.nt[1]),
             tz = (int)(tile / ((int64_t)G.nt[0] * G.nt[1]));
-  const int lx = threadIdx.x % G.tx, ly = (threadIdx.x / G.tx) % G.ty, lz = threadIdx.x / (G.tx * G.ty);
-  const int x = tx * G.tx + lx, y = ty * G.ty + ly, z = G.z0 + tz * G.tz + lz;
-  const bool valid = x < G.nx && y < G.ny && z < G.z1;
-  const double px = (double)x, py = (double)y, pz = (double)z;
-  int best = -1;
-  double best_key = 0.0;
+  const int lx = threadIdx.x % kTX, ly = threadIdx.x / kTX;
+  const int x = tx * G.tx + lx;
+  int yv[NV], zv[NV];
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    yv[k] = D == 3 ? ty * G.ty + ly : ty * G.ty + ly + k * kTY;
+    zv[k] = D == 3 ? G.z0 + tz * G.tz + k : G.z0;
+  }
+  int best[NV];
+  double best_key[NV];
+#pragma unroll
+  for (int k = 0; k < NV; ++k) { best[k] = -1; best_key[k] = 0.0; }
+  const double px = (double)x;
   const int64_t e0 = offsets[tile], e1 = offsets[tile + 1];
   for (int64_t s = e0; s < e1; s += kStage) {
     const int cnt = (int)(e1 - s < kStage ? e1 - s : kStage);
@@ -101,33 +113,54 @@ __global__ void __launch_bounds__(512) label_kernel(const snk_cell* __restrict__
       s_idx[k] = i;
     }
     __syncthreads();
-    if (!valid) continue;
     for (int k = 0; k < cnt; ++k) {
-      const double dx = __dsub_rn(px, s_c[0][k]);
-      const double dy = __dsub_rn(py, s_c[1][k]);
-      double d2 = __dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy));
-      if (D == 3) {
-        const double dz = __dsub_rn(pz, s_c[2][k]);
-        d2 = __dadd_rn(d2, __dmul_rn(dz, dz));
-      }
       const double thr = s_thr[k];
-      if (d2 <= thr) {
-        const double key = __ddiv_rn(d2, thr);
-        const int i = s_idx[k];
-        if (best < 0 || key < best_key || (key == best_key && i < best)) {
-          best = i;
-          best_key = key;
+      const int i = s_idx[k];
+      const double dx = __dsub_rn(px, s_c[0][k]);
+      const double dx2 = __dmul_rn(dx, dx);
+      if (D == 3) {
+        const double dy = __dsub_rn((double)yv[0], s_c[1][k]);
+        const double dxy = __dadd_rn(dx2, __dmul_rn(dy, dy));   // d2 = (dx^2 + dy^2) + dz^2
+        if (!(dxy <= thr)) continue;                             // dz^2 >= 0: no plane can qualify
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+          const double dz = __dsub_rn((double)zv[v], s_c[2][k]);
+          const double d2 = __dadd_rn(dxy, __dmul_rn(dz, dz));
+          if (d2 <= thr) {
+            const double key = __ddiv_rn(d2, thr);
+            if (best[v] < 0 || key < best_key[v] || (key == best_key[v] && i < best[v])) {
+              best[v] = i;
+              best_key[v] = key;
+            }
+          }
+        }
+      } else {
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+          const double dy = __dsub_rn((double)yv[v], s_c[1][k]);
+          const double d2 = __dadd_rn(dx2, __dmul_rn(dy, dy));
+          if (d2 <= thr) {
+            const double key = __ddiv_rn(d2, thr);
+            if (best[v] < 0 || key < best_key[v] || (key == best_key[v] && i < best[v])) {
+              best[v] = i;
+              best_key[v] = key;
+            }
+          }
         }
       }
     }
   }
-  if (valid) labels[((int64_t)(z - G.z0) * G.ny + y) * G.nx + x] = best + 1;
+  if (x >= G.nx) return;
+#pragma unroll
+  for (int v = 0; v < NV; ++v)
+    if (yv[v] < G.ny && zv[v] < G.z1)
+      labels[((int64_t)(zv[v] - G.z0) * G.ny + yv[v]) * G.nx + x] = best[v] + 1;
 }
 
 TileGrid make_grid(const snk_grid* g) {
   TileGrid G;
-  if (g->dim == 3) { G.tx = 8; G.ty = 8; G.tz = 8; }
-  else { G.tx = 32; G.ty = 16; G.tz = 1; }
+  if (g->dim == 3) { G.tx = kTX; G.ty = kTY; G.tz = kTZ3; }
+  else { G.tx = kTX; G.ty = kTY2; G.tz = 1; }
   G.nx = (int)g->n[0];
   G.ny = (int)g->n[1];
   G.z0 = (int)g->own_z0;
@@ -154,7 +187,8 @@ size_t label_ws(const snk_grid* g, const snk_params* p, int64_t max_cells) {
   const TileGrid G = make_grid(g);
   const size_t ntiles = (size_t)G.nt[0] * G.nt[1] * std::max(G.nt[2], 1);
   const size_t ent = (size_t)std::max<int64_t>(max_cells, 1) * tiles_per_det_bound(g, p, G);
-  return ntiles * (2 * sizeof(int) + sizeof(int64_t)) + sizeof(int64_t) + ent * sizeof(int) + 4096;
+  return ntiles * (2 * sizeof(int) + sizeof(int64_t)) + sizeof(int64_t) + ent * sizeof(int) +
+         scan_ws((int64_t)ntiles) + 4096;
 }
 
 int32_t label_impl(const snk_grid* g, const snk_params* p, const snk_cell* d_dets, int64_t n,
@@ -166,6 +200,7 @@ int32_t label_impl(const snk_grid* g, const snk_params* p, const snk_cell* d_det
   int* counts = cv.take<int>(ntiles);
   int* cursor = cv.take<int>(ntiles);
   int64_t* offsets = cv.take<int64_t>(ntiles + 1);
+  void* stmp = cv.take<char>(scan_ws(ntiles));
   const size_t ent_cap = (size_t)std::max<int64_t>(n, 1) * tiles_per_det_bound(g, p, G);
   int* entries = cv.take<int>(ent_cap);
   if (cv.overflow || !d_ws) return fail(SNK_CAPACITY, "workspace too small for label");
@@ -175,7 +210,7 @@ int32_t label_impl(const snk_grid* g, const snk_params* p, const snk_cell* d_det
     tile_count_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(d_dets, n, G, counts);
     SNK_LAUNCH_CHECK("tile_count_kernel");
   }
-  SNK_TRY(scan_counts(counts, ntiles, offsets, st));
+  SNK_TRY(scan_counts(counts, ntiles, offsets, st, stmp));
   int64_t total = 0;
   SNK_CUDA_CHECK(cudaMemcpyAsync(&total, offsets + ntiles, sizeof total, cudaMemcpyDeviceToHost, st));
   SNK_CUDA_CHECK(cudaStreamSynchronize(st));
@@ -184,9 +219,8 @@ int32_t label_impl(const snk_grid* g, const snk_params* p, const snk_cell* d_det
     tile_fill_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(d_dets, n, G, offsets, cursor, entries);
     SNK_LAUNCH_CHECK("tile_fill_kernel");
   }
-  const int threads = G.tx * G.ty * G.tz;
-  if (g->dim == 3) label_kernel<3><<<(unsigned)ntiles, threads, 0, st>>>(d_dets, G, offsets, entries, d_labels);
-  else label_kernel<2><<<(unsigned)ntiles, threads, 0, st>>>(d_dets, G, offsets, entries, d_labels);
+  if (g->dim == 3) label_kernel<3><<<(unsigned)ntiles, kThreads, 0, st>>>(d_dets, G, offsets, entries, d_labels);
+  else label_kernel<2><<<(unsigned)ntiles, kThreads, 0, st>>>(d_dets, G, offsets, entries, d_labels);
   SNK_LAUNCH_CHECK("label_kernel");
   return SNK_OK;
 }

@@ -149,31 +149,6 @@ __global__ void __launch_bounds__(kCompactThreads) maxima_write_kernel(MaxArgs A
     }
 }
 
-// Exclusive scan of n block counts into int64 offsets (+ total at offsets[n]); one block.
-__global__ void __launch_bounds__(1024) scan_counts_kernel(const int* counts, int64_t n,
-                                                           int64_t* offsets) {
-  __shared__ int64_t part[1024];
-  const int t = threadIdx.x;
-  const int64_t per = (n + 1023) / 1024;
-  const int64_t b = t * per, e = min(n, b + per);
-  int64_t s = 0;
-  for (int64_t i = b; i < e; ++i) s += counts[i];
-  part[t] = s;
-  __syncthreads();
-  for (int o = 1; o < 1024; o <<= 1) {
-    int64_t y = t >= o ? part[t - o] : 0;
-    __syncthreads();
-    part[t] += y;
-    __syncthreads();
-  }
-  int64_t run = t > 0 ? part[t - 1] : 0;
-  for (int64_t i = b; i < e; ++i) {
-    offsets[i] = run;
-    run += counts[i];
-  }
-  if (t == 1023) offsets[n] = part[1023];
-}
-
 // LATTICE positions: o + i s per axis in double (no FMA), stored as fp32.
 __global__ void lattice_kernel(int64_t kx, int64_t ky, int64_t iz0, int64_t nzl, double ox,
                                double oy, double oz, double s, int dim, float* seeds) {
@@ -188,12 +163,12 @@ __global__ void lattice_kernel(int64_t kx, int64_t ky, int64_t iz0, int64_t nzl,
 }  // namespace
 
 size_t seeds_ws(const snk_grid* g, const snk_params* p) {
-  if (p->seed_mode != SNK_SEED_MAXIMA) return 256;
+  if (p->seed_mode != SNK_SEED_MAXIMA) return 0;
   const int64_t nvox = g->n[0] * g->n[1] * g->nz_buf;
   const int64_t nown = g->n[0] * g->n[1] * (g->own_z1 - g->own_z0);
   const int64_t nb = ceil_div(std::max<int64_t>(nown, 1), kChunk);
   return 2 * ((size_t)nvox * sizeof(uint16_t) + 256) + (size_t)nb * sizeof(int) +
-         (size_t)(nb + 1) * sizeof(int64_t) + 1024;
+         (size_t)(nb + 1) * sizeof(int64_t) + scan_ws(nb) + 1024;
 }
 
 int32_t seeds_impl(const snk_grid* g, const snk_params* p, const uint16_t* d_smooth,
@@ -264,6 +239,7 @@ int32_t seeds_impl(const snk_grid* g, const snk_params* p, const uint16_t* d_smo
   const int64_t nb = ceil_div(std::max<int64_t>(v1 - v0, 1), kChunk);
   int* counts = cv.take<int>(nb);
   int64_t* offsets = cv.take<int64_t>(nb + 1);
+  void* stmp = cv.take<char>(scan_ws(nb));
   if (cv.overflow) return fail(SNK_CAPACITY, "workspace too small for seeds");
   const unsigned grid = (unsigned)ceil_div(nvox, 256);
   // window clipped to the volume; z additionally to the buffer (only own planes are used)
@@ -297,8 +273,7 @@ int32_t seeds_impl(const snk_grid* g, const snk_params* p, const uint16_t* d_smo
   }
   maxima_count_kernel<<<(unsigned)nb, kCompactThreads, 0, st>>>(A, counts);
   SNK_LAUNCH_CHECK("maxima_count_kernel");
-  scan_counts_kernel<<<1, 1024, 0, st>>>(counts, nb, offsets);
-  SNK_LAUNCH_CHECK("scan_counts_kernel");
+  SNK_TRY(scan_counts(counts, nb, offsets, st, stmp));
   maxima_write_kernel<<<(unsigned)nb, kCompactThreads, 0, st>>>(A, offsets, d_seeds, cap);
   SNK_LAUNCH_CHECK("maxima_write_kernel");
   int64_t total = 0;
