@@ -160,9 +160,204 @@ __global__ void lattice_kernel(int64_t kx, int64_t ky, int64_t iz0, int64_t nzl,
   seeds[3 * t + 2] = dim == 3 ? __double2float_rn(__dadd_rn(oz, __dmul_rn((double)iz, s))) : 0.0f;
 }
 
+// ---------------------------------------------------------------------------
+// Fused MAXIMA (3D, w <= 8; 2D any w): one CTA per 64 x 16 output columns and
+// a 32-plane z-chunk of the owned planes.  Per input plane the (16+2w) x
+// (64+2w) tile is staged in shared memory (voxels outside the volume -> 0,
+// the neutral element of max, i.e. the clipped window), the x and y box-max
+// run there, and the y-maxima enter a per-thread register ring of 2w+1 planes
+// (with the centre values B), from which M = box max of plane z - w follows.
+// Candidates B >= thr && B == M get the tie check (an equal value earlier in
+// linear order inside the clipped window) from global memory; the result is a
+// bitmask (bit x of word (z, y, x/32)), so the compaction below emits seeds in
+// linear-index order.
+constexpr int kMX = 64, kMY = 16, kMZC = 32, kMThreads = 256;
+
+struct FusedArgs {
+  const uint16_t* B;
+  uint32_t* bits;          // words per row: ceil(nx/32); rows: own planes x ny
+  int nx, ny, nzg, z_lo, own_z0, own_z1, wpr;
+  int w;
+  uint32_t thr;
+  MaxArgs ma;              // for the tie check (is_seed semantics)
+};
+
+__device__ __forceinline__ bool tie_free(const MaxArgs& A, int x, int y, int z, uint16_t b) {
+  const int z0 = A.dim == 3 ? max(z - A.w, 0) : z;
+  const int y0 = max(y - A.w, 0), y1 = min(y + A.w, A.ny - 1);
+  const int x0 = max(x - A.w, 0), x1 = min(x + A.w, A.nx - 1);
+  for (int zz = z0; zz <= z; ++zz)
+    for (int yy = y0; yy <= (zz == z ? y : y1); ++yy) {
+      const uint16_t* row = A.B + ((int64_t)(zz - A.z_lo) * A.ny + yy) * A.nx;
+      const int xe = (zz == z && yy == y) ? x - 1 : x1;
+      for (int xx = x0; xx <= xe; ++xx)
+        if (__ldg(row + xx) == b) return false;
+    }
+  return true;
+}
+
+// K = 2W+1 z-ring (3D) ; W = 0 selects the 2D kernel with runtime window
+template <int D, int W>
+__global__ void __launch_bounds__(kMThreads) maxima_fused_kernel(FusedArgs A) {
+  constexpr int K = 2 * W + 1;
+  extern __shared__ uint16_t sm[];
+  const int w = D == 3 ? W : A.w;
+  const int RX = kMX + 2 * w, RY = kMY + 2 * w;
+  uint16_t* s_in = sm;                   // [RY][RX]
+  uint16_t* s_x = sm + RY * RX;          // [RY][kMX]
+  const int x0 = blockIdx.x * kMX, y0 = blockIdx.y * kMY;
+  const int z0 = A.own_z0 + blockIdx.z * kMZC;
+  const int tx = threadIdx.x % kMX, ty = threadIdx.x / kMX;
+  const int lane = threadIdx.x & 31;
+  const int zend = D == 3 ? min(z0 + kMZC, A.own_z1) : z0 + 1;
+  const int nplanes = (zend - z0) + 2 * (D == 3 ? W : 0);
+  uint32_t ring[K][4], ringb[K][4];
+  auto plane = [&](int zin, uint32_t* ym, uint32_t* yb) {
+    const bool valid = zin >= 0 && zin < A.nzg;
+    const uint16_t* src = A.B + (int64_t)(zin - A.z_lo) * A.nx * A.ny;
+    __syncthreads();
+    for (int e = threadIdx.x; e < RY * RX; e += kMThreads) {
+      const int r = e / RX, c = e % RX;
+      const int gy = y0 - w + r, gx = x0 - w + c;
+      s_in[e] = (valid && gy >= 0 && gy < A.ny && gx >= 0 && gx < A.nx) ? __ldg(src + (int64_t)gy * A.nx + gx) : 0;
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < RY * kMX; e += kMThreads) {
+      const int r = e / kMX, c = e % kMX;
+      uint32_t m = 0;
+      for (int i = 0; i <= 2 * w; ++i) m = max(m, (uint32_t)s_in[r * RX + c + i]);
+      s_x[e] = (uint16_t)m;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      uint32_t m = 0;
+      const int r = ty * 4 + k;
+      for (int i = 0; i <= 2 * w; ++i) m = max(m, (uint32_t)s_x[(r + i) * kMX + tx]);
+      ym[k] = m;
+      yb[k] = s_in[(r + w) * RX + tx + w];
+    }
+  };
+  auto emit = [&](int zo, const uint32_t* M, const uint32_t* Bv) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int x = x0 + tx, y = y0 + ty * 4 + k;
+      bool seed = false;
+      if (x < A.nx && y < A.ny && Bv[k] >= A.thr && Bv[k] == M[k])
+        seed = tie_free(A.ma, x, y, zo, (uint16_t)Bv[k]);
+      const unsigned m = __ballot_sync(0xffffffffu, seed);
+      if (lane == 0 && y < A.ny && x < A.nx)
+        A.bits[((int64_t)(zo - A.own_z0) * A.ny + y) * A.wpr + (x >> 5)] = m;
+    }
+  };
+  if (D == 2) {
+    uint32_t ym[4], yb[4];
+    plane(z0, ym, yb);
+    emit(z0, ym, yb);
+    return;
+  }
+  for (int base = 0; base < nplanes; base += K) {
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+      const int pi = base + j;
+      if (pi >= nplanes) break;
+      plane(z0 - W + pi, ring[j], ringb[j]);
+      if (pi >= 2 * W) {
+        uint32_t M[4], Bv[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          uint32_t m = 0;
+#pragma unroll
+          for (int i = 0; i < K; ++i) m = max(m, ring[(j + 1 + i) % K][k]);
+          M[k] = m;
+          Bv[k] = ringb[(j + 1 + W) % K][k];
+        }
+        emit(z0 + pi - 2 * W, M, Bv);
+      }
+    }
+  }
+}
+
+// compaction of the bitmask: words in linear order, 1024 words per block
+__global__ void __launch_bounds__(1024) bits_count_kernel(const uint32_t* bits, int64_t nwords, int* counts) {
+  const int64_t i = (int64_t)blockIdx.x * 1024 + threadIdx.x;
+  int c = i < nwords ? __popc(bits[i]) : 0;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  __shared__ int ws[32];
+  if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = c;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    int v = ws[threadIdx.x];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (threadIdx.x == 0) counts[blockIdx.x] = v;
+  }
+}
+
+__global__ void __launch_bounds__(1024) bits_write_kernel(const uint32_t* bits, int64_t nwords, int wpr,
+                                                          int nx, int ny, int own_z0,
+                                                          const int64_t* offsets, float* seeds,
+                                                          int64_t cap) {
+  __shared__ int ws[32];
+  const int64_t i = (int64_t)blockIdx.x * 1024 + threadIdx.x;
+  const uint32_t word = i < nwords ? bits[i] : 0u;
+  const int c = __popc(word);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int x = c;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) ws[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    int v = ws[lane];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, v, o);
+      if (lane >= o) v += y;
+    }
+    ws[lane] = v;
+  }
+  __syncthreads();
+  int64_t o = offsets[blockIdx.x] + (warp > 0 ? ws[warp - 1] : 0) + x - c;
+  if (!word) return;
+  const int64_t row = i / wpr;                 // (z - own_z0) * ny + y
+  const int xw = (int)(i % wpr) * 32;
+  const float fy = (float)(row % ny), fz = (float)(row / ny + own_z0);
+  uint32_t m = word;
+  while (m) {
+    const int b = __ffs(m) - 1;
+    m &= m - 1;
+    if (o < cap) {
+      seeds[3 * o + 0] = (float)(xw + b);
+      seeds[3 * o + 1] = fy;
+      seeds[3 * o + 2] = fz;
+    }
+    ++o;
+  }
+  (void)nx;
+}
+
+bool fused_ok(const snk_grid* g, const snk_params* p) {
+  return (g->dim == 2 && p->seed_window <= 32) || (g->dim == 3 && p->seed_window >= 1 && p->seed_window <= 8);
+}
+
+int64_t fused_words(const snk_grid* g) {
+  return ceil_div(g->n[0], 32) * g->n[1] * std::max<int64_t>(g->own_z1 - g->own_z0, 0);
+}
+
 }  // namespace
 
 size_t seeds_ws(const snk_grid* g, const snk_params* p) {
+  if (p->seed_mode == SNK_SEED_MAXIMA && fused_ok(g, p)) {
+    const int64_t nw = fused_words(g);
+    const int64_t nb = ceil_div(std::max<int64_t>(nw, 1), 1024);
+    return (size_t)nw * 4 + 256 + (size_t)nb * sizeof(int) + 256 + (size_t)(nb + 1) * sizeof(int64_t) + 256 +
+           scan_ws(nb) + 1024;
+  }
   if (p->seed_mode != SNK_SEED_MAXIMA) return 0;
   const int64_t nvox = g->n[0] * g->n[1] * g->nz_buf;
   const int64_t nown = g->n[0] * g->n[1] * (g->own_z1 - g->own_z0);
@@ -233,6 +428,70 @@ int32_t seeds_impl(const snk_grid* g, const snk_params* p, const uint16_t* d_smo
   const int64_t plane = (int64_t)nx * ny;
   const int64_t nvox = plane * nzb;
   Carve cv(d_ws, ws_bytes);
+  if (fused_ok(g, p)) {
+    if (g->own_z1 <= g->own_z0) {
+      *n_out = 0;
+      return SNK_OK;
+    }
+    const int64_t nw = fused_words(g);
+    const int64_t nbw = ceil_div(nw, 1024);
+    uint32_t* bits = cv.take<uint32_t>(nw);
+    int* wcounts = cv.take<int>(nbw);
+    int64_t* woff = cv.take<int64_t>(nbw + 1);
+    void* stmp = cv.take<char>(scan_ws(nbw));
+    if (cv.overflow) return fail(SNK_CAPACITY, "workspace too small for seeds");
+    FusedArgs F;
+    F.B = d_smooth;
+    F.bits = bits;
+    F.nx = nx;
+    F.ny = ny;
+    F.nzg = (int)g->n[2];
+    F.z_lo = (int)g->z_lo;
+    F.own_z0 = (int)g->own_z0;
+    F.own_z1 = (int)g->own_z1;
+    F.wpr = (int)ceil_div(nx, 32);
+    F.w = w;
+    F.thr = p->seed_threshold;
+    F.ma.B = d_smooth;
+    F.ma.M = nullptr;
+    F.ma.nx = nx;
+    F.ma.ny = ny;
+    F.ma.nz_glob = (int)g->n[2];
+    F.ma.z_lo = (int)g->z_lo;
+    F.ma.w = w;
+    F.ma.dim = dim;
+    F.ma.thr = p->seed_threshold;
+    const int RX = kMX + 2 * w, RY = kMY + 2 * w;
+    const size_t smem = (size_t)(RY * RX + RY * kMX) * sizeof(uint16_t);
+    dim3 grid((unsigned)ceil_div(nx, kMX), (unsigned)ceil_div(ny, kMY),
+              dim == 3 ? (unsigned)ceil_div(g->own_z1 - g->own_z0, kMZC) : 1u);
+    if (dim == 2) {
+      maxima_fused_kernel<2, 0><<<grid, kMThreads, smem, st>>>(F);
+    } else {
+      switch (w) {
+        case 1: maxima_fused_kernel<3, 1><<<grid, kMThreads, smem, st>>>(F); break;
+        case 2: maxima_fused_kernel<3, 2><<<grid, kMThreads, smem, st>>>(F); break;
+        case 3: maxima_fused_kernel<3, 3><<<grid, kMThreads, smem, st>>>(F); break;
+        case 4: maxima_fused_kernel<3, 4><<<grid, kMThreads, smem, st>>>(F); break;
+        case 5: maxima_fused_kernel<3, 5><<<grid, kMThreads, smem, st>>>(F); break;
+        case 6: maxima_fused_kernel<3, 6><<<grid, kMThreads, smem, st>>>(F); break;
+        case 7: maxima_fused_kernel<3, 7><<<grid, kMThreads, smem, st>>>(F); break;
+        default: maxima_fused_kernel<3, 8><<<grid, kMThreads, smem, st>>>(F); break;
+      }
+    }
+    SNK_LAUNCH_CHECK("maxima_fused_kernel");
+    bits_count_kernel<<<(unsigned)nbw, 1024, 0, st>>>(bits, nw, wcounts);
+    SNK_LAUNCH_CHECK("bits_count_kernel");
+    SNK_TRY(scan_counts(wcounts, nbw, woff, st, stmp));
+    bits_write_kernel<<<(unsigned)nbw, 1024, 0, st>>>(bits, nw, F.wpr, nx, ny, F.own_z0, woff, d_seeds, cap);
+    SNK_LAUNCH_CHECK("bits_write_kernel");
+    int64_t total = 0;
+    SNK_CUDA_CHECK(cudaMemcpyAsync(&total, woff + nbw, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    SNK_CUDA_CHECK(cudaStreamSynchronize(st));
+    *n_out = total;
+    if (total > cap) return fail(SNK_CAPACITY, "seed buffer too small");
+    return SNK_OK;
+  }
   uint16_t* ta = cv.take<uint16_t>(nvox);
   uint16_t* tb = cv.take<uint16_t>(nvox);
   const int64_t v0 = (g->own_z0 - g->z_lo) * plane, v1 = (g->own_z1 - g->z_lo) * plane;

@@ -150,10 +150,168 @@ __global__ void __launch_bounds__(256) resample_kernel(const uint16_t* __restric
 
 inline unsigned grid_for(int64_t n, int block) { return (unsigned)ceil_div(n, block); }
 
+// ---------------------------------------------------------------------------
+// Fused 3D blur: one CTA per 64 x 16 output columns and a 32-plane z-chunk.
+// Per input plane: the (16+2H) x (64+2H) tile (clamped coordinates) is
+// staged in shared memory, the x pass and the y pass run there (each rounding
+// to an integer, exactly as the three separate passes), and the y-passed
+// values enter a per-thread register ring of 2H+1 planes, from which the z
+// pass produces output plane z - H.  Each voxel is read from HBM ~once and
+// written once (the three-pass version moved it 3x each way).
+constexpr int kBX = 64, kBY = 16, kBZC = 32, kBThreads = 256;
+
+template <int H>
+__global__ void __launch_bounds__(kBThreads) blur3d_fused_kernel(const uint16_t* __restrict__ in,
+                                                                 uint16_t* __restrict__ out, int nx,
+                                                                 int ny, int nz) {
+  constexpr int K = 2 * H + 1, RX = kBX + 2 * H, RY = kBY + 2 * H;
+  __shared__ uint16_t s_in[RY][RX];
+  __shared__ uint16_t s_x[RY][kBX];
+  const int x0 = blockIdx.x * kBX, y0 = blockIdx.y * kBY, z0 = blockIdx.z * kBZC;
+  const int tx = threadIdx.x % kBX, ty = threadIdx.x / kBX;   // 4 rows of outputs per thread
+  const int zend = min(z0 + kBZC, nz);
+  const int nplanes = (zend - z0) + 2 * H;
+  uint32_t ring[K][4];
+  for (int base = 0; base < nplanes; base += K) {
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+      const int pi = base + j;
+      if (pi >= nplanes) break;
+      const int zin = min(max(z0 - H + pi, 0), nz - 1);
+      const uint16_t* src = in + (int64_t)zin * nx * ny;
+      __syncthreads();   // previous plane's x pass finished with s_in, y pass with s_x
+      for (int e = threadIdx.x; e < RY * RX; e += kBThreads) {
+        const int r = e / RX, c = e % RX;
+        const int gy = min(max(y0 - H + r, 0), ny - 1), gx = min(max(x0 - H + c, 0), nx - 1);
+        s_in[r][c] = __ldg(src + (int64_t)gy * nx + gx);
+      }
+      __syncthreads();
+      for (int e = threadIdx.x; e < RY * kBX; e += kBThreads) {
+        const int r = e / kBX, c = e % kBX;
+        uint32_t acc = 8192;
+#pragma unroll
+        for (int i = 0; i < K; ++i) acc += (uint32_t)c_taps[i] * s_in[r][c + i];
+        s_x[r][c] = (uint16_t)(acc >> 14);
+      }
+      __syncthreads();
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        uint32_t acc = 8192;
+#pragma unroll
+        for (int i = 0; i < K; ++i) acc += (uint32_t)c_taps[i] * s_x[ty * 4 + k + i][tx];
+        ring[j][k] = acc >> 14;
+      }
+      if (pi >= 2 * H) {
+        const int zo = z0 + pi - 2 * H;
+        uint16_t* dst = out + ((int64_t)zo * ny + y0 + ty * 4) * nx + x0 + tx;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          uint32_t acc = 8192;
+#pragma unroll
+          for (int i = 0; i < K; ++i) acc += (uint32_t)c_taps[i] * ring[(j + 1 + i) % K][k];
+          if (x0 + tx < nx && y0 + ty * 4 + k < ny) dst[(int64_t)k * nx] = (uint16_t)(acc >> 14);
+        }
+      }
+    }
+  }
+}
+
+// 2D: one plane, the same staging for the x and y passes.
+template <int H>
+__global__ void __launch_bounds__(kBThreads) blur2d_fused_kernel(const uint16_t* __restrict__ in,
+                                                                 uint16_t* __restrict__ out, int nx,
+                                                                 int ny) {
+  constexpr int K = 2 * H + 1, RX = kBX + 2 * H, RY = kBY + 2 * H;
+  __shared__ uint16_t s_in[RY][RX];
+  __shared__ uint16_t s_x[RY][kBX];
+  const int x0 = blockIdx.x * kBX, y0 = blockIdx.y * kBY;
+  const int tx = threadIdx.x % kBX, ty = threadIdx.x / kBX;
+  for (int e = threadIdx.x; e < RY * RX; e += kBThreads) {
+    const int r = e / RX, c = e % RX;
+    const int gy = min(max(y0 - H + r, 0), ny - 1), gx = min(max(x0 - H + c, 0), nx - 1);
+    s_in[r][c] = __ldg(in + (int64_t)gy * nx + gx);
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < RY * kBX; e += kBThreads) {
+    const int r = e / kBX, c = e % kBX;
+    uint32_t acc = 8192;
+#pragma unroll
+    for (int i = 0; i < K; ++i) acc += (uint32_t)c_taps[i] * s_in[r][c + i];
+    s_x[r][c] = (uint16_t)(acc >> 14);
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    uint32_t acc = 8192;
+#pragma unroll
+    for (int i = 0; i < K; ++i) acc += (uint32_t)c_taps[i] * s_x[ty * 4 + k + i][tx];
+    if (x0 + tx < nx && y0 + ty * 4 + k < ny)
+      out[(int64_t)(y0 + ty * 4 + k) * nx + x0 + tx] = (uint16_t)(acc >> 14);
+  }
+}
+
+// Gradient magnitude, tiled: the (16+2) x (64+2) smoothed neighbourhood of
+// three consecutive planes is staged in shared memory (plane ring), each
+// smoothed voxel is read ~once from L2/HBM.
+template <int D>
+__global__ void __launch_bounds__(kBThreads) gradmag_tiled_kernel(const uint16_t* __restrict__ B,
+                                                                  uint16_t* __restrict__ G, int nx,
+                                                                  int ny, int nz) {
+  constexpr int RX = kBX + 2, RY = kBY + 2;
+  __shared__ uint16_t s[3][RY][RX];
+  const int x0 = blockIdx.x * kBX, y0 = blockIdx.y * kBY, z0 = blockIdx.z * kBZC;
+  const int tx = threadIdx.x % kBX, ty = threadIdx.x / kBX;
+  const int zend = D == 3 ? min(z0 + kBZC, nz) : 1;
+  auto load = [&](int slot, int zp) {
+    const int zc = min(max(zp, 0), nz - 1);
+    const uint16_t* src = B + (int64_t)zc * nx * ny;
+    for (int e = threadIdx.x; e < RY * RX; e += kBThreads) {
+      const int r = e / RX, c = e % RX;
+      const int gy = min(max(y0 - 1 + r, 0), ny - 1), gx = min(max(x0 - 1 + c, 0), nx - 1);
+      s[slot][r][c] = __ldg(src + (int64_t)gy * nx + gx);
+    }
+  };
+  if (D == 3) load(0, z0 - 1);
+  load(1, z0);
+  for (int z = z0; z < zend; ++z) {
+    const int mid = (z - z0 + 1) % 3, prv = (z - z0) % 3, nxt = (z - z0 + 2) % 3;
+    if (D == 3) load(nxt, z + 1);
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int r = ty * 4 + k + 1, c = tx + 1;
+      const int gx = (int)s[mid][r][c + 1] - (int)s[mid][r][c - 1];
+      const int gy = (int)s[mid][r + 1][c] - (int)s[mid][r - 1][c];
+      uint64_t ss = (uint64_t)((int64_t)gx * gx) + (uint64_t)((int64_t)gy * gy);
+      if (D == 3) {
+        const int gz = (int)s[nxt][r][c] - (int)s[prv][r][c];
+        ss += (uint64_t)((int64_t)gz * gz);
+      }
+      if (x0 + tx < nx && y0 + r - 1 < ny)
+        G[((int64_t)z * ny + y0 + r - 1) * nx + x0 + tx] = (uint16_t)((isqrt_u64(ss) + 1) >> 1);
+    }
+    __syncthreads();
+  }
+}
+
+template <int H>
+int32_t launch_fused_blur(const snk_grid* g, const uint16_t* d_in, uint16_t* d_out, cudaStream_t st) {
+  const int nx = (int)g->n[0], ny = (int)g->n[1], nz = (int)g->nz_buf;
+  if (g->dim == 3) {
+    dim3 grid((unsigned)ceil_div(nx, kBX), (unsigned)ceil_div(ny, kBY), (unsigned)ceil_div(nz, kBZC));
+    blur3d_fused_kernel<H><<<grid, kBThreads, 0, st>>>(d_in, d_out, nx, ny, nz);
+  } else {
+    dim3 grid((unsigned)ceil_div(nx, kBX), (unsigned)ceil_div(ny, kBY));
+    blur2d_fused_kernel<H><<<grid, kBThreads, 0, st>>>(d_in, d_out, nx, ny);
+  }
+  SNK_LAUNCH_CHECK("blur_fused_kernel");
+  return SNK_OK;
+}
+
 }  // namespace
 
 size_t preprocess_ws(const snk_grid* g, const snk_params* p) {
-  (void)p;
+  if (p->sigma > 0 && std::ceil(4.0 * p->sigma) <= 8) return 0;   // fused kernel: no scratch
   return (size_t)g->n[0] * g->n[1] * g->nz_buf * sizeof(uint16_t) + 256;
 }
 
@@ -167,28 +325,45 @@ int32_t preprocess_impl(const snk_grid* g, const snk_params* p, const uint16_t* 
   const int nx = (int)g->n[0], ny = (int)g->n[1], nz = (int)g->nz_buf;
   const int64_t nvox = (int64_t)nx * ny * nz;
   Carve cv(d_ws, ws_bytes);
-  uint16_t* tmp = cv.take<uint16_t>(nvox);
+  uint16_t* tmp = h > 8 ? cv.take<uint16_t>(nvox) : nullptr;
   if (cv.overflow) return fail(SNK_CAPACITY, "workspace too small for preprocess");
-  const int64_t pairs = (int64_t)((nx + 1) / 2) * ny * nz;
-  const unsigned grid = grid_for(pairs, 256);
-  if (g->dim == 3) {
-    // x: in -> smooth, y: smooth -> tmp, z: tmp -> smooth
-    blur_pass_kernel<0><<<grid, 256, 0, st>>>(d_in, d_smooth, nx, ny, nz, h);
-    SNK_LAUNCH_CHECK("blur_pass_kernel<x>");
-    blur_pass_kernel<1><<<grid, 256, 0, st>>>(d_smooth, tmp, nx, ny, nz, h);
-    SNK_LAUNCH_CHECK("blur_pass_kernel<y>");
-    blur_pass_kernel<2><<<grid, 256, 0, st>>>(tmp, d_smooth, nx, ny, nz, h);
-    SNK_LAUNCH_CHECK("blur_pass_kernel<z>");
+  if (h == 0) {
+    SNK_CUDA_CHECK(cudaMemcpyAsync(d_smooth, d_in, nvox * sizeof(uint16_t), cudaMemcpyDeviceToDevice, st));
+  } else if (h <= 8) {
+    switch (h) {
+      case 1: SNK_TRY(launch_fused_blur<1>(g, d_in, d_smooth, st)); break;
+      case 2: SNK_TRY(launch_fused_blur<2>(g, d_in, d_smooth, st)); break;
+      case 3: SNK_TRY(launch_fused_blur<3>(g, d_in, d_smooth, st)); break;
+      case 4: SNK_TRY(launch_fused_blur<4>(g, d_in, d_smooth, st)); break;
+      case 5: SNK_TRY(launch_fused_blur<5>(g, d_in, d_smooth, st)); break;
+      case 6: SNK_TRY(launch_fused_blur<6>(g, d_in, d_smooth, st)); break;
+      case 7: SNK_TRY(launch_fused_blur<7>(g, d_in, d_smooth, st)); break;
+      default: SNK_TRY(launch_fused_blur<8>(g, d_in, d_smooth, st)); break;
+    }
   } else {
-    blur_pass_kernel<0><<<grid, 256, 0, st>>>(d_in, tmp, nx, ny, nz, h);
-    SNK_LAUNCH_CHECK("blur_pass_kernel<x>");
-    blur_pass_kernel<1><<<grid, 256, 0, st>>>(tmp, d_smooth, nx, ny, nz, h);
-    SNK_LAUNCH_CHECK("blur_pass_kernel<y>");
+    // wide kernels (sigma > 2): three separable passes through the workspace
+    const int64_t pairs = (int64_t)((nx + 1) / 2) * ny * nz;
+    const unsigned grid = grid_for(pairs, 256);
+    if (g->dim == 3) {
+      blur_pass_kernel<0><<<grid, 256, 0, st>>>(d_in, d_smooth, nx, ny, nz, h);
+      SNK_LAUNCH_CHECK("blur_pass_kernel<x>");
+      blur_pass_kernel<1><<<grid, 256, 0, st>>>(d_smooth, tmp, nx, ny, nz, h);
+      SNK_LAUNCH_CHECK("blur_pass_kernel<y>");
+      blur_pass_kernel<2><<<grid, 256, 0, st>>>(tmp, d_smooth, nx, ny, nz, h);
+      SNK_LAUNCH_CHECK("blur_pass_kernel<z>");
+    } else {
+      blur_pass_kernel<0><<<grid, 256, 0, st>>>(d_in, tmp, nx, ny, nz, h);
+      SNK_LAUNCH_CHECK("blur_pass_kernel<x>");
+      blur_pass_kernel<1><<<grid, 256, 0, st>>>(tmp, d_smooth, nx, ny, nz, h);
+      SNK_LAUNCH_CHECK("blur_pass_kernel<y>");
+    }
   }
   if (d_gradmag) {
-    if (g->dim == 3) gradmag_kernel<3><<<grid_for(nvox, 256), 256, 0, st>>>(d_smooth, d_gradmag, nx, ny, nz);
-    else gradmag_kernel<2><<<grid_for(nvox, 256), 256, 0, st>>>(d_smooth, d_gradmag, nx, ny, nz);
-    SNK_LAUNCH_CHECK("gradmag_kernel");
+    dim3 grid((unsigned)ceil_div(nx, kBX), (unsigned)ceil_div(ny, kBY),
+              g->dim == 3 ? (unsigned)ceil_div(nz, kBZC) : 1u);
+    if (g->dim == 3) gradmag_tiled_kernel<3><<<grid, kBThreads, 0, st>>>(d_smooth, d_gradmag, nx, ny, nz);
+    else gradmag_tiled_kernel<2><<<grid, kBThreads, 0, st>>>(d_smooth, d_gradmag, nx, ny, nz);
+    SNK_LAUNCH_CHECK("gradmag_tiled_kernel");
   }
   return SNK_OK;
 }
