@@ -50,6 +50,7 @@ struct EvoParams {
   float fnx1, fny1, fnz1;        // n - 1
   float mx2, my2, mz2;           // 2^23 + (n - 2): clamp of the magic floor
   float r0, half_dR, inv_dR, inv_rho_dR, eps0, max_step, r_min, r_max, leash, conv_tol;
+  float k12_rho_dR, km6_dR, k6_dR;   // 12/(rho dR), -6/dR, 6/dR
   float vscale;                  // iscale * (4/3 pi | pi) / N
   int T;
   uint32_t rk0[10], rk1[10];     // Philox round keys (seed + r * Weyl)
@@ -69,9 +70,11 @@ struct CellIt {
   float cx, cy, cz;
   float rho_s;          // R + dR/2: radius of the sampled ball
   float a;              // -(R - dR/2)/dR: offset of both ramp coordinates
+  float lg2_rho_s;      // log2(rho_s)
   uint32_t p0, p1, p3;  // Philox round-1 words that depend only on (n, id)
-  // brick: magic-offset origin (2^23 + b) per axis, as integers
-  uint32_t ob[3];
+  // brick: sum over axes of (2^23 + b_a) * stride_a (mod 2^32), so that the
+  // brick index of magic-floored coordinates is rx + ry SX + rz SP - boff
+  uint32_t boff;
 };
 
 __device__ __forceinline__ float sqrt_approx(float x) {
@@ -149,7 +152,7 @@ __device__ __forceinline__ Draw draw(const EvoParams& P, const CellIt& C, uint32
     const float st = __fmul_rn(2.0f, sqrt_approx(__fmaf_rn(-u0, u0, u0)));
     d.ox = __fmul_rn(st, cs);
     d.oy = __fmul_rn(st, sn);
-    d.t = __fmul_rn(C.rho_s, ex2_approx(__fmul_rn(lg2_approx(u2), 0.333333343f)));
+    d.t = ex2_approx(__fmaf_rn(lg2_approx(u2), 0.333333343f, C.lg2_rho_s));   // rho_s cbrt(u2)
   } else {
     d.ox = cs;
     d.oy = sn;
@@ -165,13 +168,14 @@ __device__ __forceinline__ Acc leaves(const EvoParams& P, const CellIt& C, const
   // tau_o = (t - (R - dR/2))/dR,  tau_i = (t - rho (R - dR/2))/(rho dR) = t/(rho dR) + a
   const float uo = __saturatef(__fmaf_rn(d.t, P.inv_dR, C.a));
   const float ui = __saturatef(__fmaf_rn(d.t, P.inv_rho_dR, C.a));
-  const float s3o = __fmul_rn(__fmul_rn(uo, uo), __fmaf_rn(-2.0f, uo, 3.0f));
-  const float s3i = __fmul_rn(__fmul_rn(ui, ui), __fmaf_rn(-2.0f, ui, 3.0f));
-  const float d3o = __fmul_rn(6.0f, __fmaf_rn(-uo, uo, uo));
-  const float d3i = __fmul_rn(6.0f, __fmaf_rn(-ui, ui, ui));
+  // q = u (1 - u): s3 = 3u^2 - 2u^3 = u (u + 2q), s3' = 6q
+  const float qo = __fmaf_rn(-uo, uo, uo), qi = __fmaf_rn(-ui, ui, ui);
+  const float s3o = __fmul_rn(uo, __fmaf_rn(2.0f, qo, uo));
+  const float s3i = __fmul_rn(ui, __fmaf_rn(2.0f, qi, ui));
   const float S = __fsub_rn(__fmaf_rn(2.0f, s3i, -s3o), 1.0f);             // (1-s3o) - 2(1-s3i)
-  const float Sr = __fmaf_rn(__fmul_rn(2.0f, P.inv_rho_dR), d3i, __fmul_rn(-P.inv_dR, d3o));
-  const float SR = __fmul_rn(__fmaf_rn(-2.0f, d3i, d3o), P.inv_dR);
+  // S_r = -6 qo/dR + 12 qi/(rho dR),  S_R = 6 (qo - 2 qi)/dR
+  const float Sr = __fmaf_rn(P.k12_rho_dR, qi, __fmul_rn(P.km6_dR, qo));
+  const float SR = __fmul_rn(__fmaf_rn(-2.0f, qi, qo), P.k6_dR);
   const float w = __fmul_rn(Sr, tri);
   Acc a;
   a.a0 = __fmul_rn(S, tri);
@@ -199,9 +203,10 @@ __device__ __forceinline__ Acc sample_leaf(const EvoParams& P, const CellIt& C, 
   if (MODE == G_BRICK_CLAMP || MODE == G_BRICK_FAST) {
     // brick-local index; row stride SX = S + 2 and plane stride SX * S are immediates
     constexpr int SX = S + 2, SP = SX * S;
-    const uint32_t lx = rx - C.ob[0], ly = ry - C.ob[1];
-    uint32_t li = ly * SX + lx;
-    if (D == 3) li += (rz - C.ob[2]) * SP;
+    uint32_t li = ry * SX + rx;
+    if (D == 3) li += rz * SP;
+    li -= C.boff;
+    asm("" : "+r"(li));   // materialise li: the eight tap offsets become LDS immediates
     const uint16_t* p = brick + li;
     v000 = mag(p[0]);
     v100 = mag(p[1]);
@@ -344,7 +349,8 @@ __device__ __forceinline__ CellIt cell_iter(const EvoParams& P, const CellState&
   C.p0 = (uint32_t)(p1 >> 32) ^ (uint32_t)it ^ P.rk0[0];
   C.p1 = (uint32_t)p1;
   C.p3 = s.id_hi ^ P.rk1[0];
-  C.ob[0] = C.ob[1] = C.ob[2] = kMagicBits;
+  C.lg2_rho_s = lg2_approx(C.rho_s);
+  C.boff = 0;
   return C;
 }
 
@@ -489,7 +495,7 @@ __device__ __forceinline__ void load_brick(uint16_t* brick, const EvoParams& P, 
 }
 
 template <int D, int W, int S, bool SLAB, int CH, int L>
-__global__ void __launch_bounds__(32 * W) evolve_brick_kernel(const __grid_constant__ EvoParams P) {
+__global__ void __launch_bounds__(32 * W, W == 4 ? 3 : 1) evolve_brick_kernel(const __grid_constant__ EvoParams P) {
   constexpr int B = CH << L;
   constexpr int EXT[3] = {S + 2, S, S};             // brick extent per axis
   extern __shared__ __align__(16) uint16_t brick[];
@@ -541,8 +547,8 @@ __global__ void __launch_bounds__(32 * W) evolve_brick_kernel(const __grid_const
     }
     Acc part;
     if (inside) {
-#pragma unroll
-      for (int a = 0; a < D; ++a) C.ob[a] = kMagicBits + (uint32_t)b[a];
+      C.boff = (kMagicBits + (uint32_t)b[0]) + (kMagicBits + (uint32_t)b[1]) * (uint32_t)(S + 2);
+      if (D == 3) C.boff += (kMagicBits + (uint32_t)b[2]) * (uint32_t)((S + 2) * S);
       if (interior) part = lane_sum<D, G_BRICK_FAST, S, CH, L>(P, C, j0, brick, halo);
       else part = lane_sum<D, G_BRICK_CLAMP, S, CH, L>(P, C, j0, brick, halo);
     } else {
@@ -612,7 +618,19 @@ int32_t warp_W(const EvoParams& P, int W, int B, cudaStream_t st) {
 
 template <int D, int W, int S, bool SLAB>
 int32_t brick_B(const EvoParams& P, int B, cudaStream_t st) {
-  SNK_DISPATCH_B(B, (launch_brick<D, W, S, SLAB, CH, L>(P, st)))
+  // 8 samples per chunk: the brick kernel runs 12 warps/SM (shared memory
+  // bound), so each warp needs the ILP of 8 independent sample chains
+  switch (B) {
+    case 1: return launch_brick<D, W, S, SLAB, 1, 0>(P, st);
+    case 2: return launch_brick<D, W, S, SLAB, 2, 0>(P, st);
+    case 4: return launch_brick<D, W, S, SLAB, 4, 0>(P, st);
+    case 8: return launch_brick<D, W, S, SLAB, 8, 0>(P, st);
+    case 16: return launch_brick<D, W, S, SLAB, 8, 1>(P, st);
+    case 32: return launch_brick<D, W, S, SLAB, 8, 2>(P, st);
+    case 64: return launch_brick<D, W, S, SLAB, 8, 3>(P, st);
+    case 128: return launch_brick<D, W, S, SLAB, 8, 4>(P, st);
+    default: return fail(SNK_CONFIG, "samples per thread must be a power of two <= 128");
+  }
 }
 
 }  // namespace
@@ -662,6 +680,9 @@ int32_t evolve_impl(const snk_grid* g, const snk_params* p, const uint16_t* d_im
   P.half_dR = (float)(p->delta_R / 2.0);
   P.inv_dR = (float)(1.0 / p->delta_R);
   P.inv_rho_dR = (float)(1.0 / (rho * p->delta_R));
+  P.k12_rho_dR = (float)(12.0 / (rho * p->delta_R));
+  P.km6_dR = (float)(-6.0 / p->delta_R);
+  P.k6_dR = (float)(6.0 / p->delta_R);
   P.eps0 = (float)p->eps0;
   P.max_step = (float)p->max_step;
   P.r_min = (float)p->r_min;
