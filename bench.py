@@ -186,6 +186,7 @@ def run_ours(args):
         end.record(stream)
         torch.cuda.synchronize()
     launches = snk.snk_launch_count() - l0
+    evo_stats = snk.snk_evolve_stats(reset=True)
     total_ms = start.elapsed_time(end)
     evolve_ms = [e[1].elapsed_time(e[2]) for e in evs]
     n_cells = P.n_seeds
@@ -241,6 +242,7 @@ def run_ours(args):
         "cells_per_s": cells_per_s, "phase_ms": phase, "gpu_launches": int(launches),
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
         "generate_s": round(gen_s, 2),
+        "evolve_stats_per_step": {k: v / (args.steps + args.warmup) for k, v in evo_stats.items()},
     }
     return out
 

@@ -216,6 +216,12 @@ int32_t snk_run(int32_t dim, const int64_t n_raw[3], const double spacing[3],
 /* Diagnostics: number of kernel launches issued by this thread since load. */
 int64_t snk_launch_count(void);
 
+/* Diagnostics of the evolve brick kernel on the current device since the last
+ * reset: out4[0] = brick (re)loads, out4[1] = cell-iterations that gathered
+ * from global memory (sampled ball larger than the brick), out4[2..3] = 0.
+ * reset != 0 zeroes the counters.  Synchronous. */
+int32_t snk_evolve_stats(int64_t* out4, int32_t reset);
+
 #ifdef __cplusplus
 }
 #endif

@@ -110,6 +110,12 @@ const char* snk_status_string(int32_t s) {
 
 int64_t snk_launch_count(void) { return g_launches; }
 
+int32_t snk_evolve_stats(int64_t* out4, int32_t reset) {
+  clear_error();
+  if (!out4) return fail(SNK_CONFIG, "out4 is null");
+  return evolve_stats(out4, reset != 0);
+}
+
 int32_t snk_validate(const snk_grid* g, const snk_params* p) {
   clear_error();
   return validate(g, p);

@@ -97,6 +97,7 @@ int32_t label_impl(const snk_grid* g, const snk_params* p, const snk_cell* d_det
                    int32_t* d_labels, void* d_ws, size_t ws_bytes, cudaStream_t st);
 
 int evolve_warps_per_cell(const snk_params* p, int64_t n_cells);
+int32_t evolve_stats(int64_t out[4], bool reset);
 
 // exclusive scan of n int counts into n + 1 int64 offsets (offsets[n] = total);
 // tmp: scan_ws(n) bytes of scratch (nullptr: single-block scan)

@@ -40,6 +40,10 @@ constexpr uint32_t kW0 = 0x9E3779B9u, kW1 = 0xBB67AE85u;   // Weyl key bumps
 constexpr float kMagic = 8388608.0f;                        // 2^23
 constexpr uint32_t kMagicBits = 0x4B000000u;
 
+// diagnostics of the brick kernel: [0] brick (re)loads, [1] cell-iterations
+// that took the global-gather path (ball larger than the brick)
+__device__ unsigned long long g_evolve_stats[4];
+
 struct EvoParams {
   const uint16_t* img;
   const float* seeds;
@@ -544,6 +548,7 @@ __global__ void __launch_bounds__(32 * W, W == 4 ? 3 : 1) evolve_brick_kernel(co
       // every read of the old brick finished before last iteration's barrier
       load_brick<D, S>(brick, P, b[0], b[1], D == 3 ? b[2] : 0, zlo);
       inside = true;
+      if (threadIdx.x == 0) atomicAdd(&g_evolve_stats[0], 1ull);
     }
     Acc part;
     if (inside) {
@@ -553,6 +558,7 @@ __global__ void __launch_bounds__(32 * W, W == 4 ? 3 : 1) evolve_brick_kernel(co
       else part = lane_sum<D, G_BRICK_CLAMP, S, CH, L>(P, C, j0, brick, halo);
     } else {
       part = lane_sum<D, SLAB ? G_GLOBAL_SLAB : G_GLOBAL, S, CH, L>(P, C, j0, brick, halo);
+      if (threadIdx.x == 0) atomicAdd(&g_evolve_stats[1], 1ull);
     }
     Acc sum = warp_butterfly(part);
     if (lane == 0) xch[it & 1][wsub] = sum;
@@ -634,6 +640,17 @@ int32_t brick_B(const EvoParams& P, int B, cudaStream_t st) {
 }
 
 }  // namespace
+
+int32_t evolve_stats(int64_t out[4], bool reset) {
+  unsigned long long h[4];
+  SNK_CUDA_CHECK(cudaMemcpyFromSymbol(h, g_evolve_stats, sizeof h));
+  for (int i = 0; i < 4; ++i) out[i] = (int64_t)h[i];
+  if (reset) {
+    const unsigned long long z[4] = {0, 0, 0, 0};
+    SNK_CUDA_CHECK(cudaMemcpyToSymbol(g_evolve_stats, z, sizeof z));
+  }
+  return SNK_OK;
+}
 
 int evolve_warps_per_cell(const snk_params* p, int64_t n_cells) {
   int W = p->cta_warps;

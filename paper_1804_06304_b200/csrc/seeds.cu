@@ -211,16 +211,26 @@ __global__ void __launch_bounds__(kMThreads) maxima_fused_kernel(FusedArgs A) {
   const int lane = threadIdx.x & 31;
   const int zend = D == 3 ? min(z0 + kMZC, A.own_z1) : z0 + 1;
   const int nplanes = (zend - z0) + 2 * (D == 3 ? W : 0);
-  uint32_t ring[K][4], ringb[K][4];
-  auto plane = [&](int zin, uint32_t* ym, uint32_t* yb) {
+  uint32_t ring[K][4];
+  // 3D: the next plane's tile is prefetched into registers while this plane
+  // computes (the walk over planes is otherwise latency-bound)
+  constexpr int PER3 = ((kMY + 2 * W) * (kMX + 2 * W) + kMThreads - 1) / kMThreads;
+  uint16_t pf[D == 3 ? PER3 : 1];
+  auto fetch = [&](int zin) {
     const bool valid = zin >= 0 && zin < A.nzg;
     const uint16_t* src = A.B + (int64_t)(zin - A.z_lo) * A.nx * A.ny;
-    __syncthreads();
-    for (int e = threadIdx.x; e < RY * RX; e += kMThreads) {
-      const int r = e / RX, c = e % RX;
-      const int gy = y0 - w + r, gx = x0 - w + c;
-      s_in[e] = (valid && gy >= 0 && gy < A.ny && gx >= 0 && gx < A.nx) ? __ldg(src + (int64_t)gy * A.nx + gx) : 0;
+#pragma unroll
+    for (int q = 0; q < PER3; ++q) {
+      const int e = threadIdx.x + q * kMThreads;
+      if (e < RY * RX) {
+        const int r = e / RX, c = e % RX;
+        const int gy = y0 - w + r, gx = x0 - w + c;
+        pf[q] = (valid && gy >= 0 && gy < A.ny && gx >= 0 && gx < A.nx) ? __ldg(src + (int64_t)gy * A.nx + gx) : 0;
+      }
     }
+  };
+  // separable box max of the staged plane: x in shared memory, y per thread
+  auto boxmax = [&](uint32_t* ym) {
     __syncthreads();
     for (int e = threadIdx.x; e < RY * kMX; e += kMThreads) {
       const int r = e / kMX, c = e % kMX;
@@ -235,44 +245,58 @@ __global__ void __launch_bounds__(kMThreads) maxima_fused_kernel(FusedArgs A) {
       const int r = ty * 4 + k;
       for (int i = 0; i <= 2 * w; ++i) m = max(m, (uint32_t)s_x[(r + i) * kMX + tx]);
       ym[k] = m;
-      yb[k] = s_in[(r + w) * RX + tx + w];
     }
   };
-  auto emit = [&](int zo, const uint32_t* M, const uint32_t* Bv) {
+  auto emit = [&](int zo, const uint32_t* M) {
+    const uint16_t* bp = A.B + (int64_t)(zo - A.z_lo) * A.nx * A.ny;
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       const int x = x0 + tx, y = y0 + ty * 4 + k;
       bool seed = false;
-      if (x < A.nx && y < A.ny && Bv[k] >= A.thr && Bv[k] == M[k])
-        seed = tie_free(A.ma, x, y, zo, (uint16_t)Bv[k]);
+      if (x < A.nx && y < A.ny) {
+        const uint32_t b = __ldg(bp + (int64_t)y * A.nx + x);
+        if (b >= A.thr && b == M[k]) seed = tie_free(A.ma, x, y, zo, (uint16_t)b);
+      }
       const unsigned m = __ballot_sync(0xffffffffu, seed);
       if (lane == 0 && y < A.ny && x < A.nx)
         A.bits[((int64_t)(zo - A.own_z0) * A.ny + y) * A.wpr + (x >> 5)] = m;
     }
   };
   if (D == 2) {
-    uint32_t ym[4], yb[4];
-    plane(z0, ym, yb);
-    emit(z0, ym, yb);
+    for (int e = threadIdx.x; e < RY * RX; e += kMThreads) {
+      const int r = e / RX, c = e % RX;
+      const int gy = y0 - w + r, gx = x0 - w + c;
+      s_in[e] = (gy >= 0 && gy < A.ny && gx >= 0 && gx < A.nx) ? __ldg(A.B + (int64_t)gy * A.nx + gx) : 0;
+    }
+    uint32_t ym[4];
+    boxmax(ym);
+    emit(z0, ym);
     return;
   }
+  fetch(z0 - W);
   for (int base = 0; base < nplanes; base += K) {
 #pragma unroll
     for (int j = 0; j < K; ++j) {
       const int pi = base + j;
       if (pi >= nplanes) break;
-      plane(z0 - W + pi, ring[j], ringb[j]);
+      __syncthreads();   // the previous plane is done with s_in / s_x
+#pragma unroll
+      for (int q = 0; q < PER3; ++q) {
+        const int e = threadIdx.x + q * kMThreads;
+        if (e < RY * RX) s_in[e] = pf[q];
+      }
+      if (pi + 1 < nplanes) fetch(z0 - W + pi + 1);
+      boxmax(ring[j]);
       if (pi >= 2 * W) {
-        uint32_t M[4], Bv[4];
+        uint32_t M[4];
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
           uint32_t m = 0;
 #pragma unroll
           for (int i = 0; i < K; ++i) m = max(m, ring[(j + 1 + i) % K][k]);
           M[k] = m;
-          Bv[k] = ringb[(j + 1 + W) % K][k];
         }
-        emit(z0 + pi - 2 * W, M, Bv);
+        emit(z0 + pi - 2 * W, M);
       }
     }
   }

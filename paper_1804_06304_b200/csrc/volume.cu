@@ -172,19 +172,35 @@ __global__ void __launch_bounds__(kBThreads) blur3d_fused_kernel(const uint16_t*
   const int zend = min(z0 + kBZC, nz);
   const int nplanes = (zend - z0) + 2 * H;
   uint32_t ring[K][4];
+  // the next plane's tile is prefetched into registers while this plane computes
+  constexpr int PER = (RY * RX + kBThreads - 1) / kBThreads;
+  uint16_t pf[PER];
+  auto fetch = [&](int pi) {
+    const int zin = min(max(z0 - H + pi, 0), nz - 1);
+    const uint16_t* src = in + (int64_t)zin * nx * ny;
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+      const int e = threadIdx.x + q * kBThreads;
+      if (e < RY * RX) {
+        const int r = e / RX, c = e % RX;
+        const int gy = min(max(y0 - H + r, 0), ny - 1), gx = min(max(x0 - H + c, 0), nx - 1);
+        pf[q] = __ldg(src + (int64_t)gy * nx + gx);
+      }
+    }
+  };
+  fetch(0);
   for (int base = 0; base < nplanes; base += K) {
 #pragma unroll
     for (int j = 0; j < K; ++j) {
       const int pi = base + j;
       if (pi >= nplanes) break;
-      const int zin = min(max(z0 - H + pi, 0), nz - 1);
-      const uint16_t* src = in + (int64_t)zin * nx * ny;
       __syncthreads();   // previous plane's x pass finished with s_in, y pass with s_x
-      for (int e = threadIdx.x; e < RY * RX; e += kBThreads) {
-        const int r = e / RX, c = e % RX;
-        const int gy = min(max(y0 - H + r, 0), ny - 1), gx = min(max(x0 - H + c, 0), nx - 1);
-        s_in[r][c] = __ldg(src + (int64_t)gy * nx + gx);
+#pragma unroll
+      for (int q = 0; q < PER; ++q) {
+        const int e = threadIdx.x + q * kBThreads;
+        if (e < RY * RX) (&s_in[0][0])[e] = pf[q];
       }
+      if (pi + 1 < nplanes) fetch(pi + 1);
       __syncthreads();
       for (int e = threadIdx.x; e < RY * kBX; e += kBThreads) {
         const int r = e / kBX, c = e % kBX;

@@ -86,6 +86,7 @@ _SIGS = {
     "snk_run": (_i32, [_i32, _vp, _vp, _P(snk_params), _vp, _vp, _i64, _P(_i64), _vp, _i64, _vp, _sz,
                        _vp]),
     "snk_launch_count": (_i64, []),
+    "snk_evolve_stats": (_i32, [_vp, _i32]),
 }
 for _name, (_res, _args) in _SIGS.items():
     _f = getattr(_lib, _name)
@@ -159,6 +160,12 @@ snk_status_string = status_string
 
 def snk_launch_count() -> int:
     return _lib.snk_launch_count()
+
+
+def snk_evolve_stats(reset: bool = False) -> dict:
+    out = np.zeros(4, np.int64)
+    _check(_lib.snk_evolve_stats(out.ctypes.data_as(C.c_void_p), int(reset)), "snk_evolve_stats")
+    return {"brick_loads": int(out[0]), "global_iterations": int(out[1])}
 
 
 def snk_validate(g: snk_grid, p: snk_params) -> int:
