@@ -322,7 +322,7 @@ __global__ void __launch_bounds__(1024) bits_count_kernel(const uint32_t* bits, 
 __global__ void __launch_bounds__(1024) bits_write_kernel(const uint32_t* bits, int64_t nwords, int wpr,
                                                           int nx, int ny, int own_z0,
                                                           const int64_t* offsets, float* seeds,
-                                                          int64_t cap) {
+                                                          int64_t cap, int linear) {
   __shared__ int ws[32];
   const int64_t i = (int64_t)blockIdx.x * 1024 + threadIdx.x;
   const uint32_t word = i < nwords ? bits[i] : 0u;
@@ -348,10 +348,25 @@ __global__ void __launch_bounds__(1024) bits_write_kernel(const uint32_t* bits, 
   __syncthreads();
   int64_t o = offsets[blockIdx.x] + (warp > 0 ? ws[warp - 1] : 0) + x - c;
   if (!word) return;
+  uint32_t m = word;
+  if (linear) {   // bit b of word i = own-region voxel 32 i + b (x fastest)
+    const int64_t plane = (int64_t)nx * ny;
+    while (m) {
+      const int b = __ffs(m) - 1;
+      m &= m - 1;
+      const int64_t v = i * 32 + b;
+      if (o < cap) {
+        seeds[3 * o + 0] = (float)(v % nx);
+        seeds[3 * o + 1] = (float)((v / nx) % ny);
+        seeds[3 * o + 2] = (float)(v / plane + own_z0);
+      }
+      ++o;
+    }
+    return;
+  }
   const int64_t row = i / wpr;                 // (z - own_z0) * ny + y
   const int xw = (int)(i % wpr) * 32;
   const float fy = (float)(row % ny), fz = (float)(row / ny + own_z0);
-  uint32_t m = word;
   while (m) {
     const int b = __ffs(m) - 1;
     m &= m - 1;
@@ -362,7 +377,71 @@ __global__ void __launch_bounds__(1024) bits_write_kernel(const uint32_t* bits, 
     }
     ++o;
   }
-  (void)nx;
+}
+
+// ---------------------------------------------------------------------------
+// Vectorised MAXIMA (w <= 8, nx % 8 == 0): the x and y box-max are two
+// streaming sep_pass launches (volume.cu) into XY; this kernel takes one
+// 8-voxel group of the owned region per thread, folds the z box-max from the
+// 2w+1 XY planes (3D; clipped to the volume), tests B >= thr && B == M, runs
+// the tie check for the (rare) candidates, and writes one mask byte (bit k =
+// voxel 8 t + k), so the mask words are in linear voxel order.
+__device__ __forceinline__ void unpack8s(const uint4 q, uint32_t* v) {
+  v[0] = q.x & 0xffffu; v[1] = q.x >> 16; v[2] = q.y & 0xffffu; v[3] = q.y >> 16;
+  v[4] = q.z & 0xffffu; v[5] = q.z >> 16; v[6] = q.w & 0xffffu; v[7] = q.w >> 16;
+}
+
+template <int D, int W>
+__global__ void __launch_bounds__(256) maxima_pred8_kernel(MaxArgs A, const uint16_t* __restrict__ XY,
+                                                           uint8_t* __restrict__ mask, int64_t ngroups,
+                                                           int own_z0) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= ngroups) return;
+  const int nc = A.nx >> 3;
+  const int xc = (int)(t % nc);
+  const int64_t row = t / nc;
+  const int y = (int)(row % A.ny);
+  const int zo = (int)(row / A.ny) + own_z0;   // global plane
+  const int64_t idx = ((int64_t)(zo - A.z_lo) * A.ny + y) * nc + xc;
+  uint32_t b[8], m[8];
+  unpack8s(__ldg(reinterpret_cast<const uint4*>(A.B) + idx), b);
+  if (D == 3) {
+    const int64_t pstride = (int64_t)A.ny * nc;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) m[k] = 0;
+#pragma unroll
+    for (int i = -W; i <= W; ++i) {
+      if (zo + i < 0 || zo + i >= A.nz_glob) continue;
+      uint32_t v[8];
+      unpack8s(__ldg(reinterpret_cast<const uint4*>(XY) + idx + i * pstride), v);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) m[k] = max(m[k], v[k]);
+    }
+  } else {
+    unpack8s(__ldg(reinterpret_cast<const uint4*>(XY) + idx), m);
+  }
+  uint32_t bits = 0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k)
+    if (b[k] >= A.thr && b[k] == m[k]) bits |= 1u << k;
+  if (bits) {
+    for (int k = 0; k < 8; ++k)
+      if ((bits >> k & 1u) && !tie_free(A, xc * 8 + k, y, zo, (uint16_t)b[k])) bits &= ~(1u << k);
+  }
+  mask[t] = (uint8_t)bits;
+}
+
+bool vec_ok(const snk_grid* g, const snk_params* p) {
+  return g->n[0] % 8 == 0 && p->seed_window >= 0 && p->seed_window <= 8;
+}
+
+size_t vec_ws(const snk_grid* g) {
+  const int64_t nvox = g->n[0] * g->n[1] * g->nz_buf;
+  const int64_t nown = g->n[0] * g->n[1] * std::max<int64_t>(g->own_z1 - g->own_z0, 0);
+  const int64_t nw = ceil_div(std::max<int64_t>(nown, 1), 32);
+  const int64_t nb = ceil_div(nw, 1024);
+  return 2 * ((size_t)nvox * sizeof(uint16_t) + 256) + (size_t)nw * 4 + 256 + (size_t)nb * sizeof(int) +
+         256 + (size_t)(nb + 1) * sizeof(int64_t) + 256 + scan_ws(nb) + 1024;
 }
 
 bool fused_ok(const snk_grid* g, const snk_params* p) {
@@ -376,13 +455,14 @@ int64_t fused_words(const snk_grid* g) {
 }  // namespace
 
 size_t seeds_ws(const snk_grid* g, const snk_params* p) {
-  if (p->seed_mode == SNK_SEED_MAXIMA && fused_ok(g, p)) {
+  if (p->seed_mode != SNK_SEED_MAXIMA) return 0;
+  const size_t vws = vec_ok(g, p) ? vec_ws(g) : 0;
+  if (fused_ok(g, p)) {
     const int64_t nw = fused_words(g);
     const int64_t nb = ceil_div(std::max<int64_t>(nw, 1), 1024);
-    return (size_t)nw * 4 + 256 + (size_t)nb * sizeof(int) + 256 + (size_t)(nb + 1) * sizeof(int64_t) + 256 +
-           scan_ws(nb) + 1024;
+    return std::max(vws, (size_t)nw * 4 + 256 + (size_t)nb * sizeof(int) + 256 +
+                             (size_t)(nb + 1) * sizeof(int64_t) + 256 + scan_ws(nb) + 1024);
   }
-  if (p->seed_mode != SNK_SEED_MAXIMA) return 0;
   const int64_t nvox = g->n[0] * g->n[1] * g->nz_buf;
   const int64_t nown = g->n[0] * g->n[1] * (g->own_z1 - g->own_z0);
   const int64_t nb = ceil_div(std::max<int64_t>(nown, 1), kChunk);
@@ -451,6 +531,69 @@ int32_t seeds_impl(const snk_grid* g, const snk_params* p, const uint16_t* d_smo
   }
   const int64_t plane = (int64_t)nx * ny;
   const int64_t nvox = plane * nzb;
+  if (vec_ok(g, p) && ws_bytes >= vec_ws(g) && vec8_ok(g, d_smooth, nullptr, nullptr)) {
+    if (g->own_z1 <= g->own_z0) {
+      *n_out = 0;
+      return SNK_OK;
+    }
+    Carve cv(d_ws, ws_bytes);
+    uint16_t* ta = cv.take<uint16_t>(nvox);
+    uint16_t* tb = cv.take<uint16_t>(nvox);
+    const int64_t nown = plane * (g->own_z1 - g->own_z0);
+    const int64_t nw = ceil_div(nown, 32);
+    const int64_t nbw = ceil_div(nw, 1024);
+    uint32_t* bits = cv.take<uint32_t>(nw);
+    int* wcounts = cv.take<int>(nbw);
+    int64_t* woff = cv.take<int64_t>(nbw + 1);
+    void* stmp = cv.take<char>(scan_ws(nbw));
+    if (cv.overflow) return fail(SNK_CAPACITY, "workspace too small for seeds");
+    // x / y box max only over the planes the z window touches
+    const int64_t zb0 = dim == 3 ? std::max<int64_t>(g->own_z0 - w, 0) - g->z_lo : g->own_z0 - g->z_lo;
+    const int64_t zb1 = dim == 3 ? std::min<int64_t>(g->own_z1 - 1 + w, g->n[2] - 1) - g->z_lo + 1
+                                 : g->own_z1 - g->z_lo;
+    const int nzp = (int)(zb1 - zb0);
+    SNK_TRY(sep_pass(0, 1, w, d_smooth + zb0 * plane, ta + zb0 * plane, nx, ny, nzp, 0, nx - 1, st));
+    SNK_TRY(sep_pass(1, 1, w, ta + zb0 * plane, tb + zb0 * plane, nx, ny, nzp, 0, ny - 1, st));
+    SNK_CUDA_CHECK(cudaMemsetAsync(bits + nw - 1, 0, sizeof(uint32_t), st));
+    MaxArgs A;
+    A.B = d_smooth;
+    A.M = tb;
+    A.nx = nx;
+    A.ny = ny;
+    A.nz_glob = (int)g->n[2];
+    A.z_lo = (int)g->z_lo;
+    A.w = w;
+    A.dim = dim;
+    A.thr = p->seed_threshold;
+    A.v0 = A.v1 = 0;
+    const int64_t ng = nown / 8;
+    uint8_t* mask = reinterpret_cast<uint8_t*>(bits);
+    const unsigned grid = (unsigned)ceil_div(ng, 256);
+    const int oz = (int)g->own_z0;
+    if (dim == 2) {
+      maxima_pred8_kernel<2, 0><<<grid, 256, 0, st>>>(A, tb, mask, ng, oz);
+    } else {
+      switch (w) {
+#define SNK_PRED_CASE(WW) \
+        case WW: maxima_pred8_kernel<3, WW><<<grid, 256, 0, st>>>(A, tb, mask, ng, oz); break;
+        SNK_PRED_CASE(0) SNK_PRED_CASE(1) SNK_PRED_CASE(2) SNK_PRED_CASE(3) SNK_PRED_CASE(4)
+        SNK_PRED_CASE(5) SNK_PRED_CASE(6) SNK_PRED_CASE(7) SNK_PRED_CASE(8)
+#undef SNK_PRED_CASE
+      }
+    }
+    SNK_LAUNCH_CHECK("maxima_pred8_kernel");
+    bits_count_kernel<<<(unsigned)nbw, 1024, 0, st>>>(bits, nw, wcounts);
+    SNK_LAUNCH_CHECK("bits_count_kernel");
+    SNK_TRY(scan_counts(wcounts, nbw, woff, st, stmp));
+    bits_write_kernel<<<(unsigned)nbw, 1024, 0, st>>>(bits, nw, 0, nx, ny, oz, woff, d_seeds, cap, 1);
+    SNK_LAUNCH_CHECK("bits_write_kernel");
+    int64_t total = 0;
+    SNK_CUDA_CHECK(cudaMemcpyAsync(&total, woff + nbw, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    SNK_CUDA_CHECK(cudaStreamSynchronize(st));
+    *n_out = total;
+    if (total > cap) return fail(SNK_CAPACITY, "seed buffer too small");
+    return SNK_OK;
+  }
   Carve cv(d_ws, ws_bytes);
   if (fused_ok(g, p)) {
     if (g->own_z1 <= g->own_z0) {
@@ -507,7 +650,7 @@ int32_t seeds_impl(const snk_grid* g, const snk_params* p, const uint16_t* d_smo
     bits_count_kernel<<<(unsigned)nbw, 1024, 0, st>>>(bits, nw, wcounts);
     SNK_LAUNCH_CHECK("bits_count_kernel");
     SNK_TRY(scan_counts(wcounts, nbw, woff, st, stmp));
-    bits_write_kernel<<<(unsigned)nbw, 1024, 0, st>>>(bits, nw, F.wpr, nx, ny, F.own_z0, woff, d_seeds, cap);
+    bits_write_kernel<<<(unsigned)nbw, 1024, 0, st>>>(bits, nw, F.wpr, nx, ny, F.own_z0, woff, d_seeds, cap, 0);
     SNK_LAUNCH_CHECK("bits_write_kernel");
     int64_t total = 0;
     SNK_CUDA_CHECK(cudaMemcpyAsync(&total, woff + nbw, sizeof(int64_t), cudaMemcpyDeviceToHost, st));

@@ -151,6 +151,102 @@ __global__ void __launch_bounds__(256) resample_kernel(const uint16_t* __restric
 inline unsigned grid_for(int64_t n, int block) { return (unsigned)ceil_div(n, block); }
 
 // ---------------------------------------------------------------------------
+// Vectorised separable pass: each thread produces 8 consecutive x outputs
+// (one 16-byte store) from 16-byte loads; no shared memory, no barriers, so
+// the pass streams at HBM rate (stencil neighbours come from L1/L2).
+//   OP_BLUR: (sum_i w_i v[clamp(p+i)] + 8192) >> 14 (clamp-to-edge, G18)
+//   OP_MAX:  max over the window clipped to [lo, hi] (the MAXIMA box, G20)
+// Requires nx % 8 == 0 and 16-byte aligned buffers.
+enum { OP_BLUR = 0, OP_MAX = 1 };
+
+__device__ __forceinline__ void unpack8(const uint4 q, uint32_t* v) {
+  v[0] = q.x & 0xffffu; v[1] = q.x >> 16; v[2] = q.y & 0xffffu; v[3] = q.y >> 16;
+  v[4] = q.z & 0xffffu; v[5] = q.z >> 16; v[6] = q.w & 0xffffu; v[7] = q.w >> 16;
+}
+__device__ __forceinline__ uint4 pack8(const uint32_t* o) {
+  return make_uint4(o[0] | (o[1] << 16), o[2] | (o[3] << 16), o[4] | (o[5] << 16), o[6] | (o[7] << 16));
+}
+
+template <int AXIS, int OP, int H>
+__global__ void __launch_bounds__(256) sep8_kernel(const uint16_t* __restrict__ in, uint16_t* __restrict__ out,
+                                                   int nx, int ny, int nz, int lo, int hi) {
+  const int nc = nx >> 3;
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (int64_t)nc * ny * nz) return;
+  const int xc = (int)(t % nc);
+  const int64_t row = t / nc;                     // z * ny + y
+  const int y = (int)(row % ny), z = (int)(row / ny);
+  const uint4* rin = reinterpret_cast<const uint4*>(in);
+  uint32_t o[8];
+  if (AXIS == 0) {
+    uint32_t v[24];
+    const int64_t rb = row * nc;
+    unpack8(__ldg(rin + rb + xc), v + 8);
+    if (xc > 0) unpack8(__ldg(rin + rb + xc - 1), v);
+    else {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) v[k] = OP == OP_BLUR ? v[8] : 0u;
+    }
+    if (xc < nc - 1) unpack8(__ldg(rin + rb + xc + 1), v + 16);
+    else {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) v[16 + k] = OP == OP_BLUR ? v[15] : 0u;
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      uint32_t acc = OP == OP_BLUR ? 8192u : 0u;
+#pragma unroll
+      for (int i = -H; i <= H; ++i) {
+        if (OP == OP_BLUR) acc += (uint32_t)c_taps[i + H] * v[8 + k + i];
+        else acc = max(acc, v[8 + k + i]);
+      }
+      o[k] = OP == OP_BLUR ? acc >> 14 : acc;
+    }
+  } else {
+    const int p = AXIS == 1 ? y : z;
+    const int np = AXIS == 1 ? ny : nz;
+    const int64_t stride = AXIS == 1 ? nc : (int64_t)nc * ny;   // in uint4 units
+    const uint4* base = rin + row * nc + xc - (int64_t)p * stride;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) o[k] = OP == OP_BLUR ? 8192u : 0u;
+#pragma unroll
+    for (int i = -H; i <= H; ++i) {
+      int q = p + i;
+      if (OP == OP_BLUR) q = min(max(q, 0), np - 1);
+      else if (q < lo || q > hi) continue;
+      uint32_t v[8];
+      unpack8(__ldg(base + (int64_t)q * stride), v);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        if (OP == OP_BLUR) o[k] += (uint32_t)c_taps[i + H] * v[k];
+        else o[k] = max(o[k], v[k]);
+      }
+    }
+    if (OP == OP_BLUR) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) o[k] >>= 14;
+    }
+  }
+  reinterpret_cast<uint4*>(out)[t] = pack8(o);
+}
+
+template <int AXIS, int OP>
+int32_t sep8_launch(int h, const uint16_t* in, uint16_t* out, int nx, int ny, int nz, int lo, int hi,
+                    cudaStream_t st) {
+  const unsigned grid = (unsigned)ceil_div((int64_t)(nx / 8) * ny * nz, 256);
+  switch (h) {
+#define SNK_SEP_CASE(HH) \
+    case HH: sep8_kernel<AXIS, OP, HH><<<grid, 256, 0, st>>>(in, out, nx, ny, nz, lo, hi); break;
+    SNK_SEP_CASE(0) SNK_SEP_CASE(1) SNK_SEP_CASE(2) SNK_SEP_CASE(3) SNK_SEP_CASE(4)
+    SNK_SEP_CASE(5) SNK_SEP_CASE(6) SNK_SEP_CASE(7) SNK_SEP_CASE(8)
+#undef SNK_SEP_CASE
+    default: return fail(SNK_INTERNAL, "sep8: radius > 8");
+  }
+  SNK_LAUNCH_CHECK("sep8_kernel");
+  return SNK_OK;
+}
+
+// ---------------------------------------------------------------------------
 // Fused 3D blur: one CTA per 64 x 16 output columns and a 32-plane z-chunk.
 // Per input plane: the (16+2H) x (64+2H) tile (clamped coordinates) is
 // staged in shared memory, the x pass and the y pass run there (each rounding
@@ -327,8 +423,25 @@ int32_t launch_fused_blur(const snk_grid* g, const uint16_t* d_in, uint16_t* d_o
 }  // namespace
 
 size_t preprocess_ws(const snk_grid* g, const snk_params* p) {
-  if (p->sigma > 0 && std::ceil(4.0 * p->sigma) <= 8) return 0;   // fused kernel: no scratch
-  return (size_t)g->n[0] * g->n[1] * g->nz_buf * sizeof(uint16_t) + 256;
+  if (!(p->sigma > 0)) return 0;
+  return (size_t)g->n[0] * g->n[1] * g->nz_buf * sizeof(uint16_t) + 256;   // separable ping-pong
+}
+
+bool vec8_ok(const snk_grid* g, const void* a, const void* b, const void* c) {
+  auto al = [](const void* q) { return q == nullptr || (reinterpret_cast<uintptr_t>(q) & 15) == 0; };
+  return g->n[0] % 8 == 0 && al(a) && al(b) && al(c);
+}
+
+int32_t sep_pass(int axis, int op, int h, const uint16_t* in, uint16_t* out, int nx, int ny, int nz,
+                 int lo, int hi, cudaStream_t st) {
+  if (op == OP_BLUR) {
+    if (axis == 0) return sep8_launch<0, OP_BLUR>(h, in, out, nx, ny, nz, lo, hi, st);
+    if (axis == 1) return sep8_launch<1, OP_BLUR>(h, in, out, nx, ny, nz, lo, hi, st);
+    return sep8_launch<2, OP_BLUR>(h, in, out, nx, ny, nz, lo, hi, st);
+  }
+  if (axis == 0) return sep8_launch<0, OP_MAX>(h, in, out, nx, ny, nz, lo, hi, st);
+  if (axis == 1) return sep8_launch<1, OP_MAX>(h, in, out, nx, ny, nz, lo, hi, st);
+  return sep8_launch<2, OP_MAX>(h, in, out, nx, ny, nz, lo, hi, st);
 }
 
 int32_t preprocess_impl(const snk_grid* g, const snk_params* p, const uint16_t* d_in,
@@ -341,10 +454,20 @@ int32_t preprocess_impl(const snk_grid* g, const snk_params* p, const uint16_t* 
   const int nx = (int)g->n[0], ny = (int)g->n[1], nz = (int)g->nz_buf;
   const int64_t nvox = (int64_t)nx * ny * nz;
   Carve cv(d_ws, ws_bytes);
-  uint16_t* tmp = h > 8 ? cv.take<uint16_t>(nvox) : nullptr;
+  uint16_t* tmp = h > 0 ? cv.take<uint16_t>(nvox) : nullptr;
   if (cv.overflow) return fail(SNK_CAPACITY, "workspace too small for preprocess");
   if (h == 0) {
     SNK_CUDA_CHECK(cudaMemcpyAsync(d_smooth, d_in, nvox * sizeof(uint16_t), cudaMemcpyDeviceToDevice, st));
+  } else if (h <= 8 && vec8_ok(g, d_in, d_smooth, tmp)) {
+    // three (2D: two) streaming separable passes, 8 voxels per thread
+    if (g->dim == 3) {
+      SNK_TRY(sep_pass(0, OP_BLUR, h, d_in, d_smooth, nx, ny, nz, 0, 0, st));
+      SNK_TRY(sep_pass(1, OP_BLUR, h, d_smooth, tmp, nx, ny, nz, 0, 0, st));
+      SNK_TRY(sep_pass(2, OP_BLUR, h, tmp, d_smooth, nx, ny, nz, 0, 0, st));
+    } else {
+      SNK_TRY(sep_pass(0, OP_BLUR, h, d_in, tmp, nx, ny, nz, 0, 0, st));
+      SNK_TRY(sep_pass(1, OP_BLUR, h, tmp, d_smooth, nx, ny, nz, 0, 0, st));
+    }
   } else if (h <= 8) {
     switch (h) {
       case 1: SNK_TRY(launch_fused_blur<1>(g, d_in, d_smooth, st)); break;
