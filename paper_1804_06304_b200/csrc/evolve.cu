@@ -190,6 +190,10 @@ __device__ __forceinline__ Acc leaves(const EvoParams& P, const CellIt& C, const
   return a;
 }
 
+// Brick row length: S + 2 rounded down to even (the x origin is even, the
+// copies are 4-byte words), so a ball box of width SX - 1 always fits in x.
+__host__ __device__ constexpr int brick_sx(int S) { return (S + 2) & ~1; }
+
 // Gather modes
 enum { G_GLOBAL = 0, G_GLOBAL_SLAB = 1, G_BRICK_CLAMP = 2, G_BRICK_FAST = 3 };
 
@@ -205,8 +209,8 @@ __device__ __forceinline__ Acc sample_leaf(const EvoParams& P, const CellIt& C, 
   if (D == 3) fz = split_axis<CLAMP>(__fmaf_rn(d.t, d.oz, C.cz), P.fnz1, P.mz2, &rz);
   float v000, v100, v010, v110, v001 = 0, v101 = 0, v011 = 0, v111 = 0;
   if (MODE == G_BRICK_CLAMP || MODE == G_BRICK_FAST) {
-    // brick-local index; row stride SX = S + 2 and plane stride SX * S are immediates
-    constexpr int SX = S + 2, SP = SX * S;
+    // brick-local index; row stride SX and plane stride SX * S are immediates
+    constexpr int SX = brick_sx(S), SP = SX * S;
     uint32_t li = ry * SX + rx;
     if (D == 3) li += rz * SP;
     li -= C.boff;
@@ -468,7 +472,7 @@ __global__ void __launch_bounds__(W >= 4 ? 32 * W : 128)
 
 // =========================================================================
 // Brick kernel: one CTA (W warps) per cell; the u16 neighbourhood of the cell
-// (x: S + 2 columns from an even origin, y and z: S rows/planes) lives in
+// (x: brick_sx(S) columns from an even origin, y and z: S rows/planes) lives in
 // shared memory, filled by 4-byte cp.async copies (LDGSTS) when the sampled
 // ball leaves it.
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -478,7 +482,7 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
 template <int D, int S>
 __device__ __forceinline__ void load_brick(uint16_t* brick, const EvoParams& P, int bx, int by, int bz,
                                            int zlo_buf) {
-  constexpr int SX = S + 2, WPR = SX / 2;          // u16 per row, 32-bit words per row
+  constexpr int SX = brick_sx(S), WPR = SX / 2;          // u16 per row, 32-bit words per row
   constexpr int ROWS = D == 3 ? S * S : S;
   const int nw = min(WPR, (P.nx - bx + 1) / 2);     // words inside the volume (x)
   const int ny = min(S, P.ny - by);
@@ -501,7 +505,7 @@ __device__ __forceinline__ void load_brick(uint16_t* brick, const EvoParams& P, 
 template <int D, int W, int S, bool SLAB, int CH, int L>
 __global__ void __launch_bounds__(32 * W, W == 4 ? 3 : 1) evolve_brick_kernel(const __grid_constant__ EvoParams P) {
   constexpr int B = CH << L;
-  constexpr int EXT[3] = {S + 2, S, S};             // brick extent per axis
+  constexpr int EXT[3] = {brick_sx(S), S, S};       // brick extent per axis
   extern __shared__ __align__(16) uint16_t brick[];
   __shared__ Acc xch[2][W];
   const int lane = threadIdx.x & 31, wsub = threadIdx.x >> 5;
@@ -528,7 +532,7 @@ __global__ void __launch_bounds__(32 * W, W == 4 ? 3 : 1) evolve_brick_kernel(co
       interior &= lo[a] >= 0 && hi[a] <= n[a] - 1;
       lo[a] = max(lo[a], 0);
       hi[a] = min(hi[a], n[a] - 1);
-      fits &= hi[a] - lo[a] + 1 <= S;
+      fits &= hi[a] - lo[a] + 1 <= (a == 0 ? EXT[0] - 1 : S);
       inside &= lo[a] >= b[a] && hi[a] <= b[a] + EXT[a] - 1;
     }
     if (D == 3 && SLAB) fits &= lo[2] >= zlo && hi[2] <= zhi;
@@ -552,8 +556,8 @@ __global__ void __launch_bounds__(32 * W, W == 4 ? 3 : 1) evolve_brick_kernel(co
     }
     Acc part;
     if (inside) {
-      C.boff = (kMagicBits + (uint32_t)b[0]) + (kMagicBits + (uint32_t)b[1]) * (uint32_t)(S + 2);
-      if (D == 3) C.boff += (kMagicBits + (uint32_t)b[2]) * (uint32_t)((S + 2) * S);
+      C.boff = (kMagicBits + (uint32_t)b[0]) + (kMagicBits + (uint32_t)b[1]) * (uint32_t)brick_sx(S);
+      if (D == 3) C.boff += (kMagicBits + (uint32_t)b[2]) * (uint32_t)(brick_sx(S) * S);
       if (interior) part = lane_sum<D, G_BRICK_FAST, S, CH, L>(P, C, j0, brick, halo);
       else part = lane_sum<D, G_BRICK_CLAMP, S, CH, L>(P, C, j0, brick, halo);
     } else {
@@ -582,7 +586,7 @@ int32_t launch_warp(const EvoParams& P, cudaStream_t st) {
 template <int D, int W, int S, bool SLAB, int CH, int L>
 int32_t launch_brick(const EvoParams& P, cudaStream_t st) {
   auto k = evolve_brick_kernel<D, W, S, SLAB, CH, L>;
-  const int smem = (D == 3 ? (S + 2) * S * S : (S + 2) * S) * 2;
+  const int smem = (D == 3 ? brick_sx(S) * S * S : brick_sx(S) * S) * 2;
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [&] { attr_err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); });
@@ -621,6 +625,8 @@ int32_t warp_W(const EvoParams& P, int W, int B, cudaStream_t st) {
     default: return fail(SNK_CONFIG, "bad warps per cell");
   }
 }
+
+constexpr int kS3 = 33;
 
 template <int D, int W, int S, bool SLAB>
 int32_t brick_B(const EvoParams& P, int B, cudaStream_t st) {
@@ -730,8 +736,9 @@ int32_t evolve_impl(const snk_grid* g, const snk_params* p, const uint16_t* d_im
   if (variant == 2 && !brick_ok) return fail(SNK_CONFIG, "brick kernel unavailable for this volume");
   if (brick_ok) {
     if (D == 3) {
-      if (Wb == 4) return slab ? brick_B<3, 4, 32, true>(P, Bb, st) : brick_B<3, 4, 32, false>(P, Bb, st);
-      return slab ? brick_B<3, 8, 32, true>(P, Bb, st) : brick_B<3, 8, 32, false>(P, Bb, st);
+      // S = 33: 34 x 33 x 33 u16 = 72.3 KB, three CTAs per SM; covers balls up to rho_s ~ 15.5
+      if (Wb == 4) return slab ? brick_B<3, 4, kS3, true>(P, Bb, st) : brick_B<3, 4, kS3, false>(P, Bb, st);
+      return slab ? brick_B<3, 8, kS3, true>(P, Bb, st) : brick_B<3, 8, kS3, false>(P, Bb, st);
     }
     if (Wb == 4) return brick_B<2, 4, 64, false>(P, Bb, st);
     return brick_B<2, 8, 64, false>(P, Bb, st);
