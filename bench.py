@@ -31,10 +31,10 @@ import synth  # noqa: E402  (input generator: no method arithmetic)
 
 METRIC = "contour ray-samples/sec and cells segmented/sec at 1/2/4/8 B200; HBM/L2 GB/s"
 UNIT = "ray-samples/s"
-# Algorithmic issue slots per MC sample: Philox4x32-10 40, uniforms 6,
-# direction + radius 12 (5 SFU), position 3, d-linear gather 8 loads + 26 ALU,
-# weights S, S_r, S_R 17, leaves 6, tree adds 5  ->  123 lane-ops per sample.
-OPS_PER_SAMPLE = 123
+# Algorithmic issue slots per MC sample: Philox4x32-10 30 (3/4 block),
+# uniforms 6, direction + radius 12 (5 SFU), position 3, d-linear gather 8 loads + 26 ALU,
+# weights S, S_r, S_R 15, leaves 6, tree adds 5  ->  111 lane-ops per sample.
+OPS_PER_SAMPLE = 111
 SMS = 148
 LANES_PER_SM = 128
 

@@ -57,7 +57,8 @@ inline int64_t clampi(int64_t v, int64_t lo, int64_t hi) { return v < lo ? lo : 
 // ---------------------------------------------------------------------------
 // Philox4x32-10 (Salmon et al., Random123) — the counter-based generator the
 // north_star names; stream key per SPEC S:186/S:238 and G11:
-//   ctr = {sample j, iteration n, id_lo, id_hi}, key = {seed_lo, seed_hi}.
+//   ctr = {block b, iteration n, id_lo, id_hi}, key = {seed_lo, seed_hi}
+// (the samples' words are laid out over the blocks by stream_word below).
 void philox4x32_10(const uint32_t ctr_in[4], const uint32_t key_in[2], uint32_t out[4]) {
   const uint32_t M0 = 0xD2511F53u, M1 = 0xCD9E8D57u;   // Philox multipliers
   const uint32_t W0 = 0x9E3779B9u, W1 = 0xBB67AE85u;   // Weyl key increments
@@ -86,14 +87,30 @@ inline double uniform01(uint32_t x) { return (double)(x >> 9) * 0x1p-23; }
 //   3D direction by Archimedes' hat-box theorem (G10): z = 1 - 2u0, phi = 2 pi u1;
 //   3D radius t = rho_s * cbrt(u2) (volume-uniform radial law);
 //   2D radius t = rho_s * sqrt(u2).
-void mc_sample(int dim, uint32_t j, uint32_t iter, int64_t id, uint64_t seed,
-               double rho_s, double omega[3], double* t) {
-  const uint32_t ctr[4] = {j, iter, (uint32_t)((uint64_t)id & 0xffffffffu),
+// Word w of the stream of one cell-iteration (G11): word w is output w mod 4 of
+// Philox4x32-10 at ctr = {floor(w / 4), n, id_lo, id_hi}, key = seed.  A 3D
+// sample j takes words 3j, 3j+1, 3j+2 (u0, u1, u2); a 2D sample j takes words
+// 2j, 2j+1 (u1, u2): every generated word is used exactly once.
+uint32_t stream_word(uint64_t w, uint32_t iter, int64_t id, uint64_t seed) {
+  const uint32_t ctr[4] = {(uint32_t)(w >> 2), iter, (uint32_t)((uint64_t)id & 0xffffffffu),
                            (uint32_t)((uint64_t)id >> 32)};
   const uint32_t key[2] = {(uint32_t)(seed & 0xffffffffu), (uint32_t)(seed >> 32)};
   uint32_t x[4];
   philox4x32_10(ctr, key, x);
-  const double u0 = uniform01(x[0]), u1 = uniform01(x[1]), u2 = uniform01(x[2]);
+  return x[w & 3];
+}
+
+void mc_sample(int dim, uint32_t j, uint32_t iter, int64_t id, uint64_t seed,
+               double rho_s, double omega[3], double* t) {
+  double u0 = 0.0, u1, u2;
+  if (dim == 3) {
+    u0 = uniform01(stream_word(3ull * j, iter, id, seed));
+    u1 = uniform01(stream_word(3ull * j + 1, iter, id, seed));
+    u2 = uniform01(stream_word(3ull * j + 2, iter, id, seed));
+  } else {
+    u1 = uniform01(stream_word(2ull * j, iter, id, seed));
+    u2 = uniform01(stream_word(2ull * j + 1, iter, id, seed));
+  }
   const double phi = 2.0 * PI * u1;
   if (dim == 3) {
     const double z = 1.0 - 2.0 * u0;

@@ -14,8 +14,10 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
-OBJ = os.path.join(HERE, "build_obj")
-LIB = os.path.join(HERE, "libsnk.so")
+# SNK_BUILD_TAG (tuning experiments only): objects and library under a tagged name
+_TAG = os.environ.get("SNK_BUILD_TAG", "")
+OBJ = os.path.join(HERE, "build_obj" + (f"_{_TAG}" if _TAG else ""))
+LIB = os.path.join(HERE, f"libsnk_{_TAG}.so" if _TAG else "libsnk.so")
 SOURCES = ["abi.cu", "volume.cu", "seeds.cu", "evolve.cu", "cull.cu", "label.cu"]
 HEADERS = ["common.cuh"]
 
@@ -49,7 +51,9 @@ def build(force: bool = False, verbose: bool = False) -> str:
         src = os.path.join(CSRC, s)
         obj = os.path.join(OBJ, s.replace(".cu", ".o"))
         if force or _stale(obj, src):
-            cmd = [cc, *ARCH, *BASE, *PER_FILE.get(s, []), "-c", src, "-o", obj]
+            # SNK_NVCC_EXTRA: extra -D flags for tuning experiments (scripts/)
+            extra = os.environ.get("SNK_NVCC_EXTRA", "").split()
+            cmd = [cc, *ARCH, *BASE, *PER_FILE.get(s, []), *extra, "-c", src, "-o", obj]
             if verbose:
                 cmd += ["-Xptxas", "-v"]
             jobs.append((s, cmd))

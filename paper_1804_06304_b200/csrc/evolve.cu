@@ -17,8 +17,9 @@
 //    gathers straight from global memory (L1/L2).
 //
 // Each iteration draws a FIXED number N of samples per cell (no
-// divergence), 32 W threads x B = N/(32 W) each.  Per sample: Philox4x32-10
-// -> (omega, t) -> 8 u16 taps -> trilinear -> S, S_r, S_R -> 5 leaf products.
+// divergence), 32 W threads x B = N/(32 W) each.  Per sample: 3 (2D: 2) words
+// of the Philox4x32-10 stream (4 samples per 3 blocks) -> (omega, t) -> 8 u16
+// taps -> trilinear -> S, S_r, S_R -> 5 leaf products.
 // Sums follow one canonical pairwise tree over the N sample positions
 // (in-thread binary counter -> xor butterfly over lanes -> pairwise over
 // warps), so every W and both kernels give bit-identical results (S:314,
@@ -54,8 +55,9 @@ struct EvoParams {
   float fnx1, fny1, fnz1;        // n - 1
   float mx2, my2, mz2;           // 2^23 + (n - 2): clamp of the magic floor
   float r0, half_dR, inv_dR, inv_rho_dR, eps0, max_step, r_min, r_max, leash, conv_tol;
-  float k12_rho_dR, km6_dR, k6_dR;   // 12/(rho dR), -6/dR, 6/dR
+  float k2_rho, k6_dR;           // 2/rho, 6/dR
   float vscale;                  // iscale * (4/3 pi | pi) / N
+  float half_eps0;               // eps0 / 2
   int T;
   uint32_t rk0[10], rk1[10];     // Philox round keys (seed + r * Weyl)
 };
@@ -84,6 +86,16 @@ struct CellIt {
 __device__ __forceinline__ float sqrt_approx(float x) {
   float r;
   asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+__device__ __forceinline__ float rcp_approx(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+__device__ __forceinline__ float rsqrt_approx(float x) {
+  float r;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
   return r;
 }
 __device__ __forceinline__ float lg2_approx(float x) {
@@ -130,12 +142,11 @@ struct Draw {
   float ox, oy, oz, t;
 };
 
-// Philox4x32-10 with ctr = {j, n, id_lo, id_hi}, key = seed (G11) -> the
-// sample's direction (Archimedes, G10) and distance.
-template <int D>
-__device__ __forceinline__ Draw draw(const EvoParams& P, const CellIt& C, uint32_t j) {
-  const uint64_t pj = (uint64_t)kM0 * j;
-  uint32_t c0 = C.p0, c1 = C.p1, c2 = (uint32_t)(pj >> 32) ^ C.p3, c3 = (uint32_t)pj;
+// Philox4x32-10 block b of the cell-iteration stream: ctr = {b, n, id_lo,
+// id_hi}, key = seed (G11); round 1's products of the constant words are in C.
+__device__ __forceinline__ void philox_block(const EvoParams& P, const CellIt& C, uint32_t b, uint32_t x[4]) {
+  const uint64_t pb = (uint64_t)kM0 * b;
+  uint32_t c0 = C.p0, c1 = C.p1, c2 = (uint32_t)(pb >> 32) ^ C.p3, c3 = (uint32_t)pb;
 #pragma unroll
   for (int r = 1; r < 10; ++r) {
     const uint64_t p0 = (uint64_t)kM0 * c0;
@@ -147,23 +158,72 @@ __device__ __forceinline__ Draw draw(const EvoParams& P, const CellIt& C, uint32
     c2 = n2;
     c3 = (uint32_t)p0;
   }
-  const float u0 = u01(c0), u1 = u01(c1), u2 = u01(c2);
+  x[0] = c0; x[1] = c1; x[2] = c2; x[3] = c3;
+}
+
+// Words -> the sample's direction (Archimedes, G10) and distance (P:194-195,
+// S:224).  3D: (w0, w1, w2) = (u0, u1, u2); 2D: (w1, w2) = (u1, u2).
+template <int D>
+__device__ __forceinline__ Draw draw_words(const CellIt& C, uint32_t w0, uint32_t w1, uint32_t w2) {
+  const float u1 = u01(w1), u2 = u01(w2);
   float sn, cs;
   __sincosf(__fmul_rn(6.2831853071795865f, u1), &sn, &cs);
   Draw d;
   if (D == 3) {
+    const float u0 = u01(w0);
     d.oz = __fmaf_rn(-2.0f, u0, 1.0f);
     const float st = __fmul_rn(2.0f, sqrt_approx(__fmaf_rn(-u0, u0, u0)));
     d.ox = __fmul_rn(st, cs);
     d.oy = __fmul_rn(st, sn);
     d.t = ex2_approx(__fmaf_rn(lg2_approx(u2), 0.333333343f, C.lg2_rho_s));   // rho_s cbrt(u2)
   } else {
+    (void)w0;
     d.ox = cs;
     d.oy = sn;
     d.oz = 0.0f;
     d.t = __fmul_rn(C.rho_s, sqrt_approx(u2));
   }
   return d;
+}
+
+// Sample j alone (G11 word layout: 3D words 3j..3j+2, 2D words 2j, 2j+1).
+template <int D>
+__device__ __forceinline__ Draw draw(const EvoParams& P, const CellIt& C, uint32_t j) {
+  uint32_t x[4];
+  if (D == 3) {
+    const uint32_t w = 3u * j, o = w & 3u;
+    philox_block(P, C, w >> 2, x);
+    if (o == 0) return draw_words<3>(C, x[0], x[1], x[2]);
+    if (o == 1) return draw_words<3>(C, x[1], x[2], x[3]);
+    uint32_t y[4];
+    philox_block(P, C, (w >> 2) + 1, y);
+    if (o == 2) return draw_words<3>(C, x[2], x[3], y[0]);
+    return draw_words<3>(C, x[3], y[0], y[1]);
+  }
+  philox_block(P, C, j >> 1, x);
+  return (j & 1u) ? draw_words<2>(C, 0, x[2], x[3]) : draw_words<2>(C, 0, x[0], x[1]);
+}
+
+// The G samples j .. j + G - 1 of one group (j % G == 0; G = 4 in 3D, 2 in 2D):
+// 3 (3D) or 1 (2D) Philox blocks.
+template <int D>
+__device__ __forceinline__ void draw_group(const EvoParams& P, const CellIt& C, uint32_t j, Draw* d) {
+  if (D == 3) {
+    uint32_t a[4], b[4], c[4];
+    const uint32_t b0 = (j >> 2) * 3u;
+    philox_block(P, C, b0, a);
+    philox_block(P, C, b0 + 1, b);
+    philox_block(P, C, b0 + 2, c);
+    d[0] = draw_words<3>(C, a[0], a[1], a[2]);
+    d[1] = draw_words<3>(C, a[3], b[0], b[1]);
+    d[2] = draw_words<3>(C, b[2], b[3], c[0]);
+    d[3] = draw_words<3>(C, c[1], c[2], c[3]);
+  } else {
+    uint32_t a[4];
+    philox_block(P, C, j >> 1, a);
+    d[0] = draw_words<2>(C, 0, a[0], a[1]);
+    d[1] = draw_words<2>(C, 0, a[2], a[3]);
+  }
 }
 
 // S(t; R) and partials (G1) -> the five leaves for image value tri.
@@ -177,9 +237,10 @@ __device__ __forceinline__ Acc leaves(const EvoParams& P, const CellIt& C, const
   const float s3o = __fmul_rn(uo, __fmaf_rn(2.0f, qo, uo));
   const float s3i = __fmul_rn(ui, __fmaf_rn(2.0f, qi, ui));
   const float S = __fsub_rn(__fmaf_rn(2.0f, s3i, -s3o), 1.0f);             // (1-s3o) - 2(1-s3i)
-  // S_r = -6 qo/dR + 12 qi/(rho dR),  S_R = 6 (qo - 2 qi)/dR
-  const float Sr = __fmaf_rn(P.k12_rho_dR, qi, __fmul_rn(P.km6_dR, qo));
-  const float SR = __fmul_rn(__fmaf_rn(-2.0f, qi, qo), P.k6_dR);
+  // S_r = (6/dR) (2 qi/rho - qo),  S_R = (6/dR) (qo - 2 qi): the common factor
+  // 6/dR is applied once to the sums (cell_update)
+  const float Sr = __fmaf_rn(P.k2_rho, qi, -qo);
+  const float SR = __fmaf_rn(-2.0f, qi, qo);
   const float w = __fmul_rn(Sr, tri);
   Acc a;
   a.a0 = __fmul_rn(S, tri);
@@ -198,9 +259,8 @@ __host__ __device__ constexpr int brick_sx(int S) { return (S + 2) & ~1; }
 enum { G_GLOBAL = 0, G_GLOBAL_SLAB = 1, G_BRICK_CLAMP = 2, G_BRICK_FAST = 3 };
 
 template <int D, int MODE, int S>
-__device__ __forceinline__ Acc sample_leaf(const EvoParams& P, const CellIt& C, uint32_t j,
+__device__ __forceinline__ Acc sample_leaf(const EvoParams& P, const CellIt& C, const Draw& d,
                                            const uint16_t* brick, uint32_t& halo) {
-  const Draw d = draw<D>(P, C, j);
   constexpr bool CLAMP = MODE != G_BRICK_FAST;
   uint32_t rx, ry, rz = kMagicBits;
   const float fx = split_axis<CLAMP>(__fmaf_rn(d.t, d.ox, C.cx), P.fnx1, P.mx2, &rx);
@@ -256,12 +316,22 @@ __device__ __forceinline__ Acc sample_leaf(const EvoParams& P, const CellIt& C, 
   return leaves(P, C, d, tri, D == 3);
 }
 
-// Pairwise sum over CH consecutive samples (CH a power of two).
+// Pairwise sum over CH consecutive samples (CH a power of two).  Groups of G
+// samples share their Philox blocks (draw_group); smaller chunks draw alone.
 template <int D, int MODE, int S, int CH>
 __device__ __forceinline__ Acc chunk_sum(const EvoParams& P, const CellIt& C, uint32_t j0,
                                          const uint16_t* brick, uint32_t& halo) {
+  constexpr int G = D == 3 ? 4 : 2;
   if constexpr (CH == 1) {
-    return sample_leaf<D, MODE, S>(P, C, j0, brick, halo);
+    return sample_leaf<D, MODE, S>(P, C, draw<D>(P, C, j0), brick, halo);
+  } else if constexpr (CH == G) {
+    Draw d[G];
+    draw_group<D>(P, C, j0, d);
+    Acc l[G];
+#pragma unroll
+    for (int k = 0; k < G; ++k) l[k] = sample_leaf<D, MODE, S>(P, C, d[k], brick, halo);
+    if constexpr (G == 4) return acc_add(acc_add(l[0], l[1]), acc_add(l[2], l[3]));
+    else return acc_add(l[0], l[1]);
   } else {
     const Acc l = chunk_sum<D, MODE, S, CH / 2>(P, C, j0, brick, halo);
     const Acc r = chunk_sum<D, MODE, S, CH / 2>(P, C, j0 + CH / 2, brick, halo);
@@ -309,6 +379,38 @@ __device__ __forceinline__ Acc warp_butterfly(Acc s) {
     s = acc_add(s, q);
   }
   return s;
+}
+
+// The same pairwise lane tree as warp_butterfly, as a reduce-scatter: at each
+// of the first three levels a lane keeps part of the components (and only
+// exchanges the others), so 8 shuffles + 8 adds replace 25 + 25.  Each final
+// sum equals warp_butterfly's bit for bit (same pairs; a + b == b + a).  The
+// warp's five sums end in lanes 0..4 as components {0, 3, 2, 4, 1}; those lanes
+// store them into out (the warp's Acc slot in shared memory).
+__device__ __forceinline__ void warp_reduce_scatter(const Acc& v, float* out, int lane) {
+  const unsigned F = 0xffffffffu;
+  const bool odd = lane & 1, b1 = (lane >> 1) & 1, b2 = (lane >> 2) & 1;
+  // level 1 (lanes l, l^1): even lanes keep {a0, cx, cy}, odd lanes {cz, aR}
+  const float r0 = __shfl_xor_sync(F, odd ? v.a0 : v.cz, 1);
+  const float r1 = __shfl_xor_sync(F, odd ? v.cx : v.aR, 1);
+  const float r2 = __shfl_xor_sync(F, v.cy, 1);
+  const float k0 = __fadd_rn(odd ? v.cz : v.a0, r0);
+  const float k1 = __fadd_rn(odd ? v.aR : v.cx, r1);
+  const float k2 = __fadd_rn(v.cy, r2);
+  // level 2 (l, l^2): even: b1 = 0 keeps {a0, cx}, b1 = 1 keeps {cy}; odd: b1 = 0 keeps cz, b1 = 1 keeps aR
+  const bool e0 = !odd && !b1;
+  const float s0 = odd ? (b1 ? k0 : k1) : (b1 ? k0 : k2);
+  const float q0 = __shfl_xor_sync(F, s0, 2);
+  const float q1 = __shfl_xor_sync(F, k1, 2);
+  const float m0 = __fadd_rn(odd ? (b1 ? k1 : k0) : (b1 ? k2 : k0), q0);
+  const float m1 = __fadd_rn(k1, q1);   // meaningful on e0 lanes only
+  // level 3 (l, l^4): e0 lanes split {a0, cx} by b2; the others hold one component
+  const float t0 = __shfl_xor_sync(F, (e0 && !b2) ? m1 : m0, 4);
+  float n0 = __fadd_rn((e0 && b2) ? m1 : m0, t0);
+  // levels 4, 5: one component per lane
+  n0 = __fadd_rn(n0, __shfl_xor_sync(F, n0, 8));
+  n0 = __fadd_rn(n0, __shfl_xor_sync(F, n0, 16));
+  if (lane < 5) out[(0x14230u >> (4 * lane)) & 0xFu] = n0;
 }
 
 template <int W>
@@ -372,15 +474,15 @@ __device__ __forceinline__ bool cell_update(const EvoParams& P, CellState& s, co
   const float A0 = __fmul_rn(sum.a0, scale);
   const float twoR = __fmul_rn(2.0f, s.R);
   const float gden = D == 3 ? __fmul_rn(__fmul_rn(twoR, twoR), twoR) : __fmul_rn(twoR, twoR);
-  const float gamma = __fdiv_rn(1.0f, gden);
-  const float gs = __fmul_rn(gamma, scale);
+  const float gamma = rcp_approx(gden);
   s.E = __fmul_rn(gamma, A0);
   if (it == P.T + 1) return true;
+  const float gs = __fmul_rn(__fmul_rn(gamma, scale), P.k6_dR);   // the leaves' 6/dR
   const float gcx = -__fmul_rn(gs, sum.cx), gcy = -__fmul_rn(gs, sum.cy), gcz = -__fmul_rn(gs, sum.cz);
-  const float gR = __fmul_rn(gamma, __fsub_rn(__fmul_rn(sum.aR, scale),
-                                              __fmul_rn(__fdiv_rn(D == 3 ? 3.0f : 2.0f, s.R), A0)));
+  const float gR = __fmul_rn(gamma, __fsub_rn(__fmul_rn(__fmul_rn(sum.aR, scale), P.k6_dR),
+                                              __fmul_rn(__fmul_rn(D == 3 ? 3.0f : 2.0f, rcp_approx(s.R)), A0)));
   // step eps_n / 2 with eps_n = eps0 / sqrt(n), clipped (G8)
-  const float h = __fmul_rn(0.5f, __fdiv_rn(P.eps0, __fsqrt_rn((float)it)));
+  const float h = __fmul_rn(P.half_eps0, rsqrt_approx((float)it));
   const float dcx = clampf(-__fmul_rn(h, gcx), -P.max_step, P.max_step);
   const float dcy = clampf(-__fmul_rn(h, gcy), -P.max_step, P.max_step);
   const float dcz = D == 3 ? clampf(-__fmul_rn(h, gcz), -P.max_step, P.max_step) : 0.0f;
@@ -502,8 +604,12 @@ __device__ __forceinline__ void load_brick(uint16_t* brick, const EvoParams& P, 
   __syncthreads();
 }
 
+// resident CTAs per SM the register budget is sized for (shared memory allows 3)
+#ifndef SNK_BRICK_MINB8
+#define SNK_BRICK_MINB8 2
+#endif
 template <int D, int W, int S, bool SLAB, int CH, int L>
-__global__ void __launch_bounds__(32 * W, W == 4 ? 3 : 1) evolve_brick_kernel(const __grid_constant__ EvoParams P) {
+__global__ void __launch_bounds__(32 * W, W == 4 ? 3 : SNK_BRICK_MINB8) evolve_brick_kernel(const __grid_constant__ EvoParams P) {
   constexpr int B = CH << L;
   constexpr int EXT[3] = {brick_sx(S), S, S};       // brick extent per axis
   extern __shared__ __align__(16) uint16_t brick[];
@@ -564,10 +670,9 @@ __global__ void __launch_bounds__(32 * W, W == 4 ? 3 : 1) evolve_brick_kernel(co
       part = lane_sum<D, SLAB ? G_GLOBAL_SLAB : G_GLOBAL, S, CH, L>(P, C, j0, brick, halo);
       if (threadIdx.x == 0) atomicAdd(&g_evolve_stats[1], 1ull);
     }
-    Acc sum = warp_butterfly(part);
-    if (lane == 0) xch[it & 1][wsub] = sum;
+    warp_reduce_scatter(part, reinterpret_cast<float*>(&xch[it & 1][wsub]), lane);
     __syncthreads();   // also: every brick read of this iteration is done
-    if constexpr (W > 1) sum = warp_tree<W>(xch[it & 1]);
+    const Acc sum = warp_tree<W>(xch[it & 1]);
     if (cell_update<D>(P, s, C, sum, it)) break;
   }
   if (SLAB && __syncthreads_or(halo != 0)) s.flags |= SNK_F_HALO;
@@ -632,15 +737,19 @@ template <int D, int W, int S, bool SLAB>
 int32_t brick_B(const EvoParams& P, int B, cudaStream_t st) {
   // 8 samples per chunk: the brick kernel runs 12 warps/SM (shared memory
   // bound), so each warp needs the ILP of 8 independent sample chains
+#ifndef SNK_BRICK_CH
+#define SNK_BRICK_CH 8
+#endif
+  constexpr int C8 = SNK_BRICK_CH;
   switch (B) {
     case 1: return launch_brick<D, W, S, SLAB, 1, 0>(P, st);
     case 2: return launch_brick<D, W, S, SLAB, 2, 0>(P, st);
     case 4: return launch_brick<D, W, S, SLAB, 4, 0>(P, st);
-    case 8: return launch_brick<D, W, S, SLAB, 8, 0>(P, st);
-    case 16: return launch_brick<D, W, S, SLAB, 8, 1>(P, st);
-    case 32: return launch_brick<D, W, S, SLAB, 8, 2>(P, st);
-    case 64: return launch_brick<D, W, S, SLAB, 8, 3>(P, st);
-    case 128: return launch_brick<D, W, S, SLAB, 8, 4>(P, st);
+    case 8: return launch_brick<D, W, S, SLAB, (C8 < 8 ? C8 : 8), (C8 < 8 ? 1 : 0)>(P, st);
+    case 16: return launch_brick<D, W, S, SLAB, C8, (C8 < 8 ? 2 : 1)>(P, st);
+    case 32: return launch_brick<D, W, S, SLAB, C8, (C8 < 8 ? 3 : 2)>(P, st);
+    case 64: return launch_brick<D, W, S, SLAB, C8, (C8 < 8 ? 4 : 3)>(P, st);
+    case 128: return launch_brick<D, W, S, SLAB, C8, (C8 < 8 ? 5 : 4)>(P, st);
     default: return fail(SNK_CONFIG, "samples per thread must be a power of two <= 128");
   }
 }
@@ -703,10 +812,10 @@ int32_t evolve_impl(const snk_grid* g, const snk_params* p, const uint16_t* d_im
   P.half_dR = (float)(p->delta_R / 2.0);
   P.inv_dR = (float)(1.0 / p->delta_R);
   P.inv_rho_dR = (float)(1.0 / (rho * p->delta_R));
-  P.k12_rho_dR = (float)(12.0 / (rho * p->delta_R));
-  P.km6_dR = (float)(-6.0 / p->delta_R);
+  P.k2_rho = (float)(2.0 / rho);
   P.k6_dR = (float)(6.0 / p->delta_R);
   P.eps0 = (float)p->eps0;
+  P.half_eps0 = (float)(p->eps0 / 2.0);
   P.max_step = (float)p->max_step;
   P.r_min = (float)p->r_min;
   P.r_max = (float)p->r_max;

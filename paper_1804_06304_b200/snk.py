@@ -16,7 +16,8 @@ import re
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libsnk.so")
+# SNK_LIB: an alternative build (tuning experiments, scripts/); default the in-tree libsnk.so
+LIB_PATH = os.environ.get("SNK_LIB") or os.path.join(HERE, "libsnk.so")
 HEADER = os.path.join(os.path.dirname(HERE), "include", "snk.h")
 
 OK, EMPTY_DOMAIN, CONFIG, SHAPE, INTERNAL, CUDA, CAPACITY = 0, 1, 2, 3, 4, 5, 6

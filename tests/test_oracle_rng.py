@@ -87,3 +87,30 @@ def test_direction_hatbox(ora):
     az = np.arctan2(om[:, 1], om[:, 0])
     counts, _ = np.histogram(az, np.linspace(-np.pi, np.pi, 17))
     assert stats.chisquare(counts).pvalue > 0.01
+
+
+@pytest.mark.parametrize("dim", [3, 2])
+def test_word_stream_layout(ora, dim):
+    """G11: the samples of one cell-iteration consume the Philox word stream in
+    order, each word once (3D: 3 words per sample, 4 samples per 3 blocks; 2D: 2
+    words per sample).  The uniforms are recovered from the sample itself."""
+    it, cid, seed, rho_s = 11, (5 << 32) + 9, 1804063040, 2.5
+    key = [seed & 0xFFFFFFFF, seed >> 32]
+    words = []
+    for b in range(8):
+        words += [int(x) for x in ora.philox4x32_10([b, it, cid & 0xFFFFFFFF, cid >> 32], key)]
+    u = [(w >> 9) * 2.0 ** -23 for w in words]
+    k = 3 if dim == 3 else 2
+    for j in range(10):
+        om, t = ora.sample(dim, j, it, cid, seed, rho_s)
+        got_u1 = (np.arctan2(om[1], om[0]) / (2 * np.pi)) % 1.0
+        if dim == 3:
+            assert abs((1.0 - om[2]) / 2.0 - u[3 * j]) < 1e-12
+            assert abs((t / rho_s) ** 3 - u[3 * j + 2]) < 1e-12
+            exp_u1 = u[3 * j + 1]
+        else:
+            assert abs((t / rho_s) ** 2 - u[2 * j + 1]) < 1e-12
+            exp_u1 = u[2 * j]
+        d = abs(got_u1 - exp_u1)
+        assert min(d, 1.0 - d) < 1e-12, (j, got_u1, exp_u1)
+    assert k * 10 <= len(words)
