@@ -114,12 +114,12 @@ __device__ __forceinline__ float u01(uint32_t x) {
   return __fsub_rn(__uint_as_float(0x3F800000u | (x >> 9)), 1.0f);
 }
 
-// u16 value v as a float offset by 2^23 (exact).
-__device__ __forceinline__ float mag(uint32_t v) { return __uint_as_float(kMagicBits | v); }
-
-__device__ __forceinline__ float lerp_mag(float A, float Bm, float f) {
-  // A, Bm are values + 2^23: a + f (b - a), with b - a = Bm - A exact and a = A - 2^23 exact
-  return __fmaf_rn(f, __fsub_rn(Bm, A), __fsub_rn(A, kMagic));
+// u16 value -> float, exact: one I2FP.F32.U32 (ALU pipe; the compiler's own
+// conversion of a known-16-bit value is the slow I2F.U16 on the SFU pipe)
+__device__ __forceinline__ float mag(uint32_t v) {
+  float r;
+  asm("cvt.rn.f32.u32 %0, %1;" : "=f"(r) : "r"(v));
+  return r;
 }
 
 __device__ __forceinline__ float lerp(float a, float b, float f) {
@@ -311,8 +311,8 @@ __device__ __forceinline__ Acc sample_leaf(const EvoParams& P, const CellIt& C, 
     }
   }
   // trilinear: x, then y, then z (G17)
-  float tri = lerp(lerp_mag(v000, v100, fx), lerp_mag(v010, v110, fx), fy);
-  if (D == 3) tri = lerp(tri, lerp(lerp_mag(v001, v101, fx), lerp_mag(v011, v111, fx), fy), fz);
+  float tri = lerp(lerp(v000, v100, fx), lerp(v010, v110, fx), fy);
+  if (D == 3) tri = lerp(tri, lerp(lerp(v001, v101, fx), lerp(v011, v111, fx), fy), fz);
   return leaves(P, C, d, tri, D == 3);
 }
 
