@@ -59,6 +59,7 @@ struct EvoParams {
   float vscale;                  // iscale * (4/3 pi | pi) / N
   float half_eps0;               // eps0 / 2
   int T;
+  int dom_small;                 // some axis has n - 1 < 2 (r_max + dR/2)
   uint32_t rk0[10], rk1[10];     // Philox round keys (seed + r * Weyl)
 };
 
@@ -386,8 +387,8 @@ __device__ __forceinline__ Acc warp_butterfly(Acc s) {
 // exchanges the others), so 8 shuffles + 8 adds replace 25 + 25.  Each final
 // sum equals warp_butterfly's bit for bit (same pairs; a + b == b + a).  The
 // warp's five sums end in lanes 0..4 as components {0, 3, 2, 4, 1}; those lanes
-// store them into out (the warp's Acc slot in shared memory).
-__device__ __forceinline__ void warp_reduce_scatter(const Acc& v, float* out, int lane) {
+// store them into out[component * stride].
+__device__ __forceinline__ void warp_reduce_scatter(const Acc& v, float* out, int lane, int stride) {
   const unsigned F = 0xffffffffu;
   const bool odd = lane & 1, b1 = (lane >> 1) & 1, b2 = (lane >> 2) & 1;
   // level 1 (lanes l, l^1): even lanes keep {a0, cx, cy}, odd lanes {cz, aR}
@@ -410,7 +411,28 @@ __device__ __forceinline__ void warp_reduce_scatter(const Acc& v, float* out, in
   // levels 4, 5: one component per lane
   n0 = __fadd_rn(n0, __shfl_xor_sync(F, n0, 8));
   n0 = __fadd_rn(n0, __shfl_xor_sync(F, n0, 16));
-  if (lane < 5) out[(0x14230u >> (4 * lane)) & 0xFu] = n0;
+  if (lane < 5) out[((0x14230u >> (4 * lane)) & 0xFu) * stride] = n0;
+}
+
+// Pairwise tree over the W warps' partial sums of one component (same pairs as warp_tree).
+template <int W>
+__device__ __forceinline__ float comp_tree(const float* v) {
+  float t[W];
+  if constexpr (W % 4 == 0) {
+#pragma unroll
+    for (int w = 0; w < W; w += 4) {
+      const float4 q = *reinterpret_cast<const float4*>(v + w);
+      t[w] = q.x; t[w + 1] = q.y; t[w + 2] = q.z; t[w + 3] = q.w;
+    }
+  } else {
+#pragma unroll
+    for (int w = 0; w < W; ++w) t[w] = v[w];
+  }
+#pragma unroll
+  for (int span = 1; span < W; span <<= 1)
+#pragma unroll
+    for (int w = 0; w + span < W; w += 2 * span) t[w] = __fadd_rn(t[w], t[w + span]);
+  return t[0];
 }
 
 template <int W>
@@ -431,9 +453,10 @@ __device__ __forceinline__ float clampf(float v, float lo, float hi) { return fm
 struct CellState {
   float sx, sy, sz;     // seed
   float cx, cy, cz, R, E;
+  float llo[3], lhi[3]; // leash box: seed -+ leash
   uint32_t flags;
   int64_t id;
-  uint32_t id_lo, id_hi;
+  uint32_t q0, q1, q3;  // Philox round-1 words of the constant counter words (id), keyed
 };
 
 __device__ __forceinline__ void cell_begin(const EvoParams& P, int64_t cell, int D, CellState& s) {
@@ -441,8 +464,20 @@ __device__ __forceinline__ void cell_begin(const EvoParams& P, int64_t cell, int
   s.sy = P.seeds[3 * cell + 1];
   s.sz = D == 3 ? P.seeds[3 * cell + 2] : 0.0f;
   s.id = P.ids ? P.ids[cell] : P.id_base + cell;
-  s.id_lo = (uint32_t)((uint64_t)s.id & 0xffffffffu);
-  s.id_hi = (uint32_t)((uint64_t)s.id >> 32);
+  const uint32_t id_lo = (uint32_t)((uint64_t)s.id & 0xffffffffu);
+  const uint32_t id_hi = (uint32_t)((uint64_t)s.id >> 32);
+  // Philox round 1 for ctr = {b, n, id_lo, id_hi}: the M1 * id_lo product and
+  // the key words do not depend on (b, n)
+  const uint64_t p1 = (uint64_t)kM1 * id_lo;
+  s.q0 = (uint32_t)(p1 >> 32) ^ P.rk0[0];
+  s.q1 = (uint32_t)p1;
+  s.q3 = id_hi ^ P.rk1[0];
+  const float sd[3] = {s.sx, s.sy, s.sz};
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    s.llo[a] = __fsub_rn(sd[a], P.leash);
+    s.lhi[a] = __fadd_rn(sd[a], P.leash);
+  }
   s.cx = s.sx; s.cy = s.sy; s.cz = s.sz;
   s.R = P.r0;
   s.E = 0.0f;
@@ -454,11 +489,9 @@ __device__ __forceinline__ CellIt cell_iter(const EvoParams& P, const CellState&
   C.cx = s.cx; C.cy = s.cy; C.cz = s.cz;
   C.rho_s = __fadd_rn(s.R, P.half_dR);
   C.a = __fmul_rn(-__fsub_rn(s.R, P.half_dR), P.inv_dR);
-  // Philox round 1: the words that come from c1 = n, c2 = id_lo, c3 = id_hi
-  const uint64_t p1 = (uint64_t)kM1 * s.id_lo;
-  C.p0 = (uint32_t)(p1 >> 32) ^ (uint32_t)it ^ P.rk0[0];
-  C.p1 = (uint32_t)p1;
-  C.p3 = s.id_hi ^ P.rk1[0];
+  C.p0 = s.q0 ^ (uint32_t)it;
+  C.p1 = s.q1;
+  C.p3 = s.q3;
   C.lg2_rho_s = lg2_approx(C.rho_s);
   C.boff = 0;
   return C;
@@ -488,21 +521,26 @@ __device__ __forceinline__ bool cell_update(const EvoParams& P, CellState& s, co
   const float dcz = D == 3 ? clampf(-__fmul_rn(h, gcz), -P.max_step, P.max_step) : 0.0f;
   const float dR = clampf(-__fmul_rn(h, gR), -P.max_step, P.max_step);
   const float ox = s.cx, oy = s.cy, oz = s.cz, oR = s.R;
-  float cx = __fadd_rn(s.cx, dcx), cy = __fadd_rn(s.cy, dcy), cz = __fadd_rn(s.cz, dcz);
+  const float cx = __fadd_rn(s.cx, dcx), cy = __fadd_rn(s.cy, dcy), cz = __fadd_rn(s.cz, dcz);
   const float R = clampf(__fadd_rn(s.R, dR), P.r_min, P.r_max);
   // leash
-  const float lx = clampf(cx, __fsub_rn(s.sx, P.leash), __fadd_rn(s.sx, P.leash));
-  const float ly = clampf(cy, __fsub_rn(s.sy, P.leash), __fadd_rn(s.sy, P.leash));
-  const float lz = clampf(cz, __fsub_rn(s.sz, P.leash), __fadd_rn(s.sz, P.leash));
-  const bool leashed = (lx != cx) || (ly != cy) || (lz != cz);
-  cx = lx; cy = ly; cz = lz;
-  // domain: c_a in [m, n_a - 1 - m], m = R + dR/2, or the axis centre
-  const float m = __fadd_rn(R, P.half_dR), m2 = __fmul_rn(2.0f, m);
-  const float dx = P.fnx1 < m2 ? __fmul_rn(0.5f, P.fnx1) : clampf(cx, m, __fsub_rn(P.fnx1, m));
-  const float dy = P.fny1 < m2 ? __fmul_rn(0.5f, P.fny1) : clampf(cy, m, __fsub_rn(P.fny1, m));
-  float dz = cz;
-  if (D == 3) dz = P.fnz1 < m2 ? __fmul_rn(0.5f, P.fnz1) : clampf(cz, m, __fsub_rn(P.fnz1, m));
-  const bool domained = (dx != cx) || (dy != cy) || (dz != cz);
+  const float lx = clampf(cx, s.llo[0], s.lhi[0]);
+  const float ly = clampf(cy, s.llo[1], s.lhi[1]);
+  const float lz = D == 3 ? clampf(cz, s.llo[2], s.lhi[2]) : cz;
+  // domain: c_a in [m, n_a - 1 - m], m = R + dR/2, or the axis centre when
+  // n_a - 1 < 2m (P.dom_small: possible for some axis at all)
+  const float m = __fadd_rn(R, P.half_dR);
+  float dx, dy, dz = lz;
+  if (P.dom_small) {
+    const float m2 = __fmul_rn(2.0f, m);
+    dx = P.fnx1 < m2 ? __fmul_rn(0.5f, P.fnx1) : clampf(lx, m, __fsub_rn(P.fnx1, m));
+    dy = P.fny1 < m2 ? __fmul_rn(0.5f, P.fny1) : clampf(ly, m, __fsub_rn(P.fny1, m));
+    if (D == 3) dz = P.fnz1 < m2 ? __fmul_rn(0.5f, P.fnz1) : clampf(lz, m, __fsub_rn(P.fnz1, m));
+  } else {
+    dx = clampf(lx, m, __fsub_rn(P.fnx1, m));
+    dy = clampf(ly, m, __fsub_rn(P.fny1, m));
+    if (D == 3) dz = clampf(lz, m, __fsub_rn(P.fnz1, m));
+  }
   s.cx = dx; s.cy = dy; s.cz = dz;
   s.R = R;
   if (it == P.T) {
@@ -511,8 +549,8 @@ __device__ __forceinline__ bool cell_update(const EvoParams& P, CellState& s, co
     mv = fmaxf(mv, fabsf(__fsub_rn(s.cy, oy)));
     mv = fmaxf(mv, fabsf(__fsub_rn(s.cz, oz)));
     if (mv < P.conv_tol) s.flags |= SNK_F_CONVERGED;
-    if (leashed) s.flags |= SNK_F_LEASHED;
-    if (domained) s.flags |= SNK_F_DOMAIN;
+    if ((lx != cx) || (ly != cy) || (lz != cz)) s.flags |= SNK_F_LEASHED;
+    if ((dx != lx) || (dy != ly) || (dz != lz)) s.flags |= SNK_F_DOMAIN;
   }
   return false;
 }
@@ -613,13 +651,19 @@ __global__ void __launch_bounds__(32 * W, W == 4 ? 3 : SNK_BRICK_MINB8) evolve_b
   constexpr int B = CH << L;
   constexpr int EXT[3] = {brick_sx(S), S, S};       // brick extent per axis
   extern __shared__ __align__(16) uint16_t brick[];
-  __shared__ Acc xch[2][W];
+  __shared__ __align__(16) float xch[2][5][W];      // [parity][component][warp]
   const int lane = threadIdx.x & 31, wsub = threadIdx.x >> 5;
   const int64_t cell = blockIdx.x;
   CellState s;
   cell_begin(P, cell, D, s);
   uint32_t halo = 0;
   int b[3] = {-(1 << 28), -(1 << 28), -(1 << 28)};   // brick origin (global voxels); none yet
+  // fast test: the ball's tap box [floor(c - ext), floor(c + ext) + 1] lies in
+  // the brick iff c - ext >= in_lo and c + ext < in_hi per axis (exact for the
+  // integer bounds); only set for a brick inside the volume, so containment
+  // also means no clamping is needed
+  float in_lo[3] = {INFINITY, INFINITY, INFINITY}, in_hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+  uint32_t boff = 0;
   const int n[3] = {P.nx, P.ny, P.nz};
   // z range the brick may cover: the slab buffer
   const int zlo = SLAB ? P.z_lo : 0, zhi = SLAB ? P.z_lo + P.nz_buf - 1 : P.nz - 1;
@@ -629,50 +673,73 @@ __global__ void __launch_bounds__(32 * W, W == 4 ? 3 : SNK_BRICK_MINB8) evolve_b
     // bounding box of the sampled ball, with a margin for the fp32 rounding of t and k
     const float ext = __fmaf_rn(C.rho_s, 1.0001f, 0.01f);
     const float c[3] = {s.cx, s.cy, s.cz};
-    bool interior = true, fits = true, inside = true;
-    int lo[3], hi[3];
+    float vlo[3], vhi[3];
+    bool fast = true;
 #pragma unroll
     for (int a = 0; a < D; ++a) {
-      lo[a] = (int)floorf(__fsub_rn(c[a], ext));
-      hi[a] = (int)floorf(__fadd_rn(c[a], ext)) + 1;
-      interior &= lo[a] >= 0 && hi[a] <= n[a] - 1;
-      lo[a] = max(lo[a], 0);
-      hi[a] = min(hi[a], n[a] - 1);
-      fits &= hi[a] - lo[a] + 1 <= (a == 0 ? EXT[0] - 1 : S);
-      inside &= lo[a] >= b[a] && hi[a] <= b[a] + EXT[a] - 1;
+      vlo[a] = __fsub_rn(c[a], ext);
+      vhi[a] = __fadd_rn(c[a], ext);
+      fast &= vlo[a] >= in_lo[a] && vhi[a] < in_hi[a];
     }
-    if (D == 3 && SLAB) fits &= lo[2] >= zlo && hi[2] <= zhi;
-    if (!inside && fits) {
-      // re-centre: the ball's box in the middle of the brick, clipped to the
-      // volume (z: the slab buffer); the x origin is even (4-byte copies)
+    int mode = 0;   // 0 brick, no clamp; 1 brick with clamp; 2 global gathers
+    if (!fast) {
+      bool interior = true, fits = true, inside = true;
+      int lo[3], hi[3];
 #pragma unroll
       for (int a = 0; a < D; ++a) {
-        const int amin = (a == 2) ? zlo : 0, amax = (a == 2) ? zhi : n[a] - 1;
-        int o = lo[a] - (EXT[a] - (hi[a] - lo[a] + 1)) / 2;
-        if (a == 0) o &= ~1;
-        o = min(o, amax + 1 - EXT[a]);
-        if (a == 0) o &= ~1;
-        o = max(o, amin);
-        b[a] = o;
+        lo[a] = (int)floorf(vlo[a]);
+        hi[a] = (int)floorf(vhi[a]) + 1;
+        interior &= lo[a] >= 0 && hi[a] <= n[a] - 1;
+        lo[a] = max(lo[a], 0);
+        hi[a] = min(hi[a], n[a] - 1);
+        fits &= hi[a] - lo[a] + 1 <= (a == 0 ? EXT[0] - 1 : S);
+        inside &= lo[a] >= b[a] && hi[a] <= b[a] + EXT[a] - 1;
       }
-      // every read of the old brick finished before last iteration's barrier
-      load_brick<D, S>(brick, P, b[0], b[1], D == 3 ? b[2] : 0, zlo);
-      inside = true;
-      if (threadIdx.x == 0) atomicAdd(&g_evolve_stats[0], 1ull);
+      if (D == 3 && SLAB) fits &= lo[2] >= zlo && hi[2] <= zhi;
+      if (!inside && fits) {
+        // re-centre: the ball's box in the middle of the brick, clipped to the
+        // volume (z: the slab buffer); the x origin is even (4-byte copies)
+#pragma unroll
+        for (int a = 0; a < D; ++a) {
+          const int amin = (a == 2) ? zlo : 0, amax = (a == 2) ? zhi : n[a] - 1;
+          int o = lo[a] - (EXT[a] - (hi[a] - lo[a] + 1)) / 2;
+          if (a == 0) o &= ~1;
+          o = min(o, amax + 1 - EXT[a]);
+          if (a == 0) o &= ~1;
+          o = max(o, amin);
+          b[a] = o;
+          const bool in_vol = o >= 0 && o + EXT[a] - 1 <= n[a] - 1;
+          in_lo[a] = in_vol ? (float)o : INFINITY;
+          in_hi[a] = in_vol ? (float)(o + EXT[a] - 1) : -INFINITY;
+        }
+        // every read of the old brick finished before last iteration's barrier
+        load_brick<D, S>(brick, P, b[0], b[1], D == 3 ? b[2] : 0, zlo);
+        boff = (kMagicBits + (uint32_t)b[0]) + (kMagicBits + (uint32_t)b[1]) * (uint32_t)brick_sx(S);
+        if (D == 3) boff += (kMagicBits + (uint32_t)b[2]) * (uint32_t)(brick_sx(S) * S);
+        inside = true;
+        if (threadIdx.x == 0) atomicAdd(&g_evolve_stats[0], 1ull);
+      }
+      mode = inside ? (interior ? 0 : 1) : 2;
     }
     Acc part;
-    if (inside) {
-      C.boff = (kMagicBits + (uint32_t)b[0]) + (kMagicBits + (uint32_t)b[1]) * (uint32_t)brick_sx(S);
-      if (D == 3) C.boff += (kMagicBits + (uint32_t)b[2]) * (uint32_t)(brick_sx(S) * S);
-      if (interior) part = lane_sum<D, G_BRICK_FAST, S, CH, L>(P, C, j0, brick, halo);
-      else part = lane_sum<D, G_BRICK_CLAMP, S, CH, L>(P, C, j0, brick, halo);
+    C.boff = boff;
+    if (mode == 0) {
+      part = lane_sum<D, G_BRICK_FAST, S, CH, L>(P, C, j0, brick, halo);
+    } else if (mode == 1) {
+      part = lane_sum<D, G_BRICK_CLAMP, S, CH, L>(P, C, j0, brick, halo);
     } else {
       part = lane_sum<D, SLAB ? G_GLOBAL_SLAB : G_GLOBAL, S, CH, L>(P, C, j0, brick, halo);
       if (threadIdx.x == 0) atomicAdd(&g_evolve_stats[1], 1ull);
     }
-    warp_reduce_scatter(part, reinterpret_cast<float*>(&xch[it & 1][wsub]), lane);
+    float* xo = &xch[it & 1][0][0];
+    warp_reduce_scatter(part, xo + wsub, lane, W);
     __syncthreads();   // also: every brick read of this iteration is done
-    const Acc sum = warp_tree<W>(xch[it & 1]);
+    Acc sum;
+    sum.a0 = comp_tree<W>(xo + 0 * W);
+    sum.cx = comp_tree<W>(xo + 1 * W);
+    sum.cy = comp_tree<W>(xo + 2 * W);
+    sum.cz = comp_tree<W>(xo + 3 * W);
+    sum.aR = comp_tree<W>(xo + 4 * W);
     if (cell_update<D>(P, s, C, sum, it)) break;
   }
   if (SLAB && __syncthreads_or(halo != 0)) s.flags |= SNK_F_HALO;
@@ -824,6 +891,10 @@ int32_t evolve_impl(const snk_grid* g, const snk_params* p, const uint16_t* d_im
   const double pi = 3.14159265358979323846;
   P.vscale = (float)(p->intensity_scale * (D == 3 ? 4.0 / 3.0 * pi : pi) / (double)p->n_samples);
   P.T = p->max_iters;
+  {
+    const double m2 = 2.0 * ((double)P.r_max + (double)P.half_dR) * (1.0 + 1e-6) + 1e-3;   // conservative
+    P.dom_small = (double)P.fnx1 < m2 || (double)P.fny1 < m2 || (D == 3 && (double)P.fnz1 < m2);
+  }
   uint32_t k0 = (uint32_t)(p->seed & 0xffffffffu), k1 = (uint32_t)(p->seed >> 32);
   for (int r = 0; r < 10; ++r) {
     P.rk0[r] = k0;
