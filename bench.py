@@ -101,14 +101,9 @@ def workload_name(cfg):
 
 
 # ---------------------------------------------------------------- CPU oracle sample
-def oracle_crop_run(cfg, raw_full, target_cells: int, threads: int):
-    """The oracle as it stands on a bounded sample of the workload: a crop of the
-    raw volume, a2 blur -> a4 maxima seeds (crop interior) -> a5/a6 evolution ->
-    a7 cull.  Returns (samples, seconds, description)."""
-    import oracle
-    oracle.set_num_threads(threads)
+def crop_geometry(cfg, target_cells: int):
+    """Crop box (lo, hi) and its seeded interior (ilo, ihi) for about target_cells cells."""
     n = cfg.iso_n
-    assert tuple(n) == tuple(cfg.n), "cpu sample needs an isotropic config"
     vox_per_cell = float(np.prod(cfg.pitch[:cfg.dim])) / 1.5
     L = int(round((target_cells * vox_per_cell) ** (1.0 / cfg.dim)))
     L = max(32, min(L, min(n[:cfg.dim]) - 1))
@@ -118,7 +113,23 @@ def oracle_crop_run(cfg, raw_full, target_cells: int, threads: int):
     hi = [min(c[a] + L // 2 + reach, n[a] - 1) if a < cfg.dim else 0 for a in range(3)]
     ilo = [max(c[a] - L // 2, 0) if a < cfg.dim else 0 for a in range(3)]
     ihi = [min(c[a] + L // 2 - 1, n[a] - 1) if a < cfg.dim else 0 for a in range(3)]
-    crop = np.ascontiguousarray(raw_full[lo[2]:hi[2] + 1, lo[1]:hi[1] + 1, lo[0]:hi[0] + 1])
+    return lo, hi, ilo, ihi
+
+
+def oracle_crop_run(cfg, raw_full, target_cells: int, threads: int):
+    """The oracle as it stands on a bounded sample of the workload: a crop of the
+    raw volume, a2 blur -> a4 maxima seeds (crop interior) -> a5/a6 evolution ->
+    a7 cull.  raw_full: the (nz, ny, nx) volume, or a callable (lo, hi) -> crop.
+    Returns (samples, seconds, description, cells)."""
+    import oracle
+    oracle.set_num_threads(threads)
+    n = cfg.iso_n
+    assert tuple(n) == tuple(cfg.n), "cpu sample needs an isotropic config"
+    lo, hi, ilo, ihi = crop_geometry(cfg, target_cells)
+    if callable(raw_full):
+        crop = np.ascontiguousarray(raw_full(lo, hi))
+    else:
+        crop = np.ascontiguousarray(raw_full[lo[2]:hi[2] + 1, lo[1]:hi[1] + 1, lo[0]:hi[0] + 1])
     p = oracle.Params(r0=cfg.r0, n_samples=cfg.n_samples, max_iters=cfg.max_iters, dim=cfg.dim,
                       seed=cfg.philox_seed)
     t0 = time.perf_counter()
@@ -254,26 +265,17 @@ def run_reference(args):
         return None
     cfg = synth.CONFIGS[args.config]
     threads = os.cpu_count() or 1
-    # the bounded sample: a crop of the same workload (generated once, outside the timing)
-    raw = synth.generate(cfg) if np.prod(cfg.n) <= 64 * 2**20 else None
-    if raw is None:
-        # generate only the planes the crop needs
-        n = cfg.iso_n
-        raw = np.zeros((1, 1, 1), np.uint16)
-        zc = n[2] // 2
-        half = 120
-        z0, z1 = max(zc - half, 0), min(zc + half, n[2])
-        part = synth.generate(cfg, z0, z1)
+    # the bounded sample: a crop of the same workload (only its planes generated, outside the timing)
+    target = 60 * threads
+    lo, hi, _, _ = crop_geometry(cfg, target)
+    part = synth.generate(cfg, lo[2], hi[2] + 1)
 
-        class _Lazy:   # raw_full[z, y, x] slicing on the generated band
-            def __getitem__(self, key):
-                kz, ky, kx = key
-                return part[kz.start - z0:kz.stop - z0, ky, kx]
-        raw = _Lazy()
+    def raw(lo_, hi_):
+        return part[lo_[2] - lo[2]:hi_[2] - lo[2] + 1, lo_[1]:hi_[1] + 1, lo_[0]:hi_[0] + 1]
     samples = secs = 0.0
     desc = ""
     for k in range(args.warmup + args.steps):
-        s, dt, desc, _ = oracle_crop_run(cfg, raw, target_cells=60 * threads, threads=threads)
+        s, dt, desc, _ = oracle_crop_run(cfg, raw, target_cells=target, threads=threads)
         if k >= args.warmup:
             samples += s
             secs += dt

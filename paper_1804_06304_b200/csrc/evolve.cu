@@ -173,7 +173,7 @@ __device__ __forceinline__ Draw draw_words(const CellIt& C, uint32_t w0, uint32_
   if (D == 3) {
     const float u0 = u01(w0);
     d.oz = __fmaf_rn(-2.0f, u0, 1.0f);
-    const float st = __fmul_rn(2.0f, sqrt_approx(__fmaf_rn(-u0, u0, u0)));
+    const float st = sqrt_approx(__fmaf_rn(-d.oz, d.oz, 1.0f));   // sqrt(1 - z^2) = 2 sqrt(u0 (1 - u0))
     d.ox = __fmul_rn(st, cs);
     d.oy = __fmul_rn(st, sn);
     d.t = ex2_approx(__fmaf_rn(lg2_approx(u2), 0.333333343f, C.lg2_rho_s));   // rho_s cbrt(u2)

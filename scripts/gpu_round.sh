@@ -13,3 +13,5 @@ echo "smoke exit $?" >> $OUT/${TAG}_smoke.log
 timeout 600 python bench.py --config C3 --steps 3 --no-cpu-baseline > $OUT/${TAG}_bench_c3.json 2> $OUT/${TAG}_bench_c3.err
 timeout 900 python bench.py > $OUT/${TAG}_bench_c4.json 2> $OUT/${TAG}_bench_c4.err
 echo done
+timeout 900 python bench.py --impl reference > $OUT/${TAG}_bench_ref.json 2> $OUT/${TAG}_bench_ref.err
+echo done-ref
