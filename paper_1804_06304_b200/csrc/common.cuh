@@ -99,8 +99,8 @@ int32_t label_impl(const snk_grid* g, const snk_params* p, const snk_cell* d_det
 int evolve_warps_per_cell(const snk_params* p, int64_t n_cells);
 int32_t evolve_stats(int64_t out[4], bool reset);
 
-// vectorised separable pass (volume.cu): op 0 = Q14 blur with the taps last
-// uploaded by preprocess, 1 = box max clipped to [lo, hi] on the pass axis;
+// vectorised separable pass (volume.cu): op must be 1 = box max clipped to
+// [lo, hi] on the pass axis (the blur passes are internal to preprocess);
 // radius h <= 8; needs nx % 8 == 0 and 16-byte aligned buffers (vec8_ok)
 bool vec8_ok(const snk_grid* g, const void* a, const void* b, const void* c);
 int32_t sep_pass(int axis, int op, int h, const uint16_t* in, uint16_t* out, int nx, int ny, int nz,

@@ -16,7 +16,11 @@ namespace snk {
 namespace {
 
 constexpr int kMaxTaps = 65;   // 2 * ceil(4 * 8) + 1
-__constant__ int32_t c_taps[kMaxTaps];
+// Q14 taps, passed to the kernels by value (no shared __constant__ state, so
+// concurrent calls on different streams with different sigma cannot race)
+struct Taps {
+  int32_t w[kMaxTaps];
+};
 
 // Q14 Gaussian taps (reading G18): h = ceil(4 sigma),
 // w_i = round(16384 exp(-i^2 / 2 sigma^2) / sum), centre absorbs the remainder.
@@ -47,7 +51,7 @@ int q14_taps(double sigma, std::vector<int32_t>& taps) {
 template <int AXIS>
 __global__ void __launch_bounds__(256) blur_pass_kernel(const uint16_t* __restrict__ in,
                                                         uint16_t* __restrict__ out, int nx, int ny,
-                                                        int nz, int h) {
+                                                        int nz, int h, const __grid_constant__ Taps T) {
   const int64_t pairs_per_row = (nx + 1) >> 1;
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t total = pairs_per_row * ny * nz;
@@ -62,7 +66,7 @@ __global__ void __launch_bounds__(256) blur_pass_kernel(const uint16_t* __restri
   if (AXIS == 0) {
     const uint16_t* r = in + row * nx;
     for (int i = -h; i <= h; ++i) {
-      const uint32_t w = (uint32_t)c_taps[i + h];
+      const uint32_t w = (uint32_t)T.w[i + h];
       const int xa = min(max(x0 + i, 0), nx - 1);
       const int xb = min(max(x0 + 1 + i, 0), nx - 1);
       acc0 += w * __ldg(r + xa);
@@ -74,7 +78,7 @@ __global__ void __launch_bounds__(256) blur_pass_kernel(const uint16_t* __restri
     const int64_t stride = AXIS == 1 ? nx : plane;
     const uint16_t* base = in + row * nx - (int64_t)p * stride + x0;
     for (int i = -h; i <= h; ++i) {
-      const uint32_t w = (uint32_t)c_taps[i + h];
+      const uint32_t w = (uint32_t)T.w[i + h];
       const int q = min(max(p + i, 0), np - 1);
       const uint16_t* src = base + (int64_t)q * stride;
       acc0 += w * __ldg(src);
@@ -84,6 +88,12 @@ __global__ void __launch_bounds__(256) blur_pass_kernel(const uint16_t* __restri
   uint16_t* o = out + row * nx + x0;
   o[0] = (uint16_t)(acc0 >> 14);
   if (two) o[1] = (uint16_t)(acc1 >> 14);
+}
+
+__device__ __forceinline__ float sqrt_approx_f(float x) {
+  float r;
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
 }
 
 // a3: G = (isqrt(gx^2 + gy^2 + gz^2) + 1) >> 1, central differences, clamp-to-edge.
@@ -169,7 +179,8 @@ __device__ __forceinline__ uint4 pack8(const uint32_t* o) {
 
 template <int AXIS, int OP, int H>
 __global__ void __launch_bounds__(256) sep8_kernel(const uint16_t* __restrict__ in, uint16_t* __restrict__ out,
-                                                   int nx, int ny, int nz, int lo, int hi) {
+                                                   int nx, int ny, int nz, int lo, int hi,
+                                                   const __grid_constant__ Taps T) {
   const int nc = nx >> 3;
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= (int64_t)nc * ny * nz) return;
@@ -197,7 +208,7 @@ __global__ void __launch_bounds__(256) sep8_kernel(const uint16_t* __restrict__ 
       uint32_t acc = OP == OP_BLUR ? 8192u : 0u;
 #pragma unroll
       for (int i = -H; i <= H; ++i) {
-        if (OP == OP_BLUR) acc += (uint32_t)c_taps[i + H] * v[8 + k + i];
+        if (OP == OP_BLUR) acc += (uint32_t)T.w[i + H] * v[8 + k + i];
         else acc = max(acc, v[8 + k + i]);
       }
       o[k] = OP == OP_BLUR ? acc >> 14 : acc;
@@ -218,7 +229,7 @@ __global__ void __launch_bounds__(256) sep8_kernel(const uint16_t* __restrict__ 
       unpack8(__ldg(base + (int64_t)q * stride), v);
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
-        if (OP == OP_BLUR) o[k] += (uint32_t)c_taps[i + H] * v[k];
+        if (OP == OP_BLUR) o[k] += (uint32_t)T.w[i + H] * v[k];
         else o[k] = max(o[k], v[k]);
       }
     }
@@ -232,11 +243,11 @@ __global__ void __launch_bounds__(256) sep8_kernel(const uint16_t* __restrict__ 
 
 template <int AXIS, int OP>
 int32_t sep8_launch(int h, const uint16_t* in, uint16_t* out, int nx, int ny, int nz, int lo, int hi,
-                    cudaStream_t st) {
+                    const Taps& tp, cudaStream_t st) {
   const unsigned grid = (unsigned)ceil_div((int64_t)(nx / 8) * ny * nz, 256);
   switch (h) {
 #define SNK_SEP_CASE(HH) \
-    case HH: sep8_kernel<AXIS, OP, HH><<<grid, 256, 0, st>>>(in, out, nx, ny, nz, lo, hi); break;
+    case HH: sep8_kernel<AXIS, OP, HH><<<grid, 256, 0, st>>>(in, out, nx, ny, nz, lo, hi, tp); break;
     SNK_SEP_CASE(0) SNK_SEP_CASE(1) SNK_SEP_CASE(2) SNK_SEP_CASE(3) SNK_SEP_CASE(4)
     SNK_SEP_CASE(5) SNK_SEP_CASE(6) SNK_SEP_CASE(7) SNK_SEP_CASE(8)
 #undef SNK_SEP_CASE
@@ -259,7 +270,8 @@ constexpr int kBX = 64, kBY = 16, kBZC = 32, kBThreads = 256;
 template <int H>
 __global__ void __launch_bounds__(kBThreads) blur3d_fused_kernel(const uint16_t* __restrict__ in,
                                                                  uint16_t* __restrict__ out, int nx,
-                                                                 int ny, int nz) {
+                                                                 int ny, int nz,
+                                                                 const __grid_constant__ Taps T) {
   constexpr int K = 2 * H + 1, RX = kBX + 2 * H, RY = kBY + 2 * H;
   __shared__ uint16_t s_in[RY][RX];
   __shared__ uint16_t s_x[RY][kBX];
@@ -302,7 +314,7 @@ __global__ void __launch_bounds__(kBThreads) blur3d_fused_kernel(const uint16_t*
         const int r = e / kBX, c = e % kBX;
         uint32_t acc = 8192;
 #pragma unroll
-        for (int i = 0; i < K; ++i) acc += (uint32_t)c_taps[i] * s_in[r][c + i];
+        for (int i = 0; i < K; ++i) acc += (uint32_t)T.w[i] * s_in[r][c + i];
         s_x[r][c] = (uint16_t)(acc >> 14);
       }
       __syncthreads();
@@ -310,7 +322,7 @@ __global__ void __launch_bounds__(kBThreads) blur3d_fused_kernel(const uint16_t*
       for (int k = 0; k < 4; ++k) {
         uint32_t acc = 8192;
 #pragma unroll
-        for (int i = 0; i < K; ++i) acc += (uint32_t)c_taps[i] * s_x[ty * 4 + k + i][tx];
+        for (int i = 0; i < K; ++i) acc += (uint32_t)T.w[i] * s_x[ty * 4 + k + i][tx];
         ring[j][k] = acc >> 14;
       }
       if (pi >= 2 * H) {
@@ -320,7 +332,7 @@ __global__ void __launch_bounds__(kBThreads) blur3d_fused_kernel(const uint16_t*
         for (int k = 0; k < 4; ++k) {
           uint32_t acc = 8192;
 #pragma unroll
-          for (int i = 0; i < K; ++i) acc += (uint32_t)c_taps[i] * ring[(j + 1 + i) % K][k];
+          for (int i = 0; i < K; ++i) acc += (uint32_t)T.w[i] * ring[(j + 1 + i) % K][k];
           if (x0 + tx < nx && y0 + ty * 4 + k < ny) dst[(int64_t)k * nx] = (uint16_t)(acc >> 14);
         }
       }
@@ -332,7 +344,7 @@ __global__ void __launch_bounds__(kBThreads) blur3d_fused_kernel(const uint16_t*
 template <int H>
 __global__ void __launch_bounds__(kBThreads) blur2d_fused_kernel(const uint16_t* __restrict__ in,
                                                                  uint16_t* __restrict__ out, int nx,
-                                                                 int ny) {
+                                                                 int ny, const __grid_constant__ Taps T) {
   constexpr int K = 2 * H + 1, RX = kBX + 2 * H, RY = kBY + 2 * H;
   __shared__ uint16_t s_in[RY][RX];
   __shared__ uint16_t s_x[RY][kBX];
@@ -348,7 +360,7 @@ __global__ void __launch_bounds__(kBThreads) blur2d_fused_kernel(const uint16_t*
     const int r = e / kBX, c = e % kBX;
     uint32_t acc = 8192;
 #pragma unroll
-    for (int i = 0; i < K; ++i) acc += (uint32_t)c_taps[i] * s_in[r][c + i];
+    for (int i = 0; i < K; ++i) acc += (uint32_t)T.w[i] * s_in[r][c + i];
     s_x[r][c] = (uint16_t)(acc >> 14);
   }
   __syncthreads();
@@ -356,7 +368,7 @@ __global__ void __launch_bounds__(kBThreads) blur2d_fused_kernel(const uint16_t*
   for (int k = 0; k < 4; ++k) {
     uint32_t acc = 8192;
 #pragma unroll
-    for (int i = 0; i < K; ++i) acc += (uint32_t)c_taps[i] * s_x[ty * 4 + k + i][tx];
+    for (int i = 0; i < K; ++i) acc += (uint32_t)T.w[i] * s_x[ty * 4 + k + i][tx];
     if (x0 + tx < nx && y0 + ty * 4 + k < ny)
       out[(int64_t)(y0 + ty * 4 + k) * nx + x0 + tx] = (uint16_t)(acc >> 14);
   }
@@ -406,15 +418,64 @@ __global__ void __launch_bounds__(kBThreads) gradmag_tiled_kernel(const uint16_t
   }
 }
 
+// a3, vectorised: 8 consecutive x outputs per thread from 16-byte loads (the
+// row, the rows y -+ 1, the planes z -+ 1, and the two x neighbours of the
+// group), no shared memory.  isqrt(v) from a float estimate corrected exactly
+// in 64-bit integers (the estimate is within 1).
+__device__ __forceinline__ uint32_t isqrt_est(uint64_t v, float vf) {
+  const float e = sqrt_approx_f(vf);
+  uint32_t r = __float_as_uint(__fadd_rz(e, 8388608.0f)) - 0x4B000000u;   // trunc(e), e < 2^23
+  if ((uint64_t)r * r > v) --r;
+  else if ((uint64_t)(r + 1) * (r + 1) <= v) ++r;
+  return r;
+}
+
+template <int D>
+__global__ void __launch_bounds__(256) gradmag8_kernel(const uint16_t* __restrict__ B, uint16_t* __restrict__ G,
+                                                       int nx, int ny, int nz) {
+  const int nc = nx >> 3;
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (int64_t)nc * ny * nz) return;
+  const int xc = (int)(t % nc);
+  const int64_t row = t / nc;
+  const int y = (int)(row % ny), z = (int)(row / ny);
+  const uint4* Bq = reinterpret_cast<const uint4*>(B);
+  const int64_t rs = nc, ps = (int64_t)nc * ny;   // row / plane strides in uint4
+  uint32_t c[8], ym[8], yp[8], zm[8], zp[8];
+  unpack8(__ldg(Bq + t), c);
+  unpack8(__ldg(Bq + t - (y > 0 ? rs : 0)), ym);
+  unpack8(__ldg(Bq + t + (y < ny - 1 ? rs : 0)), yp);
+  if (D == 3) {
+    unpack8(__ldg(Bq + t - (z > 0 ? ps : 0)), zm);
+    unpack8(__ldg(Bq + t + (z < nz - 1 ? ps : 0)), zp);
+  }
+  const uint16_t* rowp = B + row * nx + xc * 8;
+  const uint32_t l = xc > 0 ? __ldg(rowp - 1) : c[0];
+  const uint32_t r = xc < nc - 1 ? __ldg(rowp + 8) : c[7];
+  uint32_t o[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const int gx = (int)(k < 7 ? c[k + 1] : r) - (int)(k > 0 ? c[k - 1] : l);
+    const int gy = (int)yp[k] - (int)ym[k];
+    const int gz = D == 3 ? (int)zp[k] - (int)zm[k] : 0;
+    const uint64_t v = (uint64_t)((int64_t)gx * gx) + (uint64_t)((int64_t)gy * gy) + (uint64_t)((int64_t)gz * gz);
+    const float fx = (float)gx, fy = (float)gy, fz = (float)gz;
+    const float vf = __fmaf_rn(fx, fx, __fmaf_rn(fy, fy, __fmul_rn(fz, fz)));
+    o[k] = (isqrt_est(v, vf) + 1) >> 1;
+  }
+  reinterpret_cast<uint4*>(G)[t] = pack8(o);
+}
+
 template <int H>
-int32_t launch_fused_blur(const snk_grid* g, const uint16_t* d_in, uint16_t* d_out, cudaStream_t st) {
+int32_t launch_fused_blur(const snk_grid* g, const uint16_t* d_in, uint16_t* d_out, const Taps& tp,
+                          cudaStream_t st) {
   const int nx = (int)g->n[0], ny = (int)g->n[1], nz = (int)g->nz_buf;
   if (g->dim == 3) {
     dim3 grid((unsigned)ceil_div(nx, kBX), (unsigned)ceil_div(ny, kBY), (unsigned)ceil_div(nz, kBZC));
-    blur3d_fused_kernel<H><<<grid, kBThreads, 0, st>>>(d_in, d_out, nx, ny, nz);
+    blur3d_fused_kernel<H><<<grid, kBThreads, 0, st>>>(d_in, d_out, nx, ny, nz, tp);
   } else {
     dim3 grid((unsigned)ceil_div(nx, kBX), (unsigned)ceil_div(ny, kBY));
-    blur2d_fused_kernel<H><<<grid, kBThreads, 0, st>>>(d_in, d_out, nx, ny);
+    blur2d_fused_kernel<H><<<grid, kBThreads, 0, st>>>(d_in, d_out, nx, ny, tp);
   }
   SNK_LAUNCH_CHECK("blur_fused_kernel");
   return SNK_OK;
@@ -432,16 +493,22 @@ bool vec8_ok(const snk_grid* g, const void* a, const void* b, const void* c) {
   return g->n[0] % 8 == 0 && al(a) && al(b) && al(c);
 }
 
+namespace {
+int32_t sep_blur(int axis, int h, const Taps& tp, const uint16_t* in, uint16_t* out, int nx, int ny, int nz,
+                 cudaStream_t st) {
+  if (axis == 0) return sep8_launch<0, OP_BLUR>(h, in, out, nx, ny, nz, 0, 0, tp, st);
+  if (axis == 1) return sep8_launch<1, OP_BLUR>(h, in, out, nx, ny, nz, 0, 0, tp, st);
+  return sep8_launch<2, OP_BLUR>(h, in, out, nx, ny, nz, 0, 0, tp, st);
+}
+}  // namespace
+
 int32_t sep_pass(int axis, int op, int h, const uint16_t* in, uint16_t* out, int nx, int ny, int nz,
                  int lo, int hi, cudaStream_t st) {
-  if (op == OP_BLUR) {
-    if (axis == 0) return sep8_launch<0, OP_BLUR>(h, in, out, nx, ny, nz, lo, hi, st);
-    if (axis == 1) return sep8_launch<1, OP_BLUR>(h, in, out, nx, ny, nz, lo, hi, st);
-    return sep8_launch<2, OP_BLUR>(h, in, out, nx, ny, nz, lo, hi, st);
-  }
-  if (axis == 0) return sep8_launch<0, OP_MAX>(h, in, out, nx, ny, nz, lo, hi, st);
-  if (axis == 1) return sep8_launch<1, OP_MAX>(h, in, out, nx, ny, nz, lo, hi, st);
-  return sep8_launch<2, OP_MAX>(h, in, out, nx, ny, nz, lo, hi, st);
+  if (op != OP_MAX) return fail(SNK_INTERNAL, "sep_pass: blur passes go through preprocess");
+  const Taps none{};
+  if (axis == 0) return sep8_launch<0, OP_MAX>(h, in, out, nx, ny, nz, lo, hi, none, st);
+  if (axis == 1) return sep8_launch<1, OP_MAX>(h, in, out, nx, ny, nz, lo, hi, none, st);
+  return sep8_launch<2, OP_MAX>(h, in, out, nx, ny, nz, lo, hi, none, st);
 }
 
 int32_t preprocess_impl(const snk_grid* g, const snk_params* p, const uint16_t* d_in,
@@ -449,8 +516,8 @@ int32_t preprocess_impl(const snk_grid* g, const snk_params* p, const uint16_t* 
                         cudaStream_t st) {
   std::vector<int32_t> taps;
   const int h = q14_taps(p->sigma, taps);
-  SNK_CUDA_CHECK(cudaMemcpyToSymbolAsync(c_taps, taps.data(), taps.size() * sizeof(int32_t), 0,
-                                         cudaMemcpyHostToDevice, st));
+  Taps tp{};
+  for (size_t i = 0; i < taps.size() && i < (size_t)kMaxTaps; ++i) tp.w[i] = taps[i];
   const int nx = (int)g->n[0], ny = (int)g->n[1], nz = (int)g->nz_buf;
   const int64_t nvox = (int64_t)nx * ny * nz;
   Carve cv(d_ws, ws_bytes);
@@ -461,43 +528,48 @@ int32_t preprocess_impl(const snk_grid* g, const snk_params* p, const uint16_t* 
   } else if (h <= 8 && vec8_ok(g, d_in, d_smooth, tmp)) {
     // three (2D: two) streaming separable passes, 8 voxels per thread
     if (g->dim == 3) {
-      SNK_TRY(sep_pass(0, OP_BLUR, h, d_in, d_smooth, nx, ny, nz, 0, 0, st));
-      SNK_TRY(sep_pass(1, OP_BLUR, h, d_smooth, tmp, nx, ny, nz, 0, 0, st));
-      SNK_TRY(sep_pass(2, OP_BLUR, h, tmp, d_smooth, nx, ny, nz, 0, 0, st));
+      SNK_TRY(sep_blur(0, h, tp, d_in, d_smooth, nx, ny, nz, st));
+      SNK_TRY(sep_blur(1, h, tp, d_smooth, tmp, nx, ny, nz, st));
+      SNK_TRY(sep_blur(2, h, tp, tmp, d_smooth, nx, ny, nz, st));
     } else {
-      SNK_TRY(sep_pass(0, OP_BLUR, h, d_in, tmp, nx, ny, nz, 0, 0, st));
-      SNK_TRY(sep_pass(1, OP_BLUR, h, tmp, d_smooth, nx, ny, nz, 0, 0, st));
+      SNK_TRY(sep_blur(0, h, tp, d_in, tmp, nx, ny, nz, st));
+      SNK_TRY(sep_blur(1, h, tp, tmp, d_smooth, nx, ny, nz, st));
     }
   } else if (h <= 8) {
     switch (h) {
-      case 1: SNK_TRY(launch_fused_blur<1>(g, d_in, d_smooth, st)); break;
-      case 2: SNK_TRY(launch_fused_blur<2>(g, d_in, d_smooth, st)); break;
-      case 3: SNK_TRY(launch_fused_blur<3>(g, d_in, d_smooth, st)); break;
-      case 4: SNK_TRY(launch_fused_blur<4>(g, d_in, d_smooth, st)); break;
-      case 5: SNK_TRY(launch_fused_blur<5>(g, d_in, d_smooth, st)); break;
-      case 6: SNK_TRY(launch_fused_blur<6>(g, d_in, d_smooth, st)); break;
-      case 7: SNK_TRY(launch_fused_blur<7>(g, d_in, d_smooth, st)); break;
-      default: SNK_TRY(launch_fused_blur<8>(g, d_in, d_smooth, st)); break;
+      case 1: SNK_TRY(launch_fused_blur<1>(g, d_in, d_smooth, tp, st)); break;
+      case 2: SNK_TRY(launch_fused_blur<2>(g, d_in, d_smooth, tp, st)); break;
+      case 3: SNK_TRY(launch_fused_blur<3>(g, d_in, d_smooth, tp, st)); break;
+      case 4: SNK_TRY(launch_fused_blur<4>(g, d_in, d_smooth, tp, st)); break;
+      case 5: SNK_TRY(launch_fused_blur<5>(g, d_in, d_smooth, tp, st)); break;
+      case 6: SNK_TRY(launch_fused_blur<6>(g, d_in, d_smooth, tp, st)); break;
+      case 7: SNK_TRY(launch_fused_blur<7>(g, d_in, d_smooth, tp, st)); break;
+      default: SNK_TRY(launch_fused_blur<8>(g, d_in, d_smooth, tp, st)); break;
     }
   } else {
     // wide kernels (sigma > 2): three separable passes through the workspace
     const int64_t pairs = (int64_t)((nx + 1) / 2) * ny * nz;
     const unsigned grid = grid_for(pairs, 256);
     if (g->dim == 3) {
-      blur_pass_kernel<0><<<grid, 256, 0, st>>>(d_in, d_smooth, nx, ny, nz, h);
+      blur_pass_kernel<0><<<grid, 256, 0, st>>>(d_in, d_smooth, nx, ny, nz, h, tp);
       SNK_LAUNCH_CHECK("blur_pass_kernel<x>");
-      blur_pass_kernel<1><<<grid, 256, 0, st>>>(d_smooth, tmp, nx, ny, nz, h);
+      blur_pass_kernel<1><<<grid, 256, 0, st>>>(d_smooth, tmp, nx, ny, nz, h, tp);
       SNK_LAUNCH_CHECK("blur_pass_kernel<y>");
-      blur_pass_kernel<2><<<grid, 256, 0, st>>>(tmp, d_smooth, nx, ny, nz, h);
+      blur_pass_kernel<2><<<grid, 256, 0, st>>>(tmp, d_smooth, nx, ny, nz, h, tp);
       SNK_LAUNCH_CHECK("blur_pass_kernel<z>");
     } else {
-      blur_pass_kernel<0><<<grid, 256, 0, st>>>(d_in, tmp, nx, ny, nz, h);
+      blur_pass_kernel<0><<<grid, 256, 0, st>>>(d_in, tmp, nx, ny, nz, h, tp);
       SNK_LAUNCH_CHECK("blur_pass_kernel<x>");
-      blur_pass_kernel<1><<<grid, 256, 0, st>>>(tmp, d_smooth, nx, ny, nz, h);
+      blur_pass_kernel<1><<<grid, 256, 0, st>>>(tmp, d_smooth, nx, ny, nz, h, tp);
       SNK_LAUNCH_CHECK("blur_pass_kernel<y>");
     }
   }
-  if (d_gradmag) {
+  if (d_gradmag && vec8_ok(g, d_smooth, d_gradmag, nullptr)) {
+    const unsigned grid = (unsigned)ceil_div(nvox / 8, 256);
+    if (g->dim == 3) gradmag8_kernel<3><<<grid, 256, 0, st>>>(d_smooth, d_gradmag, nx, ny, nz);
+    else gradmag8_kernel<2><<<grid, 256, 0, st>>>(d_smooth, d_gradmag, nx, ny, nz);
+    SNK_LAUNCH_CHECK("gradmag8_kernel");
+  } else if (d_gradmag) {
     dim3 grid((unsigned)ceil_div(nx, kBX), (unsigned)ceil_div(ny, kBY),
               g->dim == 3 ? (unsigned)ceil_div(nz, kBZC) : 1u);
     if (g->dim == 3) gradmag_tiled_kernel<3><<<grid, kBThreads, 0, st>>>(d_smooth, d_gradmag, nx, ny, nz);

@@ -56,7 +56,11 @@ def _assert_cells_close(g, o, ctx=""):
 
 @pytest.mark.parametrize("dim,shape,sigma", [(3, (37, 45, 67), 1.0), (3, (2, 17, 9), 1.0),
                                              (3, (21, 33, 70), 2.0), (3, (12, 13, 14), 0.0),
-                                             (2, (1, 129, 257), 1.0), (3, (9, 5, 300), 0.5)])
+                                             (2, (1, 129, 257), 1.0), (3, (9, 5, 300), 0.5),
+                                             # x extent % 8 == 0: the vectorised passes
+                                             (3, (19, 23, 64), 1.0), (3, (10, 12, 136), 2.0),
+                                             (3, (7, 9, 8), 1.0), (3, (33, 17, 48), 0.5),
+                                             (2, (1, 100, 256), 1.0), (2, (1, 31, 8), 2.0)])
 def test_blur_gradmag_bitexact(gpu, dim, shape, sigma):
     torch, snk, _ = gpu
     rng = np.random.default_rng(hash(shape) % 2 ** 32)
@@ -72,6 +76,46 @@ def test_blur_gradmag_bitexact(gpu, dim, shape, sigma):
     B = oracle.blur(vol, dim, sigma)
     assert np.array_equal(sm.cpu().numpy(), B)
     assert np.array_equal(gm.cpu().numpy(), oracle.gradmag(B, dim))
+
+
+@pytest.mark.parametrize("dim,shape", [(3, (6, 10, 64)), (3, (5, 7, 67)), (2, (1, 20, 32))])
+def test_gradmag_extreme_bitexact(gpu, dim, shape):
+    """a3 at the largest gradients (0 / 65535 checkerboards, v up to 3 * 65535^2):
+    the float-estimated isqrt must still be exact."""
+    torch, snk, _ = gpu
+    z, y, x = np.indices(shape)
+    vol = (((x + y + z) % 2) * 65535).astype(np.uint16)
+    vol[:, :, ::3] = 65535 - vol[:, :, ::3]
+    n = (shape[2], shape[1], shape[0])
+    g = snk.make_grid(dim, n)
+    p = snk.make_params(10.0, sigma=0.0)
+    d_in = _t(torch, vol)
+    sm, gm = torch.empty_like(d_in), torch.empty_like(d_in)
+    ws = torch.empty(snk.snk_workspace_bytes(g, p, 16), dtype=torch.uint8, device="cuda")
+    snk.snk_preprocess(g, p, d_in, sm, gm, ws)
+    torch.cuda.synchronize()
+    assert np.array_equal(sm.cpu().numpy(), vol)
+    assert np.array_equal(gm.cpu().numpy(), oracle.gradmag(vol, dim))
+
+
+@pytest.mark.parametrize("dim,shape,w", [(3, (30, 26, 64), 3), (3, (21, 19, 40), 0), (3, (40, 36, 32), 8),
+                                         (3, (25, 22, 45), 5), (2, (1, 90, 128), 6), (2, (1, 70, 75), 4)])
+def test_seeds_maxima_plateaus_bitexact(gpu, dim, shape, w):
+    """a4 MAXIMA on quantised random volumes (many equal values: the tie rule
+    decides), vectorised (x % 8 == 0) and fallback paths, w in {0, .., 8}."""
+    torch, snk, _ = gpu
+    rng = np.random.default_rng(sum(shape) + w)
+    vol = (rng.integers(0, 12, size=shape) * 5000).astype(np.uint16)
+    n = (shape[2], shape[1], shape[0])
+    g = snk.make_grid(dim, n)
+    p = snk.make_params(10.0, seed_mode=snk.SEED_MAXIMA, seed_window=w, seed_threshold=20000)
+    cap = int(np.prod(shape)) + 16
+    seeds = torch.empty((cap, 3), dtype=torch.float32, device="cuda")
+    ws = torch.empty(max(snk.snk_workspace_bytes(g, p, 16), 16), dtype=torch.uint8, device="cuda")
+    cnt, _ = snk.snk_seeds(g, p, _t(torch, vol), seeds, cap, ws)
+    exp = oracle.seeds_maxima(vol, dim, w, 20000)
+    assert cnt == len(exp) > 0
+    assert np.array_equal(seeds[:cnt].cpu().numpy(), exp)
 
 
 @pytest.mark.parametrize("n,spacing", [((40, 36, 20), (1.0, 1.0, 2.0)), ((23, 17, 11), (3.0, 1.5, 1.0)),
