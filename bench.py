@@ -151,6 +151,8 @@ def run_ours(args):
     import torch
     rank, local_rank, world = dist_env()
     cfg = synth.CONFIGS[args.config]
+    if args.n_samples:   # sweeps (e.g. the C5 N-sweep); the headline uses the config's N
+        cfg = cfg.with_(n_samples=args.n_samples)
     if world > 1:
         from paper_1804_06304_b200 import dist as D
         return D.bench_rank(args, cfg)
@@ -321,6 +323,7 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="C4")
+    ap.add_argument("--n-samples", type=int, default=0, help="override the config's N (sweeps only)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -162,29 +162,100 @@ __device__ __forceinline__ void philox_block(const EvoParams& P, const CellIt& C
   x[0] = c0; x[1] = c1; x[2] = c2; x[3] = c3;
 }
 
-// Words -> the sample's direction (Archimedes, G10) and distance (P:194-195,
-// S:224).  3D: (w0, w1, w2) = (u0, u1, u2); 2D: (w1, w2) = (u1, u2).
+// Words -> the sample's direction (Archimedes, G10) and the radial variate:
+// the part of a draw that does not depend on the contour state, so it can be
+// computed ahead (evolve_brick_kernel draws iteration n+1 while the update of
+// iteration n runs).  3D: (w0, w1, w2) = (u0, u1, u2), L = lg2(u2);
+// 2D: (w1, w2) = (u1, u2), L = sqrt(u2).
+struct Dir {
+  float ox, oy, oz, L;
+};
+
 template <int D>
-__device__ __forceinline__ Draw draw_words(const CellIt& C, uint32_t w0, uint32_t w1, uint32_t w2) {
+__device__ __forceinline__ Dir dir_words(uint32_t w0, uint32_t w1, uint32_t w2) {
   const float u1 = u01(w1), u2 = u01(w2);
   float sn, cs;
   __sincosf(__fmul_rn(6.2831853071795865f, u1), &sn, &cs);
-  Draw d;
+  Dir d;
   if (D == 3) {
     const float u0 = u01(w0);
     d.oz = __fmaf_rn(-2.0f, u0, 1.0f);
     const float st = sqrt_approx(__fmaf_rn(-d.oz, d.oz, 1.0f));   // sqrt(1 - z^2) = 2 sqrt(u0 (1 - u0))
     d.ox = __fmul_rn(st, cs);
     d.oy = __fmul_rn(st, sn);
-    d.t = ex2_approx(__fmaf_rn(lg2_approx(u2), 0.333333343f, C.lg2_rho_s));   // rho_s cbrt(u2)
+    d.L = lg2_approx(u2);
   } else {
     (void)w0;
     d.ox = cs;
     d.oy = sn;
     d.oz = 0.0f;
-    d.t = __fmul_rn(C.rho_s, sqrt_approx(u2));
+    d.L = sqrt_approx(u2);
   }
   return d;
+}
+
+// The distance: 3D t = rho_s cbrt(u2), 2D t = rho_s sqrt(u2).
+template <int D>
+__device__ __forceinline__ Draw finish_draw(const CellIt& C, const Dir& d) {
+  Draw r;
+  r.ox = d.ox;
+  r.oy = d.oy;
+  r.oz = d.oz;
+  r.t = D == 3 ? ex2_approx(__fmaf_rn(d.L, 0.333333343f, C.lg2_rho_s)) : __fmul_rn(C.rho_s, d.L);
+  return r;
+}
+
+template <int D>
+__device__ __forceinline__ Draw draw_words(const CellIt& C, uint32_t w0, uint32_t w1, uint32_t w2) {
+  return finish_draw<D>(C, dir_words<D>(w0, w1, w2));
+}
+
+// The directions of the CH samples j0 .. j0 + CH - 1 (CH a power of two, j0 %
+// CH == 0) of iteration n, keyed through C.p0/p1/p3 only.
+template <int D, int CH>
+__device__ __forceinline__ void draw_dirs(const EvoParams& P, const CellIt& C, uint32_t j0, Dir* d) {
+  constexpr int G = D == 3 ? 4 : 2;
+  if constexpr (CH >= G) {
+#pragma unroll
+    for (int g = 0; g < CH; g += G) {
+      uint32_t a[4];
+      if (D == 3) {
+        uint32_t b[4], c[4];
+        const uint32_t b0 = ((j0 + g) >> 2) * 3u;
+        philox_block(P, C, b0, a);
+        philox_block(P, C, b0 + 1, b);
+        philox_block(P, C, b0 + 2, c);
+        d[g + 0] = dir_words<3>(a[0], a[1], a[2]);
+        d[g + 1] = dir_words<3>(a[3], b[0], b[1]);
+        d[g + 2] = dir_words<3>(b[2], b[3], c[0]);
+        d[g + 3] = dir_words<3>(c[1], c[2], c[3]);
+      } else {
+        philox_block(P, C, (j0 + g) >> 1, a);
+        d[g + 0] = dir_words<2>(0, a[0], a[1]);
+        d[g + 1] = dir_words<2>(0, a[2], a[3]);
+      }
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < CH; ++k) {
+      const uint32_t j = j0 + k;
+      uint32_t x[4];
+      if (D == 3) {
+        const uint32_t w = 3u * j, o = w & 3u;
+        philox_block(P, C, w >> 2, x);
+        if (o <= 1) {
+          d[k] = o == 0 ? dir_words<3>(x[0], x[1], x[2]) : dir_words<3>(x[1], x[2], x[3]);
+        } else {
+          uint32_t y[4];
+          philox_block(P, C, (w >> 2) + 1, y);
+          d[k] = o == 2 ? dir_words<3>(x[2], x[3], y[0]) : dir_words<3>(x[3], y[0], y[1]);
+        }
+      } else {
+        philox_block(P, C, j >> 1, x);
+        d[k] = (j & 1u) ? dir_words<2>(0, x[2], x[3]) : dir_words<2>(0, x[0], x[1]);
+      }
+    }
+  }
 }
 
 // Sample j alone (G11 word layout: 3D words 3j..3j+2, 2D words 2j, 2j+1).
@@ -338,6 +409,26 @@ __device__ __forceinline__ Acc chunk_sum(const EvoParams& P, const CellIt& C, ui
     const Acc r = chunk_sum<D, MODE, S, CH / 2>(P, C, j0 + CH / 2, brick, halo);
     return acc_add(l, r);
   }
+}
+
+// Pairwise sum over CH samples with precomputed directions: the same perfect
+// binary tree as chunk_sum (leaves in sample order).
+template <int N>
+__device__ __forceinline__ Acc tree_sum(const Acc* l) {
+  if constexpr (N == 1) {
+    return l[0];
+  } else {
+    return acc_add(tree_sum<N / 2>(l), tree_sum<N / 2>(l + N / 2));
+  }
+}
+
+template <int D, int MODE, int S, int CH>
+__device__ __forceinline__ Acc chunk_sum_dirs(const EvoParams& P, const CellIt& C, const Dir* d,
+                                              const uint16_t* brick, uint32_t& halo) {
+  Acc l[CH];
+#pragma unroll
+  for (int k = 0; k < CH; ++k) l[k] = sample_leaf<D, MODE, S>(P, C, finish_draw<D>(C, d[k]), brick, halo);
+  return tree_sum<CH>(l);
 }
 
 // Pairwise sum over CH << L consecutive samples: 2^L chunks combined by a
@@ -646,12 +737,21 @@ __device__ __forceinline__ void load_brick(uint16_t* brick, const EvoParams& P, 
 #ifndef SNK_BRICK_MINB8
 #define SNK_BRICK_MINB8 2
 #endif
+// PIPE (one chunk per thread, L == 0): the state-independent part of the next
+// iteration's draws (Philox words -> direction, radial variate) is computed
+// while warp 0 alone takes the update step, which it then broadcasts; the
+// arithmetic is unchanged, only its placement.
+#ifndef SNK_BRICK_PIPE
+#define SNK_BRICK_PIPE 1
+#endif
 template <int D, int W, int S, bool SLAB, int CH, int L>
 __global__ void __launch_bounds__(32 * W, W == 4 ? 3 : SNK_BRICK_MINB8) evolve_brick_kernel(const __grid_constant__ EvoParams P) {
   constexpr int B = CH << L;
+  constexpr bool PIPE = SNK_BRICK_PIPE && L == 0;
   constexpr int EXT[3] = {brick_sx(S), S, S};       // brick extent per axis
   extern __shared__ __align__(16) uint16_t brick[];
   __shared__ __align__(16) float xch[2][5][W];      // [parity][component][warp]
+  __shared__ float bc[4];                           // PIPE: (cx, cy, cz, R) after warp 0's update
   const int lane = threadIdx.x & 31, wsub = threadIdx.x >> 5;
   const int64_t cell = blockIdx.x;
   CellState s;
@@ -668,6 +768,8 @@ __global__ void __launch_bounds__(32 * W, W == 4 ? 3 : SNK_BRICK_MINB8) evolve_b
   // z range the brick may cover: the slab buffer
   const int zlo = SLAB ? P.z_lo : 0, zhi = SLAB ? P.z_lo + P.nz_buf - 1 : P.nz - 1;
   const uint32_t j0 = (uint32_t)((wsub * 32 + lane) * B);
+  Dir dir[PIPE ? CH : 1];
+  if constexpr (PIPE) draw_dirs<D, CH>(P, cell_iter(P, s, 1), j0, dir);
   for (int it = 1; it <= P.T + 1; ++it) {
     CellIt C = cell_iter(P, s, it);
     // bounding box of the sampled ball, with a margin for the fp32 rounding of t and k
@@ -723,24 +825,57 @@ __global__ void __launch_bounds__(32 * W, W == 4 ? 3 : SNK_BRICK_MINB8) evolve_b
     }
     Acc part;
     C.boff = boff;
-    if (mode == 0) {
-      part = lane_sum<D, G_BRICK_FAST, S, CH, L>(P, C, j0, brick, halo);
-    } else if (mode == 1) {
-      part = lane_sum<D, G_BRICK_CLAMP, S, CH, L>(P, C, j0, brick, halo);
+    if constexpr (PIPE) {
+      if (mode == 0) {
+        part = chunk_sum_dirs<D, G_BRICK_FAST, S, CH>(P, C, dir, brick, halo);
+      } else if (mode == 1) {
+        part = chunk_sum_dirs<D, G_BRICK_CLAMP, S, CH>(P, C, dir, brick, halo);
+      } else {
+        part = chunk_sum_dirs<D, SLAB ? G_GLOBAL_SLAB : G_GLOBAL, S, CH>(P, C, dir, brick, halo);
+        if (threadIdx.x == 0) atomicAdd(&g_evolve_stats[1], 1ull);
+      }
     } else {
-      part = lane_sum<D, SLAB ? G_GLOBAL_SLAB : G_GLOBAL, S, CH, L>(P, C, j0, brick, halo);
-      if (threadIdx.x == 0) atomicAdd(&g_evolve_stats[1], 1ull);
+      if (mode == 0) {
+        part = lane_sum<D, G_BRICK_FAST, S, CH, L>(P, C, j0, brick, halo);
+      } else if (mode == 1) {
+        part = lane_sum<D, G_BRICK_CLAMP, S, CH, L>(P, C, j0, brick, halo);
+      } else {
+        part = lane_sum<D, SLAB ? G_GLOBAL_SLAB : G_GLOBAL, S, CH, L>(P, C, j0, brick, halo);
+        if (threadIdx.x == 0) atomicAdd(&g_evolve_stats[1], 1ull);
+      }
     }
     float* xo = &xch[it & 1][0][0];
     warp_reduce_scatter(part, xo + wsub, lane, W);
     __syncthreads();   // also: every brick read of this iteration is done
-    Acc sum;
-    sum.a0 = comp_tree<W>(xo + 0 * W);
-    sum.cx = comp_tree<W>(xo + 1 * W);
-    sum.cy = comp_tree<W>(xo + 2 * W);
-    sum.cz = comp_tree<W>(xo + 3 * W);
-    sum.aR = comp_tree<W>(xo + 4 * W);
-    if (cell_update<D>(P, s, C, sum, it)) break;
+    if constexpr (PIPE) {
+      const bool done = it == P.T + 1;
+      if (wsub == 0) {
+        Acc sum;
+        sum.a0 = comp_tree<W>(xo + 0 * W);
+        sum.cx = comp_tree<W>(xo + 1 * W);
+        sum.cy = comp_tree<W>(xo + 2 * W);
+        sum.cz = comp_tree<W>(xo + 3 * W);
+        sum.aR = comp_tree<W>(xo + 4 * W);
+        cell_update<D>(P, s, C, sum, it);
+        if (lane == 0) { bc[0] = s.cx; bc[1] = s.cy; bc[2] = s.cz; bc[3] = s.R; }
+      }
+      if (done) break;
+      CellIt Cn;   // the next iteration's Philox key words
+      Cn.p0 = s.q0 ^ (uint32_t)(it + 1);
+      Cn.p1 = s.q1;
+      Cn.p3 = s.q3;
+      draw_dirs<D, CH>(P, Cn, j0, dir);
+      __syncthreads();
+      if (wsub != 0) { s.cx = bc[0]; s.cy = bc[1]; s.cz = bc[2]; s.R = bc[3]; }
+    } else {
+      Acc sum;
+      sum.a0 = comp_tree<W>(xo + 0 * W);
+      sum.cx = comp_tree<W>(xo + 1 * W);
+      sum.cy = comp_tree<W>(xo + 2 * W);
+      sum.cz = comp_tree<W>(xo + 3 * W);
+      sum.aR = comp_tree<W>(xo + 4 * W);
+      if (cell_update<D>(P, s, C, sum, it)) break;
+    }
   }
   if (SLAB && __syncthreads_or(halo != 0)) s.flags |= SNK_F_HALO;
   if (threadIdx.x == 0) cell_finish(P, s, cell);
