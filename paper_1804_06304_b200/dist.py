@@ -62,9 +62,17 @@ def plan_slabs(n, world: int, rank: int, params) -> SlabPlan:
     return SlabPlan(n=n, world=world, rank=rank, own=(z0, z1), halo=H, blur=h, buf=(lo, hi))
 
 
+def _staged(group) -> bool:
+    """gloo moves host memory only: CUDA tensors are staged through the host
+    (used when several ranks share one GPU, where NCCL refuses; GPU tests)."""
+    return tdist.get_backend(group) == "gloo"
+
+
 def exchange_halo(plan: SlabPlan, own_raw: torch.Tensor, group=None) -> torch.Tensor:
     """N1: assemble raw planes [buf) from this rank's own planes and the other
     ranks' (point-to-point; each rank sends exactly what the others need)."""
+    if own_raw.is_cuda and _staged(group):
+        return exchange_halo(plan, own_raw.cpu(), group).to(own_raw.device)
     nz = plan.n[2]
     lo, hi = plan.buf
     z0, z1 = plan.own
@@ -112,6 +120,8 @@ def plan_like(plan: SlabPlan, rank: int) -> SlabPlan:
 
 def allgather_counts(count: int, device, group=None) -> list:
     """N2: every rank's count."""
+    if _staged(group):
+        device = torch.device("cpu")
     t = torch.tensor([count], dtype=torch.int64, device=device)
     outs = [torch.empty_like(t) for _ in range(tdist.get_world_size(group))]
     tdist.all_gather(outs, t, group=group)
@@ -120,6 +130,9 @@ def allgather_counts(count: int, device, group=None) -> list:
 
 def allgather_records(rec: torch.Tensor, count: int, device, group=None, rec_bytes: int = 48):
     """N3: concatenate every rank's `count` records (uint8, rec_bytes each) in rank order."""
+    if _staged(group) and torch.device(device).type == "cuda":
+        allrec, tot, counts = allgather_records(rec[:count * rec_bytes].cpu(), count, "cpu", group, rec_bytes)
+        return allrec.to(device), tot, counts
     counts = allgather_counts(count, device, group)
     m = max(max(counts), 1)
     pad = torch.zeros(m * rec_bytes, dtype=torch.uint8, device=device)
@@ -220,8 +233,14 @@ def bench_rank(args, cfg):
 
     rank, local_rank, world = (int(os.environ.get(k, d)) for k, d in
                                (("RANK", "0"), ("LOCAL_RANK", "0"), ("WORLD_SIZE", "1")))
+    local_rank %= max(torch.cuda.device_count(), 1)   # ranks > GPUs: share (gloo tests only)
     torch.cuda.set_device(local_rank)
-    tdist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    # SNK_DIST_BACKEND=gloo: several ranks on one GPU (host-staged exchanges; tests only)
+    backend = os.environ.get("SNK_DIST_BACKEND", "nccl")
+    if backend == "nccl":
+        tdist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    else:
+        tdist.init_process_group(backend)
     assert tuple(cfg.iso_n) == tuple(cfg.n), "the slab driver takes isotropic volumes"
     p = pipeline.params_for(cfg, image_term=snk.IMAGE_INTENSITY)
     plan = plan_slabs(cfg.n, world, rank, p)
@@ -250,7 +269,8 @@ def bench_rank(args, cfg):
         e.record()
         torch.cuda.synchronize()
         tdist.barrier()
-    ms = torch.tensor([s.elapsed_time(e)], dtype=torch.float64, device="cuda")
+    ms = torch.tensor([s.elapsed_time(e)], dtype=torch.float64,
+                      device="cpu" if backend == "gloo" else "cuda")
     tdist.all_reduce(ms, op=tdist.ReduceOp.MAX)
     total_ms = float(ms.item())
     launches = snk.snk_launch_count() - l0

@@ -18,3 +18,13 @@ def ora():
     import oracle
     oracle.lib()
     return oracle
+
+
+@pytest.fixture(scope="module")
+def gpu():
+    """(torch, snk, pipeline) on a CUDA device; libsnk must load (no fallback)."""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_1804_06304_b200 import pipeline, snk
+    return torch, snk, pipeline

@@ -1,0 +1,86 @@
+"""The z-slab driver (paper_1804_06304_b200.dist) with the real kernels: world
+sizes 2 and 3 as processes sharing one GPU (gloo, host-staged exchanges — the
+round's GPU box has one device; NCCL runs the same code on 8).  Seeds, cells,
+detections and the label map must be bit-identical to the single-GPU pipeline
+(DESIGN.md §7)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+import synth
+
+pytestmark = pytest.mark.gpu
+
+CFG = synth.Config(name="slab", dim=3, n=(48, 40, 150), count=(2, 2, 6), pitch=(24.0, 20.0, 25.0),
+                   jitter=2.0, rbar=(5.0, 6.5), bg_wavelength=64.0, r0=7.0, n_samples=128,
+                   max_iters=40, seed_window=3, gen_seed=77, philox_seed=991)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, q):
+    import torch
+    import torch.distributed as tdist
+    from paper_1804_06304_b200 import dist as D, pipeline, snk
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    tdist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        p = pipeline.params_for(CFG, image_term=snk.IMAGE_INTENSITY)
+        plan = D.plan_slabs(CFG.n, world, rank, p)
+        raw = synth.generate(CFG)
+        own = torch.from_numpy(raw[plan.own[0]:plan.own[1]].copy()).cuda()
+        be = D.CudaBackend(plan, p, max_cells=4096)
+        r = D.SlabRun(plan, be, torch.device("cuda", 0)).step(own)
+        torch.cuda.synchronize()
+        ns, nd = r["n_seeds"], r["n_dets"]
+        q.put((rank, {"seeds": r["seeds"][:ns].cpu().numpy(), "cells": r["cells"][:ns * 48].cpu().numpy(),
+                      "dets": r["dets"][:nd * 48].cpu().numpy(), "labels": r["labels"].cpu().numpy(),
+                      "id_base": r["id_base"], "n_total": r["n_total"]}))
+    except Exception as e:  # surface the failure in the parent
+        q.put((rank, repr(e)))
+        raise
+    finally:
+        tdist.destroy_process_group()
+
+
+@pytest.fixture(scope="module")
+def single(gpu):
+    torch, snk, pipeline = gpu
+    p = pipeline.params_for(CFG, image_term=snk.IMAGE_INTENSITY)
+    P = pipeline.Pipeline(3, CFG.n, p, gradmag=False)
+    P.upload(synth.generate(CFG))
+    res = P.step()
+    torch.cuda.synchronize()
+    return {"seeds": P.seeds[:res.n_seeds].cpu().numpy(), "cells": P.cells[:res.n_seeds * 48].cpu().numpy(),
+            "dets": P.dets[:res.n_dets * 48].cpu().numpy(), "labels": P.labels.cpu().numpy()}
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_slabs_match_single_gpu(single, world):
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    out = dict(q.get(timeout=600) for _ in range(world))
+    for pr in procs:
+        pr.join(timeout=120)
+    for r in range(world):
+        assert not isinstance(out[r], str), out[r]
+    assert out[0]["n_total"] == len(single["seeds"])
+    assert np.array_equal(np.concatenate([out[r]["seeds"] for r in range(world)]), single["seeds"])
+    assert np.array_equal(np.concatenate([out[r]["cells"] for r in range(world)]), single["cells"])
+    for r in range(world):
+        assert np.array_equal(out[r]["dets"], single["dets"])
+    assert np.array_equal(np.concatenate([out[r]["labels"] for r in range(world)]), single["labels"])

@@ -17,15 +17,6 @@ pytestmark = pytest.mark.gpu
 TOL_RC = 1e-3
 
 
-@pytest.fixture(scope="module")
-def gpu():
-    import torch
-    if not torch.cuda.is_available():
-        pytest.skip("no CUDA device")
-    from paper_1804_06304_b200 import pipeline, snk
-    return torch, snk, pipeline
-
-
 def _t(torch, a):
     return torch.from_numpy(np.ascontiguousarray(a)).cuda()
 
