@@ -153,14 +153,19 @@ class SlabRun:
     def __init__(self, plan: SlabPlan, backend, device, group=None):
         self.plan, self.be, self.device, self.group = plan, backend, device, group
 
-    def step(self, own_raw: torch.Tensor) -> dict:
+    def step(self, own_raw: torch.Tensor, ev=None) -> dict:
+        """ev: optional pair of CUDA events recorded around a5/a6 (bench)."""
         pl = self.plan
         local = exchange_halo(pl, own_raw, self.group)                 # N1
         smooth = self.be.preprocess(pl, local)                          # a2/a3
         seeds, ns = self.be.seeds(pl, smooth)                           # a4
         counts = allgather_counts(ns, self.device, self.group)          # N2
         id_base = sum(counts[:pl.rank])
+        if ev is not None:
+            ev[0].record()
         cells = self.be.evolve(pl, smooth, seeds, ns, id_base)          # a5/a6
+        if ev is not None:
+            ev[1].record()
         cand, nc = self.be.compact(cells, ns)                           # a7: E0
         allc, ntot, _ = allgather_records(cand, nc, self.device, self.group)   # N3
         dets, nd = self.be.cull(pl, allc, ntot)                         # a7: overlap
@@ -258,27 +263,52 @@ def bench_rank(args, cfg):
     torch.cuda.synchronize()
     tdist.barrier()
     l0 = snk.snk_launch_count()
-    from bench import ClockSampler  # noqa: E402
+    from bench import ClockSampler, OPS_PER_SAMPLE, SMS, LANES_PER_SM  # noqa: E402
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(args.steps)]
     with ClockSampler(local_rank) as clk:
         torch.cuda.synchronize()
         tdist.barrier()
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s.record()
-        for _ in range(args.steps):
-            r = run.step(own)
+        for k in range(args.steps):
+            r = run.step(own, evs[k])
         e.record()
         torch.cuda.synchronize()
         tdist.barrier()
-    ms = torch.tensor([s.elapsed_time(e)], dtype=torch.float64,
-                      device="cpu" if backend == "gloo" else "cuda")
+    red_dev = "cpu" if backend == "gloo" else "cuda"
+    evolve_ms = statistics.mean(a.elapsed_time(b) for a, b in evs)
+    ms = torch.tensor([s.elapsed_time(e), evolve_ms], dtype=torch.float64, device=red_dev)
     tdist.all_reduce(ms, op=tdist.ReduceOp.MAX)
-    total_ms = float(ms.item())
+    total_ms, evolve_ms_max = float(ms[0].item()), float(ms[1].item())
     launches = snk.snk_launch_count() - l0
     n_total = r["n_total"]
     samples = n_total * (cfg.max_iters + 1) * cfg.n_samples
+    # this rank's evolve kernel against the per-GPU ALU peak; reported as the mean over ranks
+    my_samples = r["n_seeds"] * (cfg.max_iters + 1) * cfg.n_samples
+    clocks = clk.summary()
+    f_clk = (clocks["sm_max_mhz"] or 1965.0) * 1e6
+    peak = SMS * LANES_PER_SM * f_clk / 1e9
+    ach = torch.tensor([my_samples * OPS_PER_SAMPLE / (evolve_ms / 1e3) / 1e9], dtype=torch.float64,
+                       device=red_dev)
+    tdist.all_reduce(ach, op=tdist.ReduceOp.SUM)
+    achieved = float(ach.item()) / world
+    # end to end: each step copies this rank's raw planes in (pinned host -> device)
+    # and its labels + the detections out, wall clock, max over ranks
+    h_labels = torch.empty(tuple(be.labels.shape), dtype=torch.int32, pin_memory=True)
+    h_dets = torch.empty(be.dets.numel(), dtype=torch.uint8, pin_memory=True)
+    tdist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        own.copy_(h_raw, non_blocking=True)
+        r = run.step(own)
+        h_labels.copy_(r["labels"], non_blocking=True)
+        h_dets[:r["n_dets"] * 48].copy_(r["dets"][:r["n_dets"] * 48], non_blocking=True)
+        torch.cuda.synchronize()
+    wall = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=red_dev)
+    tdist.all_reduce(wall, op=tdist.ReduceOp.MAX)
+    e2e_s = float(wall.item())
     out = None
     if rank == 0:
-        clocks = clk.summary()
         out = {"metric": "contour ray-samples/sec and cells segmented/sec at 1/2/4/8 B200; HBM/L2 GB/s",
                "value": samples * args.steps / (total_ms / 1e3), "unit": "ray-samples/s",
                "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -287,9 +317,18 @@ def bench_rank(args, cfg):
                "config": {"workload": f"{cfg.name} z-slabs", "volume_iso": list(cfg.n), "cells": n_total,
                           "detections": r["n_dets"], "n_samples": cfg.n_samples, "iters": cfg.max_iters,
                           "parallelism": f"z-slab x{world}", "halo_planes": plan.halo,
-                          "l2": "inputs larger than L2"},
+                          "l2": "inputs larger than L2", "backend": backend},
                "cells_per_s": n_total * args.steps / (total_ms / 1e3), "gpu_launches": int(launches),
-               "clocks": clocks, "roofline": None, "cpu_baseline": None, "e2e": None}
+               "phase_ms": {"evolve_max_over_ranks": evolve_ms_max},
+               "clocks": clocks,
+               "roofline": {"bound": "alu", "achieved": round(achieved, 1), "peak": round(peak, 1),
+                            "unit": "Glane-op/s", "frac": round(achieved / peak, 4), "traffic": None,
+                            "kernel": "evolve_brick_kernel (slab)", "ops_per_sample": OPS_PER_SAMPLE,
+                            "per": "GPU, mean over ranks"},
+               "cpu_baseline": None,
+               "e2e": {"value": samples * args.steps / e2e_s, "unit": "ray-samples/s",
+                       "h2d_bytes_per_step": int(nown * 2 * world),
+                       "d2h_bytes_per_step": int(cfg.n[0] * cfg.n[1] * cfg.n[2] * 4 + r["n_dets"] * 48 * world)}}
     tdist.barrier()
     tdist.destroy_process_group()
     return out
