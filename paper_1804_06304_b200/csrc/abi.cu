@@ -69,6 +69,10 @@ static int32_t validate_params(const snk_params* p, int dim) {
   if (p->image_term != SNK_IMAGE_INTENSITY && p->image_term != SNK_IMAGE_GRADMAG)
     return fail(SNK_CONFIG, "bad image_term");
   if (p->kernel_variant > 2) return fail(SNK_CONFIG, "kernel_variant must be 0, 1 or 2");
+  if (p->estimator != SNK_EST_MC && p->estimator != SNK_EST_GRID)
+    return fail(SNK_CONFIG, "estimator must be SNK_EST_MC or SNK_EST_GRID");
+  if (p->estimator == SNK_EST_GRID && p->kernel_variant == 1)
+    return fail(SNK_CONFIG, "the grid estimator runs in the brick kernel only (kernel_variant 0 or 2)");
   (void)dim;
   return SNK_OK;
 }
@@ -335,5 +339,5 @@ int32_t snk_run(int32_t dim, const int64_t n_raw[3], const double spacing[3],
 }  // extern "C"
 
 static_assert(sizeof(snk_grid) == 64, "snk_grid layout is part of the ABI");
-static_assert(sizeof(snk_params) == 128, "snk_params layout is part of the ABI");
+static_assert(sizeof(snk_params) == 136, "snk_params layout is part of the ABI");
 static_assert(sizeof(snk_cell) == 48, "snk_cell layout is part of the ABI");

@@ -589,12 +589,14 @@ __device__ __forceinline__ CellIt cell_iter(const EvoParams& P, const CellState&
 }
 
 // Energy, gradient and the clipped descent step; returns true after E_final.
-template <int D>
+// GRID: the sums are Eq. 5's voxel sums (unit voxel volume), scaled by iscale
+// alone; MC: each sample carries V/N = (4/3 pi | pi) rho_s^d / N.
+template <int D, bool GRID = false>
 __device__ __forceinline__ bool cell_update(const EvoParams& P, CellState& s, const CellIt& C,
                                             const Acc& sum, int it) {
   const float rs = C.rho_s;
   const float vol = D == 3 ? __fmul_rn(__fmul_rn(rs, rs), rs) : __fmul_rn(rs, rs);
-  const float scale = __fmul_rn(P.vscale, vol);
+  const float scale = GRID ? P.vscale : __fmul_rn(P.vscale, vol);
   const float A0 = __fmul_rn(sum.a0, scale);
   const float twoR = __fmul_rn(2.0f, s.R);
   const float gden = D == 3 ? __fmul_rn(__fmul_rn(twoR, twoR), twoR) : __fmul_rn(twoR, twoR);
@@ -744,37 +746,41 @@ __device__ __forceinline__ void load_brick(uint16_t* brick, const EvoParams& P, 
 #ifndef SNK_BRICK_PIPE
 #define SNK_BRICK_PIPE 1
 #endif
-template <int D, int W, int S, bool SLAB, int CH, int L>
-__global__ void __launch_bounds__(32 * W, W == 4 ? 3 : SNK_BRICK_MINB8) evolve_brick_kernel(const __grid_constant__ EvoParams P) {
-  constexpr int B = CH << L;
-  constexpr bool PIPE = SNK_BRICK_PIPE && L == 0;
-  constexpr int EXT[3] = {brick_sx(S), S, S};       // brick extent per axis
-  extern __shared__ __align__(16) uint16_t brick[];
-  __shared__ __align__(16) float xch[2][5][W];      // [parity][component][warp]
-  __shared__ float bc[4];                           // PIPE: (cx, cy, cz, R) after warp 0's update
-  const int lane = threadIdx.x & 31, wsub = threadIdx.x >> 5;
-  const int64_t cell = blockIdx.x;
-  CellState s;
-  cell_begin(P, cell, D, s);
-  uint32_t halo = 0;
-  int b[3] = {-(1 << 28), -(1 << 28), -(1 << 28)};   // brick origin (global voxels); none yet
-  // fast test: the ball's tap box [floor(c - ext), floor(c + ext) + 1] lies in
-  // the brick iff c - ext >= in_lo and c + ext < in_hi per axis (exact for the
-  // integer bounds); only set for a brick inside the volume, so containment
-  // also means no clamping is needed
-  float in_lo[3] = {INFINITY, INFINITY, INFINITY}, in_hi[3] = {-INFINITY, -INFINITY, -INFINITY};
-  uint32_t boff = 0;
-  const int n[3] = {P.nx, P.ny, P.nz};
-  // z range the brick may cover: the slab buffer
-  const int zlo = SLAB ? P.z_lo : 0, zhi = SLAB ? P.z_lo + P.nz_buf - 1 : P.nz - 1;
-  const uint32_t j0 = (uint32_t)((wsub * 32 + lane) * B);
-  Dir dir[PIPE ? CH : 1];
-  if constexpr (PIPE) draw_dirs<D, CH>(P, cell_iter(P, s, 1), j0, dir);
-  for (int it = 1; it <= P.T + 1; ++it) {
-    CellIt C = cell_iter(P, s, it);
+// Brick bookkeeping shared by the MC and grid brick kernels: the brick origin,
+// the float bounds of the fast containment test and the index offset.
+template <int D, int S, bool SLAB>
+struct BrickCtl {
+  int b[3];            // brick origin (global voxels)
+  float in_lo[3], in_hi[3];
+  uint32_t boff;
+  int zlo, zhi;        // z range the brick may cover: the slab buffer
+
+  __device__ __forceinline__ void init(const EvoParams& P) {
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      b[a] = -(1 << 28);   // none yet
+      in_lo[a] = INFINITY;
+      in_hi[a] = -INFINITY;
+    }
+    boff = 0;
+    zlo = SLAB ? P.z_lo : 0;
+    zhi = SLAB ? P.z_lo + P.nz_buf - 1 : P.nz - 1;
+  }
+
+  // Make the brick hold the tap box of the ball of radius rho_s around c (the
+  // d-linear taps [floor(c - ext), floor(c + ext) + 1], a superset of the grid
+  // voxels |k - c| < rho_s), re-loading it if needed.  Returns 0: inside the
+  // brick and the volume (no clamps), 1: inside the brick with clamps, 2: the
+  // ball does not fit (global gathers).  Called by all threads (uniform).
+  //
+  // Fast test: the tap box lies in the brick iff c - ext >= in_lo and c + ext <
+  // in_hi per axis (exact for the integer bounds); only set for a brick inside
+  // the volume, so containment also means no clamping is needed.
+  __device__ __forceinline__ int prepare(uint16_t* brick, const EvoParams& P, const float c[3],
+                                         float rho_s) {
+    constexpr int EXT[3] = {brick_sx(S), S, S};   // brick extent per axis
     // bounding box of the sampled ball, with a margin for the fp32 rounding of t and k
-    const float ext = __fmaf_rn(C.rho_s, 1.0001f, 0.01f);
-    const float c[3] = {s.cx, s.cy, s.cz};
+    const float ext = __fmaf_rn(rho_s, 1.0001f, 0.01f);
     float vlo[3], vhi[3];
     bool fast = true;
 #pragma unroll
@@ -783,48 +789,71 @@ __global__ void __launch_bounds__(32 * W, W == 4 ? 3 : SNK_BRICK_MINB8) evolve_b
       vhi[a] = __fadd_rn(c[a], ext);
       fast &= vlo[a] >= in_lo[a] && vhi[a] < in_hi[a];
     }
-    int mode = 0;   // 0 brick, no clamp; 1 brick with clamp; 2 global gathers
-    if (!fast) {
-      bool interior = true, fits = true, inside = true;
-      int lo[3], hi[3];
+    if (fast) return 0;
+    const int n[3] = {P.nx, P.ny, P.nz};
+    bool interior = true, fits = true, inside = true;
+    int lo[3], hi[3];
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+      lo[a] = (int)floorf(vlo[a]);
+      hi[a] = (int)floorf(vhi[a]) + 1;
+      interior &= lo[a] >= 0 && hi[a] <= n[a] - 1;
+      lo[a] = max(lo[a], 0);
+      hi[a] = min(hi[a], n[a] - 1);
+      fits &= hi[a] - lo[a] + 1 <= (a == 0 ? EXT[0] - 1 : S);
+      inside &= lo[a] >= b[a] && hi[a] <= b[a] + EXT[a] - 1;
+    }
+    if (D == 3 && SLAB) fits &= lo[2] >= zlo && hi[2] <= zhi;
+    if (!inside && fits) {
+      // re-centre: the ball's box in the middle of the brick, clipped to the
+      // volume (z: the slab buffer); the x origin is even (4-byte copies)
 #pragma unroll
       for (int a = 0; a < D; ++a) {
-        lo[a] = (int)floorf(vlo[a]);
-        hi[a] = (int)floorf(vhi[a]) + 1;
-        interior &= lo[a] >= 0 && hi[a] <= n[a] - 1;
-        lo[a] = max(lo[a], 0);
-        hi[a] = min(hi[a], n[a] - 1);
-        fits &= hi[a] - lo[a] + 1 <= (a == 0 ? EXT[0] - 1 : S);
-        inside &= lo[a] >= b[a] && hi[a] <= b[a] + EXT[a] - 1;
+        const int amin = (a == 2) ? zlo : 0, amax = (a == 2) ? zhi : n[a] - 1;
+        int o = lo[a] - (EXT[a] - (hi[a] - lo[a] + 1)) / 2;
+        if (a == 0) o &= ~1;
+        o = min(o, amax + 1 - EXT[a]);
+        if (a == 0) o &= ~1;
+        o = max(o, amin);
+        b[a] = o;
+        const bool in_vol = o >= 0 && o + EXT[a] - 1 <= n[a] - 1;
+        in_lo[a] = in_vol ? (float)o : INFINITY;
+        in_hi[a] = in_vol ? (float)(o + EXT[a] - 1) : -INFINITY;
       }
-      if (D == 3 && SLAB) fits &= lo[2] >= zlo && hi[2] <= zhi;
-      if (!inside && fits) {
-        // re-centre: the ball's box in the middle of the brick, clipped to the
-        // volume (z: the slab buffer); the x origin is even (4-byte copies)
-#pragma unroll
-        for (int a = 0; a < D; ++a) {
-          const int amin = (a == 2) ? zlo : 0, amax = (a == 2) ? zhi : n[a] - 1;
-          int o = lo[a] - (EXT[a] - (hi[a] - lo[a] + 1)) / 2;
-          if (a == 0) o &= ~1;
-          o = min(o, amax + 1 - EXT[a]);
-          if (a == 0) o &= ~1;
-          o = max(o, amin);
-          b[a] = o;
-          const bool in_vol = o >= 0 && o + EXT[a] - 1 <= n[a] - 1;
-          in_lo[a] = in_vol ? (float)o : INFINITY;
-          in_hi[a] = in_vol ? (float)(o + EXT[a] - 1) : -INFINITY;
-        }
-        // every read of the old brick finished before last iteration's barrier
-        load_brick<D, S>(brick, P, b[0], b[1], D == 3 ? b[2] : 0, zlo);
-        boff = (kMagicBits + (uint32_t)b[0]) + (kMagicBits + (uint32_t)b[1]) * (uint32_t)brick_sx(S);
-        if (D == 3) boff += (kMagicBits + (uint32_t)b[2]) * (uint32_t)(brick_sx(S) * S);
-        inside = true;
-        if (threadIdx.x == 0) atomicAdd(&g_evolve_stats[0], 1ull);
-      }
-      mode = inside ? (interior ? 0 : 1) : 2;
+      // every read of the old brick finished before last iteration's barrier
+      load_brick<D, S>(brick, P, b[0], b[1], D == 3 ? b[2] : 0, zlo);
+      boff = (kMagicBits + (uint32_t)b[0]) + (kMagicBits + (uint32_t)b[1]) * (uint32_t)brick_sx(S);
+      if (D == 3) boff += (kMagicBits + (uint32_t)b[2]) * (uint32_t)(brick_sx(S) * S);
+      inside = true;
+      if (threadIdx.x == 0) atomicAdd(&g_evolve_stats[0], 1ull);
     }
+    return inside ? (interior ? 0 : 1) : 2;
+  }
+};
+
+template <int D, int W, int S, bool SLAB, int CH, int L>
+__global__ void __launch_bounds__(32 * W, W == 4 ? 3 : SNK_BRICK_MINB8) evolve_brick_kernel(const __grid_constant__ EvoParams P) {
+  constexpr int B = CH << L;
+  constexpr bool PIPE = SNK_BRICK_PIPE && L == 0;
+  extern __shared__ __align__(16) uint16_t brick[];
+  __shared__ __align__(16) float xch[2][5][W];      // [parity][component][warp]
+  __shared__ float bc[4];                           // PIPE: (cx, cy, cz, R) after warp 0's update
+  const int lane = threadIdx.x & 31, wsub = threadIdx.x >> 5;
+  const int64_t cell = blockIdx.x;
+  CellState s;
+  cell_begin(P, cell, D, s);
+  uint32_t halo = 0;
+  BrickCtl<D, S, SLAB> bk;
+  bk.init(P);
+  const uint32_t j0 = (uint32_t)((wsub * 32 + lane) * B);
+  Dir dir[PIPE ? CH : 1];
+  if constexpr (PIPE) draw_dirs<D, CH>(P, cell_iter(P, s, 1), j0, dir);
+  for (int it = 1; it <= P.T + 1; ++it) {
+    CellIt C = cell_iter(P, s, it);
+    const float c[3] = {s.cx, s.cy, s.cz};
+    const int mode = bk.prepare(brick, P, c, C.rho_s);
     Acc part;
-    C.boff = boff;
+    C.boff = bk.boff;
     if constexpr (PIPE) {
       if (mode == 0) {
         part = chunk_sum_dirs<D, G_BRICK_FAST, S, CH>(P, C, dir, brick, halo);
@@ -847,7 +876,23 @@ __global__ void __launch_bounds__(32 * W, W == 4 ? 3 : SNK_BRICK_MINB8) evolve_b
     float* xo = &xch[it & 1][0][0];
     warp_reduce_scatter(part, xo + wsub, lane, W);
     __syncthreads();   // also: every brick read of this iteration is done
-    if constexpr (PIPE) {
+    if constexpr (PIPE && SNK_BRICK_PIPE == 2) {
+      // every warp takes the (identical) update itself: one barrier per
+      // iteration; xch is double-buffered by parity, and the next brick reload
+      // happens after this barrier, i.e. after every read of this iteration
+      Acc sum;
+      sum.a0 = comp_tree<W>(xo + 0 * W);
+      sum.cx = comp_tree<W>(xo + 1 * W);
+      sum.cy = comp_tree<W>(xo + 2 * W);
+      sum.cz = comp_tree<W>(xo + 3 * W);
+      sum.aR = comp_tree<W>(xo + 4 * W);
+      if (cell_update<D>(P, s, C, sum, it)) break;
+      CellIt Cn;
+      Cn.p0 = s.q0 ^ (uint32_t)(it + 1);
+      Cn.p1 = s.q1;
+      Cn.p3 = s.q3;
+      draw_dirs<D, CH>(P, Cn, j0, dir);
+    } else if constexpr (PIPE) {
       const bool done = it == P.T + 1;
       if (wsub == 0) {
         Acc sum;
@@ -881,6 +926,96 @@ __global__ void __launch_bounds__(32 * W, W == 4 ? 3 : SNK_BRICK_MINB8) evolve_b
   if (threadIdx.x == 0) cell_finish(P, s, cell);
 }
 
+// =========================================================================
+// Grid kernel (SNK_EST_GRID): the paper's original uniform integration, Eq. 5
+// — per iteration the sum over the voxels k with |k - c| < R + dR/2
+// of S(|k - c|) I(k) and its derivatives (Eqs. 7-10), I(k) read at the voxel (no
+// interpolation), unit voxel volume, the radial term 0 at r = 0.  The
+// baseline Monte-Carlo integration replaced (Figs. 6-7).  One CTA of W
+// warps per cell with the same shared-memory brick as the MC kernel; warp w
+// takes the rows (y, z) w, w + W, ... of the voxel box, lane l the voxels x0 +
+// l, x0 + l + 32, ... of a row (consecutive u16: conflict-free LDS), rows
+// outside the ball skipped whole.  Sums: per thread in row order, then the
+// lane and warp trees of the MC kernel — a fixed order, so the result is
+// deterministic (it is not the oracle's order: parity is to tolerance).
+template <int D, int W, int S, bool SLAB>
+__global__ void __launch_bounds__(32 * W, 3) evolve_grid_kernel(const __grid_constant__ EvoParams P) {
+  extern __shared__ __align__(16) uint16_t brick[];
+  __shared__ __align__(16) float xch[2][5][W];
+  constexpr int SX = brick_sx(S), SP = SX * S;
+  const int lane = threadIdx.x & 31, wsub = threadIdx.x >> 5;
+  const int64_t cell = blockIdx.x;
+  CellState s;
+  cell_begin(P, cell, D, s);
+  uint32_t halo = 0;
+  BrickCtl<D, S, SLAB> bk;
+  bk.init(P);
+  const int n[3] = {P.nx, P.ny, P.nz};
+  const float fn1[3] = {P.fnx1, P.fny1, P.fnz1};
+  for (int it = 1; it <= P.T + 1; ++it) {
+    const CellIt C = cell_iter(P, s, it);
+    const float c[3] = {s.cx, s.cy, s.cz};
+    const int mode = bk.prepare(brick, P, c, C.rho_s);
+    const float rs = C.rho_s, rs2 = __fmul_rn(rs, rs);
+    // the voxel box (a superset of the ball: membership is decided by r^2 < rs^2)
+    const float ext = __fmaf_rn(rs, 1.0001f, 0.01f);
+    int lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+      lo[a] = (int)ceilf(fmaxf(__fsub_rn(c[a], ext), 0.0f));
+      hi[a] = (int)floorf(fminf(__fadd_rn(c[a], ext), fn1[a]));
+    }
+    (void)n;
+    const int nyb = hi[1] - lo[1] + 1, nzb = D == 3 ? hi[2] - lo[2] + 1 : 1;
+    const int nrows = nyb * nzb;
+    Acc part{0.0f, 0.0f, 0.0f, 0.0f, 0.0f};
+    for (int r = wsub; r < nrows; r += W) {
+      const int z = D == 3 ? lo[2] + r / nyb : 0;
+      const int y = lo[1] + (D == 3 ? r % nyb : r);
+      const float dy = __fsub_rn((float)y, c[1]);
+      const float dz = D == 3 ? __fsub_rn((float)z, c[2]) : 0.0f;
+      const float dyz2 = __fmaf_rn(dz, dz, __fmul_rn(dy, dy));
+      if (!(dyz2 < rs2)) continue;   // the row misses the ball (warp-uniform)
+      const uint16_t* src;           // the row, indexed by global x
+      if (mode != 2) {
+        src = brick + ((D == 3 ? (z - bk.b[2]) * SP : 0) + (y - bk.b[1]) * SX - bk.b[0]);
+      } else {
+        if (SLAB && D == 3 && (z < P.z_lo || z >= P.z_lo + P.nz_buf)) {
+          halo = 1u;                 // a voxel of the ball outside the slab buffer
+          continue;
+        }
+        src = P.img + ((int64_t)(z - (SLAB ? P.z_lo : 0)) * P.ny + y) * (int64_t)P.nx;
+      }
+      for (int x = lo[0] + lane; x <= hi[0]; x += 32) {
+        const float dx = __fsub_rn((float)x, c[0]);
+        const float r2 = __fmaf_rn(dx, dx, dyz2);
+        if (!(r2 < rs2)) continue;
+        const float v = mag(src[x]);
+        const float rr = __fsqrt_rn(r2);
+        const float inv = r2 > 0.0f ? __frcp_rn(rr) : 0.0f;
+        Draw d;
+        d.t = rr;
+        d.ox = __fmul_rn(dx, inv);
+        d.oy = __fmul_rn(dy, inv);
+        d.oz = __fmul_rn(dz, inv);
+        part = acc_add(part, leaves(P, C, d, v, D == 3));
+      }
+    }
+    float* xo = &xch[it & 1][0][0];
+    warp_reduce_scatter(part, xo + wsub, lane, W);
+    __syncthreads();   // also: every brick read of this iteration is done
+    Acc sum;
+    sum.a0 = comp_tree<W>(xo + 0 * W);
+    sum.cx = comp_tree<W>(xo + 1 * W);
+    sum.cy = comp_tree<W>(xo + 2 * W);
+    sum.cz = comp_tree<W>(xo + 3 * W);
+    sum.aR = comp_tree<W>(xo + 4 * W);
+    if (cell_update<D, true>(P, s, C, sum, it)) break;
+  }
+  if (SLAB && __syncthreads_or(halo != 0)) s.flags |= SNK_F_HALO;
+  if (threadIdx.x == 0) cell_finish(P, s, cell);
+}
+
 // ------------------------------------------------------------------ launching
 template <int D, int W, bool SLAB, int CH, int L>
 int32_t launch_warp(const EvoParams& P, cudaStream_t st) {
@@ -900,6 +1035,19 @@ int32_t launch_brick(const EvoParams& P, cudaStream_t st) {
   if (attr_err != cudaSuccess) return cuda_fail(attr_err, "cudaFuncSetAttribute(evolve_brick_kernel)");
   k<<<(unsigned)P.n, 32 * W, smem, st>>>(P);
   SNK_LAUNCH_CHECK("evolve_brick_kernel");
+  return SNK_OK;
+}
+
+template <int D, int W, int S, bool SLAB>
+int32_t launch_grid(const EvoParams& P, cudaStream_t st) {
+  auto k = evolve_grid_kernel<D, W, S, SLAB>;
+  const int smem = (D == 3 ? brick_sx(S) * S * S : brick_sx(S) * S) * 2;
+  static std::once_flag once;
+  static cudaError_t attr_err = cudaSuccess;
+  std::call_once(once, [&] { attr_err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); });
+  if (attr_err != cudaSuccess) return cuda_fail(attr_err, "cudaFuncSetAttribute(evolve_grid_kernel)");
+  k<<<(unsigned)P.n, 32 * W, smem, st>>>(P);
+  SNK_LAUNCH_CHECK("evolve_grid_kernel");
   return SNK_OK;
 }
 
@@ -1040,6 +1188,14 @@ int32_t evolve_impl(const snk_grid* g, const snk_params* p, const uint16_t* d_im
   if (D == 3 && g->n[2] < 2) return fail(SNK_SHAPE, "3D needs nz >= 2");
   if (g->n[0] * g->n[1] * g->nz_buf >= ((int64_t)1 << 32)) return fail(SNK_SHAPE, "buffer too large");
   const bool slab = !(g->z_lo == 0 && g->nz_buf == g->n[2]);
+  if (p->estimator == SNK_EST_GRID) {
+    // Eq. 5 voxel sums: the brick kernel's brick, 8 warps per cell (rows)
+    if (g->n[0] % 2 != 0 || (reinterpret_cast<uintptr_t>(d_image) & 3) != 0 || p->kernel_variant == 1)
+      return fail(SNK_CONFIG, "the grid estimator needs the brick kernel (even nx, 4-byte aligned image)");
+    P.vscale = (float)p->intensity_scale;
+    if (D == 3) return slab ? launch_grid<3, 8, kS3, true>(P, st) : launch_grid<3, 8, kS3, false>(P, st);
+    return launch_grid<2, 8, 64, false>(P, st);
+  }
   // kernel choice: 0 auto, 1 warp (global gathers), 2 brick (shared memory)
   const uint32_t variant = p->kernel_variant;
   const int Wb = p->cta_warps > 0 ? p->cta_warps : 4;

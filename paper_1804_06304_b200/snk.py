@@ -25,6 +25,7 @@ F_CONVERGED, F_COLLAPSED, F_RMAX, F_DOMAIN, F_LEASHED, F_CULLED_E0, F_CULLED_OVE
     1, 2, 4, 8, 16, 32, 64, 128)
 SEED_LATTICE, SEED_MAXIMA, SEED_GIVEN = 0, 1, 2
 IMAGE_INTENSITY, IMAGE_GRADMAG = 0, 1
+EST_MC, EST_GRID = 0, 1
 
 
 class SNKError(RuntimeError):
@@ -52,7 +53,8 @@ class snk_params(C.Structure):
                 ("leash", C.c_double), ("conv_tol", C.c_double), ("max_iters", C.c_int32),
                 ("n_samples", C.c_int32), ("seed_mode", C.c_int32), ("seed_window", C.c_int32),
                 ("image_term", C.c_int32), ("cta_warps", C.c_int32), ("seed_threshold", C.c_uint32),
-                ("kernel_variant", C.c_uint32), ("seed", C.c_uint64)]
+                ("kernel_variant", C.c_uint32), ("estimator", C.c_int32), ("_pad1", C.c_int32),
+                ("seed", C.c_uint64)]
 
 
 class snk_cell(C.Structure):
@@ -263,7 +265,7 @@ def make_params(r0=10.0, *, delta_R=2.0, eps0=0.5, e0=-3.0, sigma=1.0, intensity
                 max_step=1.0, r_min=1.0, r_max=None, leash=None, conv_tol=1e-3, max_iters=400,
                 n_samples=1024, seed_mode=SEED_MAXIMA, seed_window=4, image_term=IMAGE_INTENSITY,
                 cta_warps=0, seed_threshold=70 * 257, seed=1804063040,
-                kernel_variant=0) -> snk_params:
+                kernel_variant=0, estimator=EST_MC) -> snk_params:
     """Defaults: DESIGN.md §3 (readings G2-G9, G18, G20)."""
     p = snk_params()
     p.r0, p.delta_R, p.eps0, p.e0, p.sigma = r0, delta_R, eps0, e0, sigma
@@ -274,5 +276,6 @@ def make_params(r0=10.0, *, delta_R=2.0, eps0=0.5, e0=-3.0, sigma=1.0, intensity
     p.seed_mode, p.seed_window, p.image_term, p.cta_warps = seed_mode, seed_window, image_term, cta_warps
     p.seed_threshold = seed_threshold
     p.kernel_variant = kernel_variant
+    p.estimator = estimator
     p.seed = seed & 0xFFFFFFFFFFFFFFFF
     return p

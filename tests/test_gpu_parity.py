@@ -368,6 +368,71 @@ def test_evolve_slab_buffer_bit_identical(gpu):
     assert got.tobytes() == full[sel].tobytes()
 
 
+# ---------------------------------------------------------------- grid estimator (Eq. 5)
+
+
+@pytest.mark.parametrize("r0,T", [(10.0, 400), (14.0, 150), (18.0, 80)])
+def test_evolve_grid_parity(gpu, r0, T):
+    """SNK_EST_GRID: the paper's uniform integration (Eq. 5 over the voxels of
+    the ball) vs the oracle's grid mode, fp32 vs fp64.  r0 = 14 and 18 move the
+    brick and take the global path (balls larger than the brick)."""
+    torch, snk, pipeline = gpu
+    n = (64, 64, 64) if r0 == 10.0 else (72, 72, 72)
+    cfg = synth.CONFIGS["C1"].with_(r0=r0, max_iters=T, n=n)
+    raw = synth.generate(synth.CONFIGS["C1"].with_(n=n))
+    p = pipeline.params_for(cfg, seed_mode=snk.SEED_LATTICE, estimator=snk.EST_GRID)
+    P = pipeline.Pipeline(3, n, p)
+    P.upload(raw)
+    P.preprocess()
+    P.seed()
+    P.evolve()
+    torch.cuda.synchronize()
+    g = P.cells_np()
+    P.evolve()
+    torch.cuda.synchronize()
+    assert P.cells_np().tobytes() == g.tobytes(), "grid evolution is not deterministic"
+    B = oracle.blur(raw, 3, 1.0)
+    o = oracle.evolve(B, _ora_params(cfg, mode=1), P.seeds_np(), ids=np.arange(P.n_seeds))
+    _assert_cells_close(g, o, f"grid r0={r0}")
+    fmask = oracle.COLLAPSED | oracle.RMAX
+    assert np.array_equal(g["flags"] & fmask, o["flags"] & fmask)
+
+
+def test_evolve_grid_2d_and_slab(gpu):
+    """Grid estimator in 2D (C2 crop) and on a z-slab buffer (bit-identical to the whole volume)."""
+    torch, snk, pipeline = gpu
+    cfg = synth.CONFIGS["C2"]
+    sub = np.ascontiguousarray(synth.generate(cfg)[0][:200, :256])
+    c2 = cfg.with_(n=(256, 200, 1), max_iters=200)
+    p = pipeline.params_for(c2, estimator=snk.EST_GRID)
+    P = pipeline.Pipeline(2, c2.n, p)
+    P.upload(sub[None])
+    P.preprocess()
+    P.seed()
+    P.evolve()
+    torch.cuda.synchronize()
+    B = oracle.blur(sub[None], 2, 1.0)
+    o = oracle.evolve(B, _ora_params(c2, mode=1), P.seeds_np(), ids=np.arange(P.n_seeds))
+    assert P.n_seeds > 3
+    _assert_cells_close(P.cells_np(), o, "grid 2D")
+    # 3D slab
+    cfg = synth.CONFIGS["C1"].with_(max_iters=100)
+    P, raw, p = _gpu_smooth_seeds(torch, snk, pipeline, cfg)
+    p = pipeline.params_for(cfg, estimator=snk.EST_GRID)
+    P.params = p
+    P.evolve()
+    torch.cuda.synchronize()
+    full = P.cells_np()
+    sel = np.nonzero(P.seeds_np()[:, 2] < 20)[0]
+    z1 = 20 + int(np.ceil(2 * cfg.r0 + 2 * cfg.r0 + 2 + 2))
+    g = snk.make_grid(3, (64, 64, 64), z_lo=0, nz_buf=z1, own=(0, 20))
+    cells = torch.empty(len(sel) * 48, dtype=torch.uint8, device="cuda")
+    snk.snk_evolve(g, p, P.smooth[:z1].contiguous(), P.seeds[sel].contiguous(),
+                   _t(torch, sel.astype(np.int64)), 0, len(sel), cells, None)
+    torch.cuda.synchronize()
+    assert pipeline.as_cells(cells, len(sel)).tobytes() == full[sel].tobytes()
+
+
 # ---------------------------------------------------------------- a7-a8, stage-isolated and end to end
 
 
