@@ -118,6 +118,7 @@ def _declare(L):
         "ora_is_maxima_seed": (i32, [vp, vp, vp, vp, i32, i32, u32, i64, i64, i64]),
         "ora_seeds_maxima": (i32, [vp, vp, vp, vp, vp, vp, i32, i32, u32, vp, i64, vp]),
         "ora_energy_mc": (None, [vp, vp, vp, vp, vp, vp, d, u32, i64, vp]),
+        "ora_evolve_range": (None, [vp, vp, vp, vp, vp, vp, i64, i32, i32]),
         "ora_energy_grid": (None, [vp, vp, vp, vp, vp, vp, d, vp]),
         "ora_energy_ss": (d, [vp, vp, vp, vp, d, i32]),
         "ora_evolve": (None, [vp, vp, vp, vp, vp, vp, vp, i64, vp]),
@@ -299,6 +300,55 @@ def evolve(vol, params: Params, seeds, ids=None, org=None, n_global=None, z_lo=0
     pc = params.c()
     lib().ora_evolve(_p(v), _p(n), _p(o), _p(nb), C.byref(pc), _p(s), _p(ids), len(s), _p(out))
     return out
+
+
+def evolve_range(vol, params: Params, cells, it0: int, it1: int, org=None, n_global=None):
+    """Continue the records ``cells`` (CELL_DTYPE; c, R, E, seed, flags, id are
+    the state) through iterations it0..it1; returns the new records."""
+    v = _u16(vol)
+    n, o, nb = _box(v, org, n_global)
+    out = np.ascontiguousarray(cells, CELL_DTYPE).copy()
+    pc = params.c()
+    lib().ora_evolve_range(_p(v), _p(n), _p(o), _p(nb), C.byref(pc), _p(out), len(out), int(it0), int(it1))
+    return out
+
+
+def init_cells(params: Params, seeds, ids=None):
+    """Records at the start of evolution: c = seed, R = r0 (O5)."""
+    s = np.ascontiguousarray(seeds, np.float32).reshape(-1, 3).astype(np.float64)
+    out = np.zeros(len(s), CELL_DTYPE)
+    out["c"] = s
+    out["seed"] = s
+    out["R"] = params.r0
+    out["id"] = np.arange(len(s), dtype=np.int64) if ids is None else np.asarray(ids, np.int64)
+    return out
+
+
+def checkpoints(T: int, k: int):
+    """Periodic-culling segments (reading G25): [1, k], [k+1, 2k], ..., the last
+    one ending at T + 1 (E_final); a cull after every segment but the last."""
+    if k <= 0 or k >= T:
+        return [(1, T + 1)]
+    ends = list(range(k, T, k)) + [T + 1]
+    starts = [1] + [e + 1 for e in ends[:-1]]
+    return list(zip(starts, ends))
+
+
+def evolve_periodic(vol, params: Params, seeds, k: int, ids=None, org=None, n_global=None):
+    """Evolution with periodic culling every k iterations (SURVEY §8(f) 2
+    "dynamic culling"; reading G25): after segment [a, b] (b < T + 1) the live
+    records — state after iteration b, E of iteration b — go through O6 (E0,
+    then the greedy overlap competition on fp32 values); the survivors continue.
+    Returns the live records after iteration T + 1 (cull them with ``cull`` for
+    the detections)."""
+    cells = init_cells(params, seeds, ids)
+    for a, b in checkpoints(params.max_iters, k):
+        cells = evolve_range(vol, params, cells, a, b, org=org, n_global=n_global)
+        if b <= params.max_iters:
+            keep = cull(cells["c"].astype(np.float32), cells["R"].astype(np.float32),
+                        cells["E"].astype(np.float32), cells["flags"], cells["id"], params.dim, params.e0)
+            cells = cells[np.sort(keep)]
+    return cells
 
 
 def cull(c, R, E, flags, ids, dim, e0):

@@ -645,61 +645,90 @@ double ora_energy_ss(const uint16_t* v, const int64_t n[3], const ora_params* p,
 // shorter than 2m.  Iteration T+1 only evaluates E_final (G13).  CONVERGED if the
 // state moved by less than conv_tol (max norm) in iteration T (G9);
 // cells are never frozen.  Stops at T = max_iters.
+// One contour from its current state through iterations it0..it1 (1 <= it0,
+// it1 <= T + 1); the state is the record itself: c, R, E, seed (the leash
+// centre), flags (accumulated), id (the Philox stream key).
+static void evolve_cell(const Image& img, const ora_params* p, const int64_t n[3], int it0, int it1,
+                        ora_cell& cell) {
+  const int d = p->dim;
+  const int T = p->max_iters;
+  const double* s = cell.seed;
+  double c[3] = {cell.c[0], cell.c[1], cell.c[2]};
+  double R = cell.R;
+  uint32_t flags = cell.flags;
+  double E = cell.E;
+  for (int it = it0; it <= it1; ++it) {
+    const EnergyOut eo = (p->mode == 1) ? energy_grid(img, *p, c, R)
+                                        : energy_mc(img, *p, c, R, (uint32_t)it, cell.id);
+    if (eo.halo) flags |= F_HALO;
+    E = eo.E;
+    if (it == T + 1) break;
+    const double eps = p->eps0 / std::sqrt((double)it);
+    const double c_old[3] = {c[0], c[1], c[2]};
+    const double R_old = R;
+    for (int a = 0; a < 3; ++a) c[a] += clampd(-(eps / 2.0) * eo.gc[a], -p->max_step, p->max_step);
+    R = clampd(R + clampd(-(eps / 2.0) * eo.gR, -p->max_step, p->max_step), p->r_min, p->r_max);
+    bool leashed = false, domained = false;
+    for (int a = 0; a < 3; ++a) {
+      const double cl = clampd(c[a], s[a] - p->leash, s[a] + p->leash);
+      if (cl != c[a]) leashed = true;
+      c[a] = cl;
+    }
+    const double m = R + p->delta_R / 2.0;
+    for (int a = 0; a < 3; ++a) {
+      double cd;
+      if ((double)(n[a] - 1) < 2.0 * m) cd = (double)(n[a] - 1) / 2.0;
+      else cd = clampd(c[a], m, (double)(n[a] - 1) - m);
+      if (cd != c[a] && a < d) domained = true;
+      c[a] = cd;
+    }
+    if (it == T) {
+      double mv = std::fabs(R - R_old);
+      for (int a = 0; a < 3; ++a) mv = std::max(mv, std::fabs(c[a] - c_old[a]));
+      if (mv < p->conv_tol) flags |= F_CONVERGED;
+      if (leashed) flags |= F_LEASHED;
+      if (domained) flags |= F_DOMAIN;
+    }
+  }
+  // trivial contours as of the last iteration run
+  flags &= ~(uint32_t)(F_COLLAPSED | F_RMAX);
+  if (R <= p->r_min) flags |= F_COLLAPSED;
+  if (R >= p->r_max) flags |= F_RMAX;
+  for (int a = 0; a < 3; ++a) cell.c[a] = c[a];
+  cell.R = R;
+  cell.E = E;
+  cell.flags = flags;
+  cell.iters = std::min(it1, T);
+}
+
 void ora_evolve(const uint16_t* v, const int64_t n[3], const int64_t org[3], const int64_t nb[3],
                 const ora_params* p, const float* seeds_xyz, const int64_t* ids, int64_t ncell,
                 ora_cell* out) {
   const Image img = make_image(v, n, org, nb, p);
-  const int d = p->dim;
-  const int T = p->max_iters;
 #pragma omp parallel for schedule(dynamic, 1)
   for (int64_t i = 0; i < ncell; ++i) {
-    double s[3] = {(double)seeds_xyz[3 * i], (double)seeds_xyz[3 * i + 1], (double)seeds_xyz[3 * i + 2]};
-    double c[3] = {s[0], s[1], s[2]};
-    double R = p->r0;
-    uint32_t flags = 0;
-    double E = 0.0;
-    for (int it = 1; it <= T + 1; ++it) {
-      const EnergyOut eo = (p->mode == 1) ? energy_grid(img, *p, c, R)
-                                          : energy_mc(img, *p, c, R, (uint32_t)it, ids[i]);
-      if (eo.halo) flags |= F_HALO;
-      if (it == T + 1) { E = eo.E; break; }
-      const double eps = p->eps0 / std::sqrt((double)it);
-      const double c_old[3] = {c[0], c[1], c[2]};
-      const double R_old = R;
-      for (int a = 0; a < 3; ++a) c[a] += clampd(-(eps / 2.0) * eo.gc[a], -p->max_step, p->max_step);
-      R = clampd(R + clampd(-(eps / 2.0) * eo.gR, -p->max_step, p->max_step), p->r_min, p->r_max);
-      bool leashed = false, domained = false;
-      for (int a = 0; a < 3; ++a) {
-        const double cl = clampd(c[a], s[a] - p->leash, s[a] + p->leash);
-        if (cl != c[a]) leashed = true;
-        c[a] = cl;
-      }
-      const double m = R + p->delta_R / 2.0;
-      for (int a = 0; a < 3; ++a) {
-        double cd;
-        if ((double)(n[a] - 1) < 2.0 * m) cd = (double)(n[a] - 1) / 2.0;
-        else cd = clampd(c[a], m, (double)(n[a] - 1) - m);
-        if (cd != c[a] && a < d) domained = true;
-        c[a] = cd;
-      }
-      if (it == T) {
-        double mv = std::fabs(R - R_old);
-        for (int a = 0; a < 3; ++a) mv = std::max(mv, std::fabs(c[a] - c_old[a]));
-        if (mv < p->conv_tol) flags |= F_CONVERGED;
-        if (leashed) flags |= F_LEASHED;
-        if (domained) flags |= F_DOMAIN;
-      }
-    }
-    if (R <= p->r_min) flags |= F_COLLAPSED;
-    if (R >= p->r_max) flags |= F_RMAX;
     ora_cell& o = out[i];
-    for (int a = 0; a < 3; ++a) { o.c[a] = c[a]; o.seed[a] = s[a]; }
-    o.R = R;
-    o.E = E;
-    o.flags = flags;
-    o.iters = T;
+    for (int a = 0; a < 3; ++a) o.c[a] = o.seed[a] = (double)seeds_xyz[3 * i + a];
+    o.R = p->r0;
+    o.E = 0.0;
+    o.flags = 0;
+    o.iters = 0;
     o.id = ids[i];
+    evolve_cell(img, p, n, 1, p->max_iters + 1, o);
   }
+}
+
+// Periodic culling ("dynamic culling"; reading G25 in
+// DESIGN.md): evolution in segments.  Continues every record of cells[] from
+// its state through iterations it0..it1; E is the MC (grid) energy of
+// iteration it1 (E_final when it1 = T + 1), COLLAPSED / RMAX reflect the
+// radius after it1.  ora_evolve = one segment 1..T+1.
+void ora_evolve_range(const uint16_t* v, const int64_t n[3], const int64_t org[3],
+                      const int64_t nb[3], const ora_params* p, ora_cell* cells, int64_t ncell,
+                      int32_t it0, int32_t it1) {
+  const Image img = make_image(v, n, org, nb, p);
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int64_t i = 0; i < ncell; ++i) evolve_cell(img, p, n, it0, it1, cells[i]);
 }
 
 // ---------------------------------------------------------------------------

@@ -230,3 +230,75 @@ def test_crop_and_slab_equal_full_volume(ora):
     # a crop that is too small is detected (HALO flag), never silently wrong
     small = ora.evolve(vol[20:30], p, seeds, ids=np.array([5, 9]), z_lo=20, n_global=(48, 48, 48))
     assert np.all(small["flags"] & ora.HALO)
+
+
+# ---------------------------------------------------------------- periodic culling
+
+
+def test_segments_resume_exactly(ora):
+    """Evolution in segments [1,a], [a+1,b], ..., [., T+1] from the records is the
+    same computation as one run (the record is the whole state)."""
+    vol = _ball_volume(40, (20.0, 20.0, 20.0), 8.0, ora=ora)
+    p = ora.Params(r0=9.0, n_samples=128, dim=3, max_iters=50)
+    seeds = np.random.default_rng(3).uniform(15, 25, (6, 3)).astype(np.float32)
+    one = ora.evolve(vol, p, seeds, ids=np.arange(10, 16))
+    assert ora.checkpoints(50, 20) == [(1, 20), (21, 40), (41, 51)]
+    assert ora.checkpoints(50, 0) == [(1, 51)] and ora.checkpoints(50, 50) == [(1, 51)]
+    cells = ora.init_cells(p, seeds, ids=np.arange(10, 16))
+    for a, b in [(1, 7), (8, 8), (9, 33), (34, 51)]:
+        cells = ora.evolve_range(vol, p, cells, a, b)
+    assert cells.tobytes() == one.tobytes()
+    # grid mode too
+    pg = ora.Params(r0=9.0, dim=3, max_iters=20, mode=1)
+    one = ora.evolve(vol, pg, seeds[:2])
+    cells = ora.evolve_range(vol, pg, ora.evolve_range(vol, pg, ora.init_cells(pg, seeds[:2]), 1, 11), 12, 21)
+    assert cells.tobytes() == one.tobytes()
+
+
+def test_periodic_culling_blank_volume(ora):
+    """A uniform image has no blob: the MC energy stays above E0 = -3 (|E| <= 2.4,
+    SURVEY A10), so the first checkpoint culls every cell."""
+    vol = np.full((48, 48, 48), 60 * 257, np.uint16)
+    p = ora.Params(r0=10.0, n_samples=256, dim=3, max_iters=60)
+    st, seeds = ora.seeds_lattice((48, 48, 48), 3, 10.0)
+    live = ora.evolve_periodic(vol, p, seeds, 20)
+    assert len(seeds) == 27 and len(live) == 0
+
+
+def test_periodic_culling_c1_same_detections(ora):
+    """On C1 (64 lattice snakes, 8 nuclei) culling every 50 iterations still finds
+    one detection per nucleus (A9 / AC6); cells never interact during evolution,
+    so every detection's record is bit-identical to the same cell's record in the
+    run without periodic culling (only WHICH cells survive may change: an early
+    overlap competition can pick a different snake of the same nucleus); and
+    every removed cell violated E0 or lost an overlap competition at its
+    checkpoint (P:227, P:326)."""
+    cfg = synth.CONFIGS["C1"]
+    raw = synth.generate(cfg)
+    p = ora.Params(r0=cfg.r0, n_samples=cfg.n_samples, dim=3, seed=cfg.philox_seed)
+    B = ora.blur(raw, 3, 1.0)
+    st, seeds = ora.seeds_lattice(cfg.n, 3, cfg.r0)
+    full = ora.evolve(B, p, seeds)
+    det_full = full[ora.cull(full["c"].astype(np.float32), full["R"].astype(np.float32),
+                             full["E"].astype(np.float32), full["flags"], full["id"], 3, p.e0)]
+    live = ora.evolve_periodic(B, p, seeds, 50)
+    assert 8 <= len(live) < 64
+    det = live[ora.cull(live["c"].astype(np.float32), live["R"].astype(np.float32),
+                        live["E"].astype(np.float32), live["flags"], live["id"], 3, p.e0)]
+    assert len(det) == 8 and len(det_full) == 8
+    truth = synth.nuclei(cfg)
+    d = np.linalg.norm(det["c"][:, None, :] - truth["c"][None, :, :], axis=2)
+    assert sorted(np.argmin(d, axis=1).tolist()) == list(range(8)) and d.min(axis=1).max() < 2.0
+    assert det.tobytes() == full[det["id"]].tobytes()
+    # the survivors of the checkpoint are exactly the O6 survivors of the records there
+    cells = ora.evolve_range(B, p, ora.init_cells(p, seeds), 1, 50)
+    keep = ora.cull(cells["c"].astype(np.float32), cells["R"].astype(np.float32),
+                    cells["E"].astype(np.float32), cells["flags"], cells["id"], 3, p.e0)
+    dropped = np.setdiff1d(np.arange(64), keep)
+    c32, R32 = cells["c"].astype(np.float32).astype(np.float64), cells["R"].astype(np.float32).astype(np.float64)
+    rho = 2.0 ** (-1.0 / 3.0)
+    for i in dropped:
+        bad_e = np.float32(cells["E"][i]) > p.e0 or cells["flags"][i] & (ora.COLLAPSED | ora.RMAX)
+        lost = any(np.sum((c32[i] - c32[a]) ** 2) < (rho * max(R32[i], R32[a])) ** 2
+                   and (np.float32(cells["E"][a]), a) < (np.float32(cells["E"][i]), i) for a in keep)
+        assert bad_e or lost, f"cell {i} dropped without a reason"
