@@ -159,7 +159,7 @@ def run_ours(args):
     torch.cuda.set_device(local_rank)
     from paper_1804_06304_b200 import pipeline, snk
     p = pipeline.params_for(cfg, image_term=snk.IMAGE_INTENSITY, cta_warps=args.cta_warps,
-                            kernel_variant=args.kernel_variant)
+                            kernel_variant=args.kernel_variant, cull_every=args.cull_every)
     P = pipeline.Pipeline(cfg.dim, cfg.n, p, spacing=cfg.spacing, gradmag=True)
     h_raw = torch.empty((cfg.n[2], cfg.n[1], cfg.n[0]), dtype=torch.uint16, pin_memory=True)
     t = time.perf_counter()
@@ -204,7 +204,8 @@ def run_ours(args):
     evolve_ms = [e[1].elapsed_time(e[2]) for e in evs]
     n_cells = P.n_seeds
     n_iso_l, n_dets = list(P.n_iso), P.n_dets
-    samples = n_cells * (cfg.max_iters + 1) * cfg.n_samples
+    # ray-samples evaluated per step (with periodic culling: only the live cells' iterations)
+    samples = P.cell_iters * cfg.n_samples
     value = samples * args.steps / (total_ms / 1e3)
     cells_per_s = n_cells * args.steps / (total_ms / 1e3)
     phase = {"preprocess+seeds": statistics.mean(e[0].elapsed_time(e[1]) for e in evs),
@@ -277,7 +278,7 @@ def run_ours(args):
         "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": workload_name(cfg), "volume_iso": n_iso_l, "cells": n_cells,
                    "detections": n_dets, "n_samples": cfg.n_samples, "iters": cfg.max_iters,
-                   "seed_mode": cfg.seed_mode, "parallelism": "1 GPU",
+                   "seed_mode": cfg.seed_mode, "parallelism": "1 GPU", "cull_every": args.cull_every,
                    "l2": "inputs larger than L2 (u16 volume %.1f GiB > 126 MB)" % (h_raw.numel() * 2 / 2**30)},
         "cells_per_s": cells_per_s, "phase_ms": phase, "gpu_launches": int(launches),
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
@@ -329,6 +330,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cta-warps", type=int, default=0, help="warps per cell (0: auto)")
     ap.add_argument("--kernel-variant", type=int, default=0, help="evolve kernel: 0 auto, 1 warp, 2 brick")
+    ap.add_argument("--cull-every", type=int, default=0,
+                    help="periodic culling every k iterations (P:326, G25); 0 = the paper's end-of-run cull")
     ap.add_argument("--e2e-inflight", type=int, default=2, help="steps in flight in the end-to-end run")
     args = ap.parse_args()
     if args.warmup < 3:

@@ -95,6 +95,12 @@ typedef struct snk_grid {
  *   image_term INTENSITY | GRADMAG                      cta_warps warps per cell: 0 auto, 1, 2, 4, 8
  *   kernel_variant  0 auto (brick kernel when nx is even), 1 warp kernel, 2 brick kernel
  *   estimator SNK_EST_MC | SNK_EST_GRID (grid: brick kernel only, even nx)
+ *   cull_every  periodic culling ("dynamic culling", reading G25): 0 = off
+ *             (the paper's end-of-run cull only); k > 0 = after iterations k, 2k, ...
+ *             (< T) the live cells go through the a7 cull (E0, then the overlap
+ *             competition, on their state after that iteration and its energy) and
+ *             only the survivors evolve on.  Used by snk_run and the drivers; the
+ *             building blocks are snk_cells_init / snk_evolve_range / snk_cull.
  *   seed      Philox key (G11) */
 typedef struct snk_params {
   double r0, delta_R, eps0, e0, sigma, intensity_scale, max_step, r_min, r_max, leash, conv_tol;
@@ -102,7 +108,7 @@ typedef struct snk_params {
   uint32_t seed_threshold;
   uint32_t kernel_variant; /* evolve kernel: 0 auto, 1 warp (global gathers), 2 brick (shared memory) */
   int32_t estimator;       /* SNK_EST_MC (default) or SNK_EST_GRID */
-  int32_t _pad1;
+  int32_t cull_every;      /* 0 off, else periodic culling every cull_every iterations (G25) */
   uint64_t seed;
 } snk_params;
 
@@ -186,6 +192,23 @@ int32_t snk_evolve(const snk_grid* g, const snk_params* p, const uint16_t* d_ima
                    const float* d_seeds, const int64_t* d_ids, int64_t id_base, int64_t n,
                    snk_cell* d_cells, void* d_ws, size_t ws_bytes, void* stream);
 
+/* Periodic culling (G25) — evolution in segments.  snk_cells_init writes
+ * the records of cells at the start of evolution (c = seed = d_seeds[i], R = r0,
+ * E = 0, flags = 0, id = d_ids ? d_ids[i] : id_base + i).  snk_evolve_range
+ * continues the n records of d_cells IN PLACE (their c, R, E, seed = leash
+ * centre, flags and id are the whole state) through iterations it0..it1
+ * (1 <= it0 <= it1 <= T + 1, the step schedule eps0/sqrt(n) and every rule of
+ * snk_evolve unchanged); afterwards E is the energy of iteration it1 (E_final if
+ * it1 = T + 1) and COLLAPSED / RMAX reflect the radius after it1.  Evolving
+ * 1..k, then k+1..T+1 gives records bit-identical to snk_evolve.  Between
+ * segments, snk_cull(d_cells -> survivors) is the checkpoint cull; the
+ * survivors (any order) are the next segment's records.  Asynchronous. */
+int32_t snk_cells_init(const snk_params* p, const float* d_seeds, const int64_t* d_ids,
+                       int64_t id_base, int64_t n, snk_cell* d_cells, void* stream);
+int32_t snk_evolve_range(const snk_grid* g, const snk_params* p, const uint16_t* d_image,
+                         snk_cell* d_cells, int64_t n, int32_t it0, int32_t it1, void* d_ws,
+                         size_t ws_bytes, void* stream);
+
 /* a7, first half — the energy cull ("energy greater than a threshold
  * (E0) are also removed", G14): copies cells with E <= e0 that are neither
  * COLLAPSED nor RMAX to d_out, preserving order; count to *n_out (host).
@@ -193,6 +216,15 @@ int32_t snk_evolve(const snk_grid* g, const snk_params* p, const uint16_t* d_ima
 int32_t snk_compact_candidates(const snk_params* p, const snk_cell* d_cells, int64_t n,
                                snk_cell* d_out, int64_t cap, int64_t* n_out, void* d_ws,
                                size_t ws_bytes, void* stream);
+
+/* Multi-GPU periodic culling (§8(e), G25): after a checkpoint cull of the
+ * all-gathered candidates, each rank keeps the survivors it owns, i.e. the
+ * records with id_lo <= id < id_hi (its exclusive prefix of seed counts).
+ * Order-preserving copy of those records of d_cells to d_out; count to *n_out
+ * (host).  Workspace: as snk_compact_candidates.  Synchronises. */
+int32_t snk_select_ids(const snk_cell* d_cells, int64_t n, int64_t id_lo, int64_t id_hi,
+                       snk_cell* d_out, int64_t cap, int64_t* n_out, void* d_ws, size_t ws_bytes,
+                       void* stream);
 
 /* a7 — culling: E0 filter as above, then the overlap competition
  * |c' - c''| < max(R', R'')/2^(1/d) -> the lower energy survives, resolved as

@@ -71,6 +71,7 @@ static int32_t validate_params(const snk_params* p, int dim) {
   if (p->kernel_variant > 2) return fail(SNK_CONFIG, "kernel_variant must be 0, 1 or 2");
   if (p->estimator != SNK_EST_MC && p->estimator != SNK_EST_GRID)
     return fail(SNK_CONFIG, "estimator must be SNK_EST_MC or SNK_EST_GRID");
+  if (p->cull_every < 0) return fail(SNK_CONFIG, "cull_every must be >= 0");
   if (p->estimator == SNK_EST_GRID && p->kernel_variant == 1)
     return fail(SNK_CONFIG, "the grid estimator runs in the brick kernel only (kernel_variant 0 or 2)");
   (void)dim;
@@ -201,6 +202,28 @@ int32_t snk_evolve(const snk_grid* g, const snk_params* p, const uint16_t* d_ima
                      as_stream(stream));
 }
 
+int32_t snk_cells_init(const snk_params* p, const float* d_seeds, const int64_t* d_ids,
+                       int64_t id_base, int64_t n, snk_cell* d_cells, void* stream) {
+  clear_error();
+  if (!p || n < 0) return fail(SNK_CONFIG, "bad args");
+  if (n > 0 && (!d_seeds || !d_cells)) return fail(SNK_CONFIG, "null buffer");
+  return cells_init_impl(p, d_seeds, d_ids, id_base, n, d_cells, as_stream(stream));
+}
+
+int32_t snk_evolve_range(const snk_grid* g, const snk_params* p, const uint16_t* d_image,
+                         snk_cell* d_cells, int64_t n, int32_t it0, int32_t it1, void* d_ws,
+                         size_t ws_bytes, void* stream) {
+  clear_error();
+  SNK_TRY(validate(g, p));
+  if (n < 0) return fail(SNK_CONFIG, "n < 0");
+  if (it0 < 1 || it1 < it0 || it1 > p->max_iters + 1) return fail(SNK_CONFIG, "need 1 <= it0 <= it1 <= T + 1");
+  if (n == 0) return SNK_OK;
+  if (!d_image || !d_cells) return fail(SNK_CONFIG, "null buffer");
+  SNK_TRY(check_ws(evolve_ws(g, p, n), d_ws, ws_bytes));
+  return evolve_impl(g, p, d_image, nullptr, nullptr, 0, n, d_cells, d_ws, ws_bytes,
+                     as_stream(stream), it0, it1, true);
+}
+
 int32_t snk_compact_candidates(const snk_params* p, const snk_cell* d_cells, int64_t n,
                                snk_cell* d_out, int64_t cap, int64_t* n_out, void* d_ws,
                                size_t ws_bytes, void* stream) {
@@ -208,6 +231,15 @@ int32_t snk_compact_candidates(const snk_params* p, const snk_cell* d_cells, int
   if (!p || !n_out || n < 0 || cap < 0) return fail(SNK_CONFIG, "bad args");
   if (n > 0 && (!d_cells || (cap > 0 && !d_out))) return fail(SNK_CONFIG, "null buffer");
   return compact_impl(p, d_cells, n, d_out, cap, n_out, d_ws, ws_bytes, as_stream(stream));
+}
+
+int32_t snk_select_ids(const snk_cell* d_cells, int64_t n, int64_t id_lo, int64_t id_hi,
+                       snk_cell* d_out, int64_t cap, int64_t* n_out, void* d_ws, size_t ws_bytes,
+                       void* stream) {
+  clear_error();
+  if (!n_out || n < 0 || cap < 0) return fail(SNK_CONFIG, "bad args");
+  if (n > 0 && (!d_cells || (cap > 0 && !d_out))) return fail(SNK_CONFIG, "null buffer");
+  return select_ids_impl(d_cells, n, id_lo, id_hi, d_out, cap, n_out, d_ws, ws_bytes, as_stream(stream));
 }
 
 int32_t snk_cull(const snk_grid* g, const snk_params* p, const snk_cell* d_cells, int64_t n,
@@ -319,11 +351,32 @@ int32_t snk_run(int32_t dim, const int64_t n_raw[3], const double spacing[3],
   SNK_TRY(preprocess_impl(&L.g, p, d_iso, d_smooth, d_grad, scratch, sb, st));
   int64_t ns = 0, first = 0;
   SNK_TRY(seeds_impl(&L.g, p, d_smooth, d_seeds, max_cells, &ns, &first, scratch, sb, st));
-  if (ns > 0)
-    SNK_TRY(evolve_impl(&L.g, p, d_grad ? d_grad : d_smooth, d_seeds, nullptr, first, ns, d_cells,
-                        scratch, sb, st));
+  const uint16_t* d_img = d_grad ? d_grad : d_smooth;
   int64_t nd = 0;
-  SNK_TRY(cull_impl(&L.g, p, d_cells, ns, d_dets, max_cells, &nd, scratch, sb, st));
+  if (p->cull_every > 0 && p->cull_every < p->max_iters) {
+    // periodic culling (G25): segments, the a7 cull after each but the last
+    static thread_local int seg[1 << 12][2];
+    const int nseg = checkpoint_segments(p->max_iters, p->cull_every, seg, 1 << 12);
+    snk_cell* cur = d_cells;
+    snk_cell* nxt = d_dets;
+    int64_t live = ns;
+    SNK_TRY(cells_init_impl(p, d_seeds, nullptr, first, ns, cur, st));
+    for (int k = 0; k < nseg; ++k) {
+      SNK_TRY(evolve_impl(&L.g, p, d_img, nullptr, nullptr, 0, live, cur, scratch, sb, st, seg[k][0],
+                          seg[k][1], true));
+      if (k + 1 < nseg) {
+        SNK_TRY(cull_impl(&L.g, p, cur, live, nxt, max_cells, &live, scratch, sb, st));
+        std::swap(cur, nxt);
+      }
+    }
+    SNK_TRY(cull_impl(&L.g, p, cur, live, nxt, max_cells, &nd, scratch, sb, st));
+    if (nxt != d_dets)
+      SNK_CUDA_CHECK(cudaMemcpyAsync(d_dets, nxt, nd * sizeof(snk_cell), cudaMemcpyDeviceToDevice, st));
+  } else {
+    if (ns > 0)
+      SNK_TRY(evolve_impl(&L.g, p, d_img, d_seeds, nullptr, first, ns, d_cells, scratch, sb, st));
+    SNK_TRY(cull_impl(&L.g, p, d_cells, ns, d_dets, max_cells, &nd, scratch, sb, st));
+  }
   *n_dets = nd;
   if (h_labels) SNK_TRY(label_impl(&L.g, p, d_dets, nd, d_labels, scratch, sb, st));
   const int64_t ncopy = std::min(nd, det_cap);

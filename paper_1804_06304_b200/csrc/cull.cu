@@ -256,6 +256,11 @@ struct CandEmit {
   snk_cell* out;
   __device__ void operator()(int64_t i, int64_t o) const { out[o] = cells[i]; }
 };
+struct IdPred {
+  const snk_cell* cells;
+  int64_t lo, hi;
+  __device__ bool operator()(int64_t i) const { return cells[i].id >= lo && cells[i].id < hi; }
+};
 struct InPred {
   const int* status;
   __device__ bool operator()(int64_t p) const { return status[p] == IN; }
@@ -406,6 +411,24 @@ int32_t compact_impl(const snk_params* p, const snk_cell* d_cells, int64_t n, sn
   SNK_TRY(compact(n, CandPred{d_cells, (float)p->e0}, CandEmit{d_cells, d_out}, cap, counts, offsets,
                   n_out, st));
   if (*n_out > cap) return fail(SNK_CAPACITY, "candidate buffer too small");
+  return SNK_OK;
+}
+
+int32_t select_ids_impl(const snk_cell* d_cells, int64_t n, int64_t id_lo, int64_t id_hi,
+                        snk_cell* d_out, int64_t cap, int64_t* n_out, void* d_ws, size_t ws_bytes,
+                        cudaStream_t st) {
+  if (n == 0) {
+    *n_out = 0;
+    return SNK_OK;
+  }
+  Carve cv(d_ws, ws_bytes);
+  const int64_t nb = ceil_div(n, 1024);
+  int* counts = cv.take<int>(nb);
+  int64_t* offsets = cv.take<int64_t>(nb + 1);
+  if (cv.overflow || !d_ws) return fail(SNK_CAPACITY, "workspace too small for compaction");
+  SNK_TRY(compact(n, IdPred{d_cells, id_lo, id_hi}, CandEmit{d_cells, d_out}, cap, counts, offsets,
+                  n_out, st));
+  if (*n_out > cap) return fail(SNK_CAPACITY, "output buffer too small");
   return SNK_OK;
 }
 

@@ -17,7 +17,11 @@ Exchange steps (the only ones the method has):
       crosses slab boundaries);
   labels stay distributed (each rank labels its own planes).
 Cells never interact during evolution, so nothing is exchanged per
-iteration.
+iteration — except with periodic culling (cull_every = k > 0, G25):
+  N6  at every checkpoint (after iterations k, 2k, ... < T) the E0 candidates
+      are all-gathered, every rank runs the same cull, and each rank keeps the
+      survivors it owns (its id range) — the per-checkpoint exchange of
+      boundary-cell records, results still bit-identical to one GPU.
 """
 from __future__ import annotations
 
@@ -144,14 +148,26 @@ def allgather_records(rec: torch.Tensor, count: int, device, group=None, rec_byt
     return allrec, sum(counts), counts
 
 
+def checkpoints(T: int, k: int) -> list:
+    """Periodic-culling segments (G25): [1, k], [k+1, 2k], ..., the last one
+    ending at T + 1; a checkpoint cull after each but the last."""
+    if k <= 0 or k >= T:
+        return [(1, T + 1)]
+    ends = list(range(k, T, k)) + [T + 1]
+    return list(zip([1] + [e + 1 for e in ends[:-1]], ends))
+
+
 class SlabRun:
     """One rank's share of one step: N1 -> a2/a3 -> a4 -> N2 -> a5/a6 -> a7
     (compact, N3, cull) -> a8.  `backend` supplies the per-stage compute:
     CudaBackend (libsnk) in production; the tests plug in the CPU oracle to check
-    the decomposition logic with gloo."""
+    the decomposition logic with gloo.  cull_every > 0: periodic culling with
+    the N6 exchange at every checkpoint (T = max_iters)."""
 
-    def __init__(self, plan: SlabPlan, backend, device, group=None):
+    def __init__(self, plan: SlabPlan, backend, device, group=None, cull_every: int = 0,
+                 max_iters: int = 0):
         self.plan, self.be, self.device, self.group = plan, backend, device, group
+        self.cull_every, self.T = cull_every, max_iters
 
     def step(self, own_raw: torch.Tensor, ev=None) -> dict:
         """ev: optional pair of CUDA events recorded around a5/a6 (bench)."""
@@ -163,14 +179,26 @@ class SlabRun:
         id_base = sum(counts[:pl.rank])
         if ev is not None:
             ev[0].record()
-        cells = self.be.evolve(pl, smooth, seeds, ns, id_base)          # a5/a6
+        live = ns
+        if self.cull_every > 0:
+            cells = self.be.init_cells(pl, seeds, ns, id_base)
+            segs = checkpoints(self.T, self.cull_every)
+            for i, (a, b) in enumerate(segs):
+                cells = self.be.evolve_range(pl, smooth, cells, live, a, b)    # a5 segment
+                if i + 1 < len(segs):                                           # checkpoint
+                    cand, nc = self.be.compact(cells, live)
+                    allc, ntot, _ = allgather_records(cand, nc, self.device, self.group)   # N6
+                    surv, nsurv = self.be.cull(pl, allc, ntot)
+                    cells, live = self.be.select_ids(surv, nsurv, id_base, id_base + ns)
+        else:
+            cells = self.be.evolve(pl, smooth, seeds, ns, id_base)      # a5/a6
         if ev is not None:
             ev[1].record()
-        cand, nc = self.be.compact(cells, ns)                           # a7: E0
+        cand, nc = self.be.compact(cells, live)                         # a7: E0
         allc, ntot, _ = allgather_records(cand, nc, self.device, self.group)   # N3
         dets, nd = self.be.cull(pl, allc, ntot)                         # a7: overlap
         labels = self.be.label(pl, dets, nd)                            # a8
-        return {"n_seeds": ns, "id_base": id_base, "n_total": sum(counts), "cells": cells,
+        return {"n_seeds": ns, "n_live": live, "id_base": id_base, "n_total": sum(counts), "cells": cells,
                 "seeds": seeds, "dets": dets, "n_dets": nd, "labels": labels, "smooth": smooth}
 
 
@@ -211,6 +239,19 @@ class CudaBackend:
             self.snk.snk_evolve(self.grid, self.p, img, seeds, None, id_base, n, self.cells, None)
         return self.cells
 
+    def init_cells(self, pl, seeds, n, id_base):
+        self.snk.snk_cells_init(self.p, seeds, None, id_base, n, self.cells)
+        return self.cells
+
+    def evolve_range(self, pl, smooth, cells, n, it0, it1):
+        img = self.grad if self.p.image_term == self.snk.IMAGE_GRADMAG else smooth
+        self.snk.snk_evolve_range(self.grid, self.p, img, cells, n, it0, it1, None)
+        return cells
+
+    def select_ids(self, recs, n, id_lo, id_hi):
+        nl = self.snk.snk_select_ids(recs, n, id_lo, id_hi, self.cells, self.max_cells, self.ws)
+        return self.cells, nl
+
     def compact(self, cells, n):
         return self.cand, self.snk.snk_compact_candidates(self.p, cells, n, self.cand, self.max_cells,
                                                           self.ws)
@@ -247,7 +288,7 @@ def bench_rank(args, cfg):
     else:
         tdist.init_process_group(backend)
     assert tuple(cfg.iso_n) == tuple(cfg.n), "the slab driver takes isotropic volumes"
-    p = pipeline.params_for(cfg, image_term=snk.IMAGE_INTENSITY)
+    p = pipeline.params_for(cfg, image_term=snk.IMAGE_INTENSITY, cull_every=getattr(args, "cull_every", 0))
     plan = plan_slabs(cfg.n, world, rank, p)
     z0, z1 = plan.own
     nown = (z1 - z0) * cfg.n[0] * cfg.n[1]
@@ -257,7 +298,8 @@ def bench_rank(args, cfg):
     synth.generate_into_ptr(cfg, h_raw.data_ptr(), z0, z1)
     own = torch.empty(h_raw.shape, dtype=torch.uint16, device="cuda")
     own.copy_(h_raw)
-    run = SlabRun(plan, be, torch.device("cuda", local_rank))
+    run = SlabRun(plan, be, torch.device("cuda", local_rank), cull_every=p.cull_every,
+                  max_iters=p.max_iters)
     for _ in range(args.warmup):
         r = run.step(own)
     torch.cuda.synchronize()

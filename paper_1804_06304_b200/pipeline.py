@@ -72,6 +72,8 @@ class Pipeline:
             ws = max(ws, 2 * nvox * 2 + 4096)
         self.ws = torch.empty(ws, dtype=torch.uint8, device=dev)
         self.n_seeds = 0
+        self.n_live = 0       # records in self.cells after evolve (< n_seeds with periodic culling)
+        self.cell_iters = 0   # cell-iterations evolved (each N samples)
         self.first_id = 0
         self.n_dets = 0
 
@@ -95,12 +97,35 @@ class Pipeline:
         return self.n_seeds
 
     def evolve(self, stream=None, n: int | None = None, ids=None, id_base: int | None = None):
+        """a5 + a6; with params.cull_every > 0 the periodic-culling segments (G25)."""
         n = self.n_seeds if n is None else n
-        snk.snk_evolve(self.grid, self.params, self.image(), self.seeds, ids,
-                       self.first_id if id_base is None else id_base, n, self.cells, None, stream)
+        base = self.first_id if id_base is None else id_base
+        if self.params.cull_every > 0:
+            return self.evolve_periodic(stream, n, ids, base)
+        snk.snk_evolve(self.grid, self.params, self.image(), self.seeds, ids, base, n, self.cells, None,
+                       stream)
+        self.n_live = n
+        self.cell_iters = n * (self.params.max_iters + 1)
+
+    def evolve_periodic(self, stream=None, n=None, ids=None, id_base=0):
+        """Evolution in segments with the a7 cull after each but the last (P:326,
+        G25); afterwards self.cells holds the self.n_live surviving records."""
+        snk.snk_cells_init(self.params, self.seeds, ids, id_base, n, self.cells, stream)
+        live, cur, nxt = n, self.cells, self.dets
+        segs = snk.checkpoints(self.params.max_iters, self.params.cull_every)
+        self.cell_iters = 0
+        for i, (a, b) in enumerate(segs):
+            snk.snk_evolve_range(self.grid, self.params, self.image(), cur, live, a, b, None, stream)
+            self.cell_iters += live * (b - a + 1)
+            if i + 1 < len(segs):
+                live = snk.snk_cull(self.grid, self.params, cur, live, nxt, self.max_cells, self.ws, stream)
+                cur, nxt = nxt, cur
+        if cur is not self.cells and live:
+            self.cells[: live * 48].copy_(cur[: live * 48])
+        self.n_live = live
 
     def cull(self, stream=None) -> int:
-        self.n_dets = snk.snk_cull(self.grid, self.params, self.cells, self.n_seeds, self.dets,
+        self.n_dets = snk.snk_cull(self.grid, self.params, self.cells, self.n_live, self.dets,
                                    self.max_cells, self.ws, stream)
         return self.n_dets
 
@@ -123,6 +148,7 @@ class Pipeline:
         mark()
         self.seed(stream)
         mark()
+        self.n_live = 0
         if self.n_seeds:
             self.evolve(stream)
         mark()
@@ -139,7 +165,7 @@ class Pipeline:
 
     # ------------------------------------------------------------------ results
     def cells_np(self) -> np.ndarray:
-        return as_cells(self.cells, self.n_seeds)
+        return as_cells(self.cells, self.n_live)
 
     def dets_np(self) -> np.ndarray:
         return as_cells(self.dets, self.n_dets)

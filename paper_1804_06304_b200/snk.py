@@ -53,7 +53,7 @@ class snk_params(C.Structure):
                 ("leash", C.c_double), ("conv_tol", C.c_double), ("max_iters", C.c_int32),
                 ("n_samples", C.c_int32), ("seed_mode", C.c_int32), ("seed_window", C.c_int32),
                 ("image_term", C.c_int32), ("cta_warps", C.c_int32), ("seed_threshold", C.c_uint32),
-                ("kernel_variant", C.c_uint32), ("estimator", C.c_int32), ("_pad1", C.c_int32),
+                ("kernel_variant", C.c_uint32), ("estimator", C.c_int32), ("cull_every", C.c_int32),
                 ("seed", C.c_uint64)]
 
 
@@ -82,7 +82,10 @@ _SIGS = {
                          _vp]),
     "snk_evolve": (_i32, [_P(snk_grid), _P(snk_params), _vp, _vp, _vp, _i64, _i64, _vp, _vp, _sz,
                           _vp]),
+    "snk_cells_init": (_i32, [_P(snk_params), _vp, _vp, _i64, _i64, _vp, _vp]),
+    "snk_evolve_range": (_i32, [_P(snk_grid), _P(snk_params), _vp, _vp, _i64, _i32, _i32, _vp, _sz, _vp]),
     "snk_compact_candidates": (_i32, [_P(snk_params), _vp, _i64, _vp, _i64, _P(_i64), _vp, _sz, _vp]),
+    "snk_select_ids": (_i32, [_vp, _i64, _i64, _i64, _vp, _i64, _P(_i64), _vp, _sz, _vp]),
     "snk_cull": (_i32, [_P(snk_grid), _P(snk_params), _vp, _i64, _vp, _i64, _P(_i64), _vp, _sz, _vp]),
     "snk_label": (_i32, [_P(snk_grid), _P(snk_params), _vp, _i64, _vp, _vp, _sz, _vp]),
     "snk_run_workspace_bytes": (_i32, [_i32, _vp, _vp, _P(snk_params), _i64, _P(_sz)]),
@@ -213,11 +216,38 @@ def snk_evolve(g, p, d_image, d_seeds, d_ids, id_base, n, d_cells, d_ws, stream=
                            _stream(stream)), "snk_evolve")
 
 
+def snk_cells_init(p, d_seeds, d_ids, id_base, n, d_cells, stream=None):
+    _check(_lib.snk_cells_init(C.byref(p), _ptr(d_seeds), _ptr(d_ids), id_base, n, _ptr(d_cells),
+                               _stream(stream)), "snk_cells_init")
+
+
+def snk_evolve_range(g, p, d_image, d_cells, n, it0, it1, d_ws, stream=None):
+    _check(_lib.snk_evolve_range(C.byref(g), C.byref(p), _ptr(d_image), _ptr(d_cells), n, it0, it1,
+                                 _ptr(d_ws), _nbytes(d_ws) if d_ws is not None else 0, _stream(stream)),
+           "snk_evolve_range")
+
+
+def checkpoints(T: int, k: int):
+    """Periodic-culling segments (G25; the library's own list in snk_run): [1, k],
+    [k+1, 2k], ..., the last ending at T + 1; a cull after each but the last."""
+    if k <= 0 or k >= T:
+        return [(1, T + 1)]
+    ends = list(range(k, T, k)) + [T + 1]
+    return list(zip([1] + [e + 1 for e in ends[:-1]], ends))
+
+
 def snk_compact_candidates(p, d_cells, n, d_out, cap, d_ws, stream=None) -> int:
     out = C.c_int64()
     _check(_lib.snk_compact_candidates(C.byref(p), _ptr(d_cells), n, _ptr(d_out), cap, C.byref(out),
                                        _ptr(d_ws), _nbytes(d_ws), _stream(stream)),
            "snk_compact_candidates")
+    return out.value
+
+
+def snk_select_ids(d_cells, n, id_lo, id_hi, d_out, cap, d_ws, stream=None) -> int:
+    out = C.c_int64()
+    _check(_lib.snk_select_ids(_ptr(d_cells), n, id_lo, id_hi, _ptr(d_out), cap, C.byref(out), _ptr(d_ws),
+                               _nbytes(d_ws), _stream(stream)), "snk_select_ids")
     return out.value
 
 
@@ -265,7 +295,7 @@ def make_params(r0=10.0, *, delta_R=2.0, eps0=0.5, e0=-3.0, sigma=1.0, intensity
                 max_step=1.0, r_min=1.0, r_max=None, leash=None, conv_tol=1e-3, max_iters=400,
                 n_samples=1024, seed_mode=SEED_MAXIMA, seed_window=4, image_term=IMAGE_INTENSITY,
                 cta_warps=0, seed_threshold=70 * 257, seed=1804063040,
-                kernel_variant=0, estimator=EST_MC) -> snk_params:
+                kernel_variant=0, estimator=EST_MC, cull_every=0) -> snk_params:
     """Defaults: DESIGN.md §3 (readings G2-G9, G18, G20)."""
     p = snk_params()
     p.r0, p.delta_R, p.eps0, p.e0, p.sigma = r0, delta_R, eps0, e0, sigma
@@ -277,5 +307,6 @@ def make_params(r0=10.0, *, delta_R=2.0, eps0=0.5, e0=-3.0, sigma=1.0, intensity
     p.seed_threshold = seed_threshold
     p.kernel_variant = kernel_variant
     p.estimator = estimator
+    p.cull_every = cull_every
     p.seed = seed & 0xFFFFFFFFFFFFFFFF
     return p

@@ -56,6 +56,23 @@ class OracleBackend:
                               n_global=pl.n)
         return torch.from_numpy(_to_rec(cells).view(np.uint8).copy())
 
+    def init_cells(self, pl, seeds, n, id_base):
+        return torch.from_numpy(_to_rec(oracle.init_cells(_params(), seeds, ids=id_base + np.arange(n)))
+                                .view(np.uint8).copy())
+
+    def evolve_range(self, pl, B, cells, n, it0, it1):
+        r = cells.numpy().view(REC)[:n]
+        o = np.zeros(n, oracle.CELL_DTYPE)
+        o["c"], o["R"], o["E"], o["seed"] = r["c"], r["R"], r["energy"], r["seed"]
+        o["flags"], o["iters"], o["id"] = r["flags"], r["iters"], r["id"]
+        o = oracle.evolve_range(B, _params(), o, it0, it1, org=(0, 0, pl.buf[0]), n_global=pl.n)
+        return torch.from_numpy(_to_rec(o).view(np.uint8).copy())
+
+    def select_ids(self, recs, n, lo, hi):
+        r = recs.numpy().view(REC)[:n]
+        keep = r[(r["id"] >= lo) & (r["id"] < hi)]
+        return torch.from_numpy(keep.view(np.uint8).copy()), len(keep)
+
     def compact(self, cells, n):
         r = cells.numpy().view(REC)[:n]
         keep = r[(r["energy"] <= -3.0) & ((r["flags"] & (oracle.COLLAPSED | oracle.RMAX)) == 0)]
@@ -71,18 +88,19 @@ class OracleBackend:
         return oracle.label(pl.n, 3, r["c"], r["R"], z0=pl.own[0], nz=pl.own[1] - pl.own[0])
 
 
-def _worker(rank, world, port, q):
+def _worker(rank, world, port, q, k=0):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     tdist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         raw = synth.generate(CFG)
         plan = D.plan_slabs(CFG.n, world, rank, P)
         own = torch.from_numpy(raw[plan.own[0]:plan.own[1]].copy())
-        out = D.SlabRun(plan, OracleBackend(), torch.device("cpu")).step(own)
+        out = D.SlabRun(plan, OracleBackend(), torch.device("cpu"), cull_every=k,
+                        max_iters=CFG.max_iters).step(own)
         # the halo exchange reproduced exactly the planes of the full volume
         local = D.exchange_halo(plan, own)
         assert np.array_equal(local.numpy(), raw[plan.buf[0]:plan.buf[1]])
-        q.put((rank, out["seeds"], out["cells"].numpy()[: out["n_seeds"] * 48].copy(),
+        q.put((rank, out["seeds"], out["cells"].numpy()[: out["n_live"] * 48].copy(),
                out["dets"].numpy()[: out["n_dets"] * 48].copy(), out["labels"], out["id_base"]))
     finally:
         tdist.destroy_process_group()
@@ -134,3 +152,45 @@ def test_plan_covers_reach():
             assert pl.buf[0] == max(z0 - 59, 0) and pl.buf[1] == min(z1 + 59, 512)
     assert sum(D.slab_bounds(512, 8, r)[1] - D.slab_bounds(512, 8, r)[0] for r in range(8)) == 512
     assert [D.slab_bounds(10, 3, r) for r in range(3)] == [(0, 4), (4, 7), (7, 10)]
+
+
+def test_slabs_periodic_culling_bit_identical():
+    """Periodic culling (G25) on 2 ranks: the N6 checkpoint exchange + the same
+    deterministic cull on every rank + ownership by id range give the live cells,
+    detections and labels of a single-process run of the same segments."""
+    k, world = 15, 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q, k)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=600) for _ in range(world)], key=lambda t: t[0])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    raw = synth.generate(CFG)
+    B = oracle.blur(raw, 3, 1.0)
+    seeds = oracle.seeds_maxima(B, 3, P.seed_window, CFG.seed_threshold)
+    be, pl = OracleBackend(), D.plan_slabs(CFG.n, 1, 0, P)
+    cells, live = be.init_cells(pl, seeds, len(seeds), 0), len(seeds)
+    segs = D.checkpoints(CFG.max_iters, k)
+    assert segs == [(1, 15), (16, 30), (31, 41)]
+    for i, (a, b) in enumerate(segs):
+        cells = be.evolve_range(pl, B, cells, live, a, b)
+        if i + 1 < len(segs):
+            cand, nc = be.compact(cells, live)
+            cells, live = be.cull(pl, cand, nc)
+    cells = cells.numpy().view(REC)[:live]
+    cells = cells[np.argsort(cells["id"], kind="stable")]
+    cand = cells[(cells["energy"] <= -3.0) & ((cells["flags"] & (oracle.COLLAPSED | oracle.RMAX)) == 0)]
+    kk = oracle.cull(cand["c"], cand["R"], cand["energy"], cand["flags"], cand["id"], 3, -3.0)
+    dets = cand[kk]
+    labels = oracle.label(CFG.n, 3, dets["c"], dets["R"])
+    assert len(seeds) > live > 5 and len(dets) > 5
+    got = np.concatenate([r[2] for r in res]).view(REC)
+    got = got[np.argsort(got["id"], kind="stable")]
+    assert got.tobytes() == cells.tobytes()
+    for r in res:
+        assert r[3].tobytes() == dets.tobytes()
+    assert np.array_equal(np.concatenate([r[4] for r in res]), labels)

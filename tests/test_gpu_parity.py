@@ -433,6 +433,82 @@ def test_evolve_grid_2d_and_slab(gpu):
     assert pipeline.as_cells(cells, len(sel)).tobytes() == full[sel].tobytes()
 
 
+# ---------------------------------------------------------------- periodic culling
+
+
+def test_evolve_range_resumes_bit_exactly(gpu):
+    """Segments 1..a, a+1..b, ..., ..T+1 of snk_evolve_range from the records give
+    records bit-identical to one snk_evolve, for the brick, warp and grid kernels."""
+    torch, snk, pipeline = gpu
+    cfg = synth.CONFIGS["C1"].with_(max_iters=90)
+    P, raw, p = _gpu_smooth_seeds(torch, snk, pipeline, cfg)
+    n = P.n_seeds
+    for kw in (dict(), dict(kernel_variant=1, cta_warps=2), dict(estimator=snk.EST_GRID)):
+        p = pipeline.params_for(cfg, **kw)
+        P.params = p
+        P.evolve()
+        torch.cuda.synchronize()
+        one = P.cells_np()
+        cells = torch.empty(n * 48, dtype=torch.uint8, device="cuda")
+        snk.snk_cells_init(p, P.seeds, None, 0, n, cells)
+        for a, b in [(1, 1), (2, 40), (41, 90), (91, 91)]:
+            snk.snk_evolve_range(P.grid, p, P.smooth, cells, n, a, b, None)
+        torch.cuda.synchronize()
+        assert pipeline.as_cells(cells, n).tobytes() == one.tobytes(), kw
+
+
+def test_periodic_culling_c1_vs_oracle(gpu):
+    """cull_every = 50 on C1: the GPU (pipeline and snk_run) keeps the same cells
+    at every checkpoint as the oracle (E, c, R within tolerance), and the final
+    detections match; every checkpoint cull is bit-exact given the GPU records."""
+    torch, snk, pipeline = gpu
+    cfg = synth.CONFIGS["C1"]
+    k = 50
+    P, raw, p = _gpu_smooth_seeds(torch, snk, pipeline, cfg, cull_every=k)
+    B = oracle.blur(raw, 3, 1.0)
+    op = _ora_params(cfg)
+    seeds = P.seeds_np()
+    # stage by stage: GPU segments, oracle cull of the GPU records == GPU cull
+    n = P.n_seeds
+    cur = torch.empty(n * 48, dtype=torch.uint8, device="cuda")
+    nxt = torch.empty(n * 48, dtype=torch.uint8, device="cuda")
+    snk.snk_cells_init(p, P.seeds, None, 0, n, cur)
+    ocells = oracle.init_cells(op, seeds)
+    live = n
+    for i, (a, b) in enumerate(snk.checkpoints(cfg.max_iters, k)):
+        snk.snk_evolve_range(P.grid, p, P.smooth, cur, live, a, b, None)
+        ocells = oracle.evolve_range(B, op, ocells, a, b)
+        torch.cuda.synchronize()
+        g = pipeline.as_cells(cur, live)
+        o = ocells[np.argsort(ocells["id"])]
+        gs = g[np.argsort(g["id"])]
+        _assert_cells_close(gs, o, f"segment {a}..{b}")
+        if b > cfg.max_iters:
+            break
+        live = snk.snk_cull(P.grid, p, cur, live, nxt, n, P.ws)
+        keep = oracle.cull(g["c"], g["R"], g["energy"], g["flags"], g["id"], 3, op.e0)
+        assert pipeline.as_cells(nxt, live).tobytes() == g[keep].tobytes(), f"checkpoint {b}"
+        okeep = oracle.cull(ocells["c"].astype(np.float32), ocells["R"].astype(np.float32),
+                            ocells["E"].astype(np.float32), ocells["flags"], ocells["id"], 3, op.e0)
+        assert np.array_equal(np.sort(ocells["id"][okeep]), np.sort(g["id"][keep])), f"checkpoint {b}"
+        ocells = ocells[np.sort(okeep)]
+        cur, nxt = nxt, cur
+    # the pipeline's periodic path and the end-to-end host call agree bit for bit
+    P.evolve()
+    P.cull()
+    torch.cuda.synchronize()
+    dets = P.dets_np()
+    o = oracle.evolve_periodic(B, op, seeds, k)
+    okeep = oracle.cull(o["c"].astype(np.float32), o["R"].astype(np.float32), o["E"].astype(np.float32),
+                        o["flags"], o["id"], 3, op.e0)
+    assert np.array_equal(dets["id"], o["id"][okeep]) and len(dets) == 8
+    _assert_cells_close(dets, o[okeep], "periodic detections")
+    hr = pipeline.HostRunner(3, cfg.n, p)
+    h_raw = torch.from_numpy(raw).pin_memory()
+    nd = hr.run(h_raw)
+    assert nd == len(dets) and hr.dets_np(nd).tobytes() == dets.tobytes()
+
+
 # ---------------------------------------------------------------- a7-a8, stage-isolated and end to end
 
 
