@@ -100,6 +100,20 @@ def workload_name(cfg):
     return f"{cfg.name}: synthetic {dims}{aniso}, {nn} nuclei, N={cfg.n_samples}, T={cfg.max_iters}"
 
 
+def ncu_traffic(config: str, kernel: str = "evolve_brick_kernel"):
+    """DRAM bytes (dram__bytes_read.sum + dram__bytes_write.sum) per launch of the
+    dominant kernel from the committed `ncu --set full` capture of this config
+    (profiles/traffic.json, written from the .ncu-rep by scripts/ncu_traffic.py),
+    or None when no capture of this config exists."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            t = json.load(f)
+        e = t[config][kernel]
+        return e["dram_bytes_per_launch"], e["source"]
+    except (OSError, KeyError, ValueError):
+        return None, None
+
+
 # ---------------------------------------------------------------- CPU oracle sample
 def crop_geometry(cfg, target_cells: int):
     """Crop box (lo, hi) and its seeded interior (ilo, ihi) for about target_cells cells."""
@@ -217,8 +231,11 @@ def run_ours(args):
     peak = SMS * LANES_PER_SM * f_clk / 1e9            # G lane-ops/s
     ev_s = statistics.mean(evolve_ms) / 1e3
     achieved = samples * OPS_PER_SAMPLE / ev_s / 1e9
+    traffic, traffic_src = ncu_traffic(cfg.name) if not args.cull_every else (None, None)
     roofline = {"bound": "alu", "achieved": round(achieved, 1), "peak": round(peak, 1),
-                "unit": "Glane-op/s", "frac": round(achieved / peak, 4), "traffic": None,
+                "unit": "Glane-op/s", "frac": round(achieved / peak, 4), "traffic": traffic,
+                "traffic_unit": "DRAM bytes per launch (ncu --set full)", "traffic_source": traffic_src,
+                "algorithmic_gather_bytes_per_launch": samples * 16,
                 "kernel": "evolve_brick_kernel" if args.kernel_variant != 1 else "evolve_warp_kernel", "ops_per_sample": OPS_PER_SAMPLE,
                 "samples_per_s_kernel": samples / ev_s,
                 "gather_GBps": round(samples * 16 / ev_s / 1e9, 1),

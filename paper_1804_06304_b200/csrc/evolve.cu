@@ -475,17 +475,24 @@ __device__ __forceinline__ Acc2 sample_pair_fast(const EvoParams& P, const CellI
   return a;
 }
 
-// chunk_sum_dirs<D, G_BRICK_FAST, S, 8> with paired samples: the same tree,
-// ((l0 + l1) + (l2 + l3)) + ((l4 + l5) + (l6 + l7)), with the two halves in
-// the two lanes of the f32x2 sums.
-template <int D, int S>
-__device__ __forceinline__ Acc chunk8_fast_x2(const EvoParams& P, const CellIt& C, const Dir* d,
-                                              const uint16_t* brick) {
-  Acc2 l[4];
+// chunk_sum_dirs<D, G_BRICK_FAST, S, CH> (CH = 4, 8) with paired samples: the
+// same tree — for CH = 8, ((l0 + l1) + (l2 + l3)) + ((l4 + l5) + (l6 + l7)) —
+// with the two halves of the chunk in the two lanes of the f32x2 sums.
+template <int N>
+__device__ __forceinline__ Acc2 tree_sum2(const Acc2* l) {
+  if constexpr (N == 1) return l[0];
+  else return acc2_add(tree_sum2<N / 2>(l), tree_sum2<N / 2>(l + N / 2));
+}
+
+template <int D, int S, int CH>
+__device__ __forceinline__ Acc chunk_fast_x2(const EvoParams& P, const CellIt& C, const Dir* d,
+                                             const uint16_t* brick) {
+  constexpr int H = CH / 2;
+  Acc2 l[H];
 #pragma unroll
-  for (int k = 0; k < 4; ++k)
-    l[k] = sample_pair_fast<D, S>(P, C, finish_draw<D>(C, d[k]), finish_draw<D>(C, d[k + 4]), brick);
-  const Acc2 h = acc2_add(acc2_add(l[0], l[1]), acc2_add(l[2], l[3]));
+  for (int k = 0; k < H; ++k)
+    l[k] = sample_pair_fast<D, S>(P, C, finish_draw<D>(C, d[k]), finish_draw<D>(C, d[k + H]), brick);
+  const Acc2 h = tree_sum2<H>(l);
   return Acc{__fadd_rn(h.a0.x, h.a0.y), __fadd_rn(h.cx.x, h.cx.y), __fadd_rn(h.cy.x, h.cy.y),
              __fadd_rn(h.cz.x, h.cz.y), __fadd_rn(h.aR.x, h.aR.y)};
 }
@@ -982,7 +989,7 @@ __global__ void __launch_bounds__(32 * W, W == 4 ? 3 : SNK_BRICK_MINB8) evolve_b
     C.boff = bk.boff;
     if constexpr (PIPE) {
       if (mode == 0) {
-        if constexpr (CH == 8 && SNK_F32X2) part = chunk8_fast_x2<D, S>(P, C, dir, brick);
+        if constexpr ((CH == 8 || CH == 4) && SNK_F32X2) part = chunk_fast_x2<D, S, CH>(P, C, dir, brick);
         else part = chunk_sum_dirs<D, G_BRICK_FAST, S, CH>(P, C, dir, brick, halo);
       } else if (mode == 1) {
         part = chunk_sum_dirs<D, G_BRICK_CLAMP, S, CH>(P, C, dir, brick, halo);

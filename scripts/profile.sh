@@ -11,7 +11,7 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:evolve_ -s 1 -c 1 \
   -o $O/${TAG}_evolve_c3 python scripts/profile_step.py --config C3 --steps 1 --warmup 1 > $O/${TAG}_evolve_c3.log 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:evolve_ -s 1 -c 1 \
-  -o $O/${TAG}_evolve_c4 python scripts/profile_step.py --config C4 --steps 1 --warmup 1 --iters 40 > $O/${TAG}_evolve_c4.log 2>&1
+  -o $O/${TAG}_evolve_c4 python scripts/profile_step.py --config C4 --steps 1 --warmup 1 > $O/${TAG}_evolve_c4.log 2>&1
 # the volume passes on C4
 timeout 600 ncu --set full --clock-control none -k regex:"blur|gradmag|maxima|label_kernel|bits_" -s 5 -c 8 \
   -o $O/${TAG}_volume_c4 python scripts/profile_step.py --config C4 --steps 1 --warmup 1 > $O/${TAG}_volume_c4.log 2>&1
