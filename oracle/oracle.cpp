@@ -199,7 +199,7 @@ extern "C" {
 
 struct ora_params {
   double r0, delta_R, eps0, e0, iscale, max_step, r_min, r_max, leash, conv_tol;
-  int32_t max_iters, n_samples, dim, mode;   // mode 0 = Monte-Carlo, 1 = grid (Eq. 5)
+  int32_t max_iters, n_samples, dim, mode;   // mode 0 MC, 1 grid (Eq. 5), 2 MC + control variate, 3 ray march
   uint64_t seed;
 };
 
@@ -500,6 +500,11 @@ struct EnergyOut { double E, gc[3], gR; bool halo; };
 // Monte-Carlo estimate: N samples uniform in the ball of radius
 // rho_s = R + dR/2, each of weight V/N, V = ball volume.  r := t and the
 // unit vector := omega (never recomputed from k - c; §8(c) O5 step 5).
+// Control variate (mode 2, reading G21 / SURVEY §8(f) 4): I(k) is replaced by
+// I(k) - I(c).  Unbiased for the same integrals because the ball integrals of
+// S, S_R and S_r omega are all zero (the zero moment of G1, its R-derivative
+// with S(rho_s) = 0, and the symmetry of omega); on a uniform image every sum
+// is then exactly zero ("the energy is zero ... uniform intensity").
 static EnergyOut energy_mc(const Image& img, const ora_params& p, const double c[3], double R,
                            uint32_t iter, int64_t id) {
   const int d = p.dim;
@@ -507,11 +512,12 @@ static EnergyOut energy_mc(const Image& img, const ora_params& p, const double c
   const double rho_s = R + p.delta_R / 2.0;
   double A0 = 0.0, Ac[3] = {0.0, 0.0, 0.0}, AR = 0.0;
   bool halo = false;
+  const double Ic = (p.mode == 2) ? img.interp(c, &halo) : 0.0;
   for (int32_t j = 0; j < p.n_samples; ++j) {
     double om[3], t;
     mc_sample(d, (uint32_t)j, iter, id, p.seed, rho_s, om, &t);
     const double k[3] = {c[0] + t * om[0], c[1] + t * om[1], c[2] + t * om[2]};
-    const double I = img.interp(k, &halo);
+    const double I = img.interp(k, &halo) - Ic;
     double S, S_r, S_R;
     weight(t, R, p.delta_R, rho, &S, &S_r, &S_R);
     A0 += S * I;
@@ -520,6 +526,60 @@ static EnergyOut energy_mc(const Image& img, const ora_params& p, const double c
   }
   const double V = (d == 3) ? (4.0 / 3.0) * PI * rho_s * rho_s * rho_s / (double)p.n_samples
                             : PI * rho_s * rho_s / (double)p.n_samples;
+  A0 *= V; AR *= V;
+  for (int a = 0; a < 3; ++a) Ac[a] *= V;
+  const double gamma = std::pow(2.0 * R, -(double)d);
+  EnergyOut o;
+  o.E = gamma * A0;
+  for (int a = 0; a < 3; ++a) o.gc[a] = -gamma * Ac[a];
+  o.gR = gamma * (AR - ((double)d / R) * A0);
+  o.halo = halo;
+  return o;
+}
+
+// Stratified ray-march estimate (mode 3: the north_star's
+// "marches a ray"; reading G27).  The ball integral in polar form,
+//   int_ball f dV = int_{S^{d-1}} int_0^{rho_s} f(t omega) t^{d-1} dt d omega,
+// estimated with N/M rays of M = 8 stratified steps: ray j has direction
+// omega_j (the MC direction law of G10 from words 0, 1) and steps
+// t_jm = rho_s (m + u_jm) / M, m = 0..M-1, u_jm uniform (words 2 + m); its
+// Philox words are the 12 words of blocks 3j, 3j+1, 3j+2 of the cell-iteration
+// stream (words 10, 11 unused).  Each step weighs |S^{d-1}| rho_s t^{d-1} / N
+// (|S^2| = 4 pi, |S^1| = 2 pi): unbiased for every stratum and direction.
+static const int RAY_M = 8;
+static EnergyOut energy_ray(const Image& img, const ora_params& p, const double c[3], double R,
+                            uint32_t iter, int64_t id) {
+  const int d = p.dim;
+  const double rho = rho_of(d);
+  const double rho_s = R + p.delta_R / 2.0;
+  double A0 = 0.0, Ac[3] = {0.0, 0.0, 0.0}, AR = 0.0;
+  bool halo = false;
+  const int32_t rays = p.n_samples / RAY_M;
+  for (int32_t j = 0; j < rays; ++j) {
+    uint32_t x[12];
+    for (int w = 0; w < 12; ++w) x[w] = stream_word(12ull * (uint64_t)j + (uint64_t)w, iter, id, p.seed);
+    const double u0 = uniform01(x[0]), u1 = uniform01(x[1]);
+    const double phi = 2.0 * PI * u1;
+    double om[3];
+    if (d == 3) {
+      const double z = 1.0 - 2.0 * u0;
+      const double st = 2.0 * std::sqrt(u0 * (1.0 - u0));
+      om[0] = st * std::cos(phi); om[1] = st * std::sin(phi); om[2] = z;
+    } else {
+      om[0] = std::cos(phi); om[1] = std::sin(phi); om[2] = 0.0;
+    }
+    for (int m = 0; m < RAY_M; ++m) {
+      const double t = rho_s * ((double)m + uniform01(x[2 + m])) / (double)RAY_M;
+      const double k[3] = {c[0] + t * om[0], c[1] + t * om[1], c[2] + t * om[2]};
+      const double Iw = img.interp(k, &halo) * (d == 3 ? t * t : t);
+      double S, S_r, S_R;
+      weight(t, R, p.delta_R, rho, &S, &S_r, &S_R);
+      A0 += S * Iw;
+      for (int a = 0; a < 3; ++a) Ac[a] += S_r * Iw * om[a];
+      AR += S_R * Iw;
+    }
+  }
+  const double V = (d == 3 ? 4.0 * PI : 2.0 * PI) * rho_s / (double)(rays * RAY_M);
   A0 *= V; AR *= V;
   for (int a = 0; a < 3; ++a) Ac[a] *= V;
   const double gamma = std::pow(2.0 * R, -(double)d);
@@ -585,7 +645,7 @@ void ora_energy_mc(const uint16_t* v, const int64_t n[3], const int64_t org[3], 
                    const ora_params* p, const double c[3], double R, uint32_t iter, int64_t id,
                    double* out6) {
   const Image img = make_image(v, n, org, nb, p);
-  const EnergyOut o = energy_mc(img, *p, c, R, iter, id);
+  const EnergyOut o = p->mode == 3 ? energy_ray(img, *p, c, R, iter, id) : energy_mc(img, *p, c, R, iter, id);
   out6[0] = o.E; out6[1] = o.gc[0]; out6[2] = o.gc[1]; out6[3] = o.gc[2]; out6[4] = o.gR;
   out6[5] = o.halo ? 1.0 : 0.0;
 }
@@ -658,8 +718,9 @@ static void evolve_cell(const Image& img, const ora_params* p, const int64_t n[3
   uint32_t flags = cell.flags;
   double E = cell.E;
   for (int it = it0; it <= it1; ++it) {
-    const EnergyOut eo = (p->mode == 1) ? energy_grid(img, *p, c, R)
-                                        : energy_mc(img, *p, c, R, (uint32_t)it, cell.id);
+    const EnergyOut eo = (p->mode == 1)   ? energy_grid(img, *p, c, R)
+                         : (p->mode == 3) ? energy_ray(img, *p, c, R, (uint32_t)it, cell.id)
+                                          : energy_mc(img, *p, c, R, (uint32_t)it, cell.id);
     if (eo.halo) flags |= F_HALO;
     E = eo.E;
     if (it == T + 1) break;

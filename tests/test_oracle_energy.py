@@ -155,3 +155,63 @@ def test_mc_matches_grid_on_large_n(ora):
     eg = ora.energy_grid(vol, p, c, R)[0]
     em = np.mean([ora.energy_mc(vol, p, c, R, 1, i)[0] for i in range(4)])
     assert abs(em - eg) / abs(eg) < 0.05
+
+
+# ------------------------------------------- estimator variants
+
+
+def _ss_gradient(ora, vol, c, R, h=0.02):
+    """Central differences of E_ss (the continuous integral every MC variant estimates)."""
+    p = ora.Params(r0=10, dim=3)
+    g = []
+    for a in range(3):
+        d = np.zeros(3)
+        d[a] = h
+        g.append((ora.energy_ss(vol, p, np.add(c, d), R, q=6) - ora.energy_ss(vol, p, np.subtract(c, d), R, q=6)) / (2 * h))
+    g.append((ora.energy_ss(vol, p, c, R + h, q=6) - ora.energy_ss(vol, p, c, R - h, q=6)) / (2 * h))
+    return np.array(g)
+
+
+@pytest.mark.parametrize("mode", [0, 2, 3])
+def test_estimators_unbiased_energy_and_gradient(ora, mode):
+    """Plain MC (0), MC with the I(c) control variate (2) and the stratified ray
+    march (3) are unbiased for E_ss and for its gradient (finite differences of
+    E_ss): the means over 256 independent streams lie within 3.5 standard errors."""
+    vol = _smooth_ellipsoid(ora)
+    c, R = (20.6, 19.2, 20.4), 11.5
+    p = ora.Params(r0=10, dim=3, n_samples=1024, mode=mode)
+    es = np.array([ora.energy_mc(vol, p, c, R, 1, i)[:5] for i in range(256)])
+    se = es.std(axis=0, ddof=1) / math.sqrt(len(es))
+    ref = np.concatenate([[ora.energy_ss(vol, p, c, R, q=6)], _ss_gradient(ora, vol, c, R)])
+    z = (es.mean(axis=0) - ref) / se
+    assert np.all(np.abs(z) < 3.5), z
+
+
+def test_ray_march_lowers_energy_variance(ora):
+    """Stratifying the radius along each ray (G27) cuts the energy's standard
+    deviation well below plain MC at the same sample count (measured 0.20 vs 0.76)."""
+    vol = _smooth_ellipsoid(ora)
+    c, R = (20.6, 19.2, 20.4), 11.5
+    s = {}
+    for mode in (0, 3):
+        p = ora.Params(r0=10, dim=3, n_samples=1024, mode=mode)
+        s[mode] = np.std([ora.energy_mc(vol, p, c, R, 1, i)[0] for i in range(128)], ddof=1)
+    assert s[3] < 0.5 * s[0]
+
+
+def test_control_variate_exact_on_uniform_image(ora):
+    """G21: with the I(c) control variate every sum vanishes on a constant image
+    (P:93), so the energy and gradient are exactly 0 and a contour does not move
+    at all — plain MC only has zero mean there (A10)."""
+    vol = np.full((40, 40, 40), 60 * 257, np.uint16)
+    p = ora.Params(r0=10, dim=3, n_samples=256, mode=2)
+    for i in range(8):
+        assert np.all(ora.energy_mc(vol, p, (20.3, 19.7, 20.1), 10.0, 1, i)[:5] == 0.0)
+    cells = ora.evolve(vol, ora.Params(r0=10, dim=3, n_samples=256, mode=2, max_iters=100),
+                       np.array([[20.3, 19.7, 20.1]], np.float32))
+    assert np.array_equal(cells["c"][0], np.float32([20.3, 19.7, 20.1]).astype(np.float64))
+    assert cells["R"][0] == 10.0 and cells["E"][0] == 0.0
+    # plain MC does move
+    cells = ora.evolve(vol, ora.Params(r0=10, dim=3, n_samples=256, max_iters=100),
+                       np.array([[20.3, 19.7, 20.1]], np.float32))
+    assert np.max(np.abs(cells["c"][0] - np.float32([20.3, 19.7, 20.1]))) > 0.05

@@ -51,13 +51,15 @@ def _ball_volume(n, c, r0, amp=100.0, dim=3, ora=None, sigma=1.0):
     return ora.blur(v, dim, sigma)
 
 
-def test_equilibrium_radius_3d(ora):
-    """r0 = 10, dR = 2, sigma = 1: R* = 12.8493, then the oracle's MC
-    evolution of centred snakes converges to within 0.1 of it."""
+@pytest.mark.parametrize("mode", [0, 2, 3])
+def test_equilibrium_radius_3d(ora, mode):
+    """r0 = 10, dR = 2, sigma = 1: R* = 12.8493, then the oracle's
+    evolution of centred snakes converges to within 0.1 of it — plain MC (0),
+    with the control variate (2) and with the stratified ray march (3)."""
     rstar = radial_argmin(ora, lambda r: blurred_ball(r, 10.0, 1.0, 100.0), 3, lo=11, hi=14)
     assert rstar == pytest.approx(12.8493, abs=2e-3)
     vol = _ball_volume(48, (24.0, 24.0, 24.0), 10.0, ora=ora)
-    p = ora.Params(r0=10.0, n_samples=1024, dim=3)
+    p = ora.Params(r0=10.0, n_samples=1024, dim=3, mode=mode)
     seeds = np.array([[25.0, 23.0, 24.5]] * 8, np.float32)
     cells = ora.evolve(vol, p, seeds, ids=np.arange(8) * 1000 + 17)
     assert abs(cells["R"].mean() - rstar) < 0.1
