@@ -68,8 +68,17 @@ enum { SNK_IMAGE_INTENSITY = 0, SNK_IMAGE_GRADMAG = 1 };
  *                voxels k with |k - c| < R + dR/2 (unit voxel volume, I(k) read
  *                at the voxel, the radial term 0 at r = 0) — deterministic,
  *                no samples (n_samples is ignored); the baseline MC replaced
- *                ("~4X gain"). */
-enum { SNK_EST_MC = 0, SNK_EST_GRID = 1 };
+ *                ("~4X gain");
+ *   SNK_EST_MC_CV MC with the control variate I(c) subtracted from every sample
+ *                (reading G21): unbiased for the same integrals, exactly zero on a
+ *                uniform image;
+ *   SNK_EST_RAY  stratified ray march (reading G27): N/8 rays per cell-iteration,
+ *                ray j's direction from words 0, 1 of Philox blocks 3j..3j+2 and
+ *                8 steps t = rho_s (m + u_m)/8 (words 2..9), each weighted
+ *                |S^(d-1)| rho_s t^(d-1) / N.
+ *   MC_CV and RAY run in the brick kernel with 8 samples per thread:
+ *   n_samples = 256 * warps per cell (cta_warps 0 or 4: N = 1024; 8: N = 2048). */
+enum { SNK_EST_MC = 0, SNK_EST_GRID = 1, SNK_EST_MC_CV = 2, SNK_EST_RAY = 3 };
 
 /* Geometry of the (isotropic) volume and of this rank's slab (§8(e)).
  *   n[3]        global dims (x, y, z); 2D images have dim = 2 and n[2] = 1.
@@ -94,7 +103,8 @@ typedef struct snk_grid {
  *   seed_mode LATTICE | MAXIMA | GIVEN                  seed_window w, seed_threshold thr (G20)
  *   image_term INTENSITY | GRADMAG                      cta_warps warps per cell: 0 auto, 1, 2, 4, 8
  *   kernel_variant  0 auto (brick kernel when nx is even), 1 warp kernel, 2 brick kernel
- *   estimator SNK_EST_MC | SNK_EST_GRID (grid: brick kernel only, even nx)
+ *   estimator SNK_EST_MC | SNK_EST_GRID | SNK_EST_MC_CV | SNK_EST_RAY (not MC: brick
+ *             kernel only, even nx)
  *   cull_every  periodic culling ("dynamic culling", reading G25): 0 = off
  *             (the paper's end-of-run cull only); k > 0 = after iterations k, 2k, ...
  *             (< T) the live cells go through the a7 cull (E0, then the overlap
@@ -107,7 +117,7 @@ typedef struct snk_params {
   int32_t max_iters, n_samples, seed_mode, seed_window, image_term, cta_warps;
   uint32_t seed_threshold;
   uint32_t kernel_variant; /* evolve kernel: 0 auto, 1 warp (global gathers), 2 brick (shared memory) */
-  int32_t estimator;       /* SNK_EST_MC (default) or SNK_EST_GRID */
+  int32_t estimator;       /* SNK_EST_MC (default), _GRID, _MC_CV or _RAY */
   int32_t cull_every;      /* 0 off, else periodic culling every cull_every iterations (G25) */
   uint64_t seed;
 } snk_params;

@@ -84,6 +84,7 @@ struct CellIt {
   // brick: sum over axes of (2^23 + b_a) * stride_a (mod 2^32), so that the
   // brick index of magic-floored coordinates is rx + ry SX + rz SP - boff
   uint32_t boff;
+  float ic;             // SNK_EST_MC_CV: the image at the centre, I(c) (u16 units)
 };
 
 __device__ __forceinline__ float sqrt_approx(float x) {
@@ -196,15 +197,57 @@ __device__ __forceinline__ Dir dir_words(uint32_t w0, uint32_t w1, uint32_t w2) 
   return d;
 }
 
-// The distance: 3D t = rho_s cbrt(u2), 2D t = rho_s sqrt(u2).
-template <int D>
+// The distance: 3D t = rho_s cbrt(u2), 2D t = rho_s sqrt(u2);
+// the ray march (EST 3, G27): t = rho_s (m + u) / M with L = (m + u) / M.
+template <int D, int EST = 0>
 __device__ __forceinline__ Draw finish_draw(const CellIt& C, const Dir& d) {
   Draw r;
   r.ox = d.ox;
   r.oy = d.oy;
   r.oz = d.oz;
-  r.t = D == 3 ? ex2_approx(__fmaf_rn(d.L, 0.333333343f, C.lg2_rho_s)) : __fmul_rn(C.rho_s, d.L);
+  if (EST == SNK_EST_RAY) r.t = __fmul_rn(C.rho_s, d.L);
+  else r.t = D == 3 ? ex2_approx(__fmaf_rn(d.L, 0.333333343f, C.lg2_rho_s)) : __fmul_rn(C.rho_s, d.L);
   return r;
+}
+
+// The ray march's draws (G27): ray `ray` of the cell-iteration takes the 12
+// words of Philox blocks 3 ray .. 3 ray + 2: words 0, 1 give the direction
+// (the MC law, G10), words 2 + m the jitter of step m, L = (m + u) / 8.
+template <int D>
+__device__ __forceinline__ void draw_dirs_ray(const EvoParams& P, const CellIt& C, uint32_t ray, Dir* d) {
+  uint32_t a[4], b[4], c[4];
+  philox_block(P, C, 3u * ray, a);
+  philox_block(P, C, 3u * ray + 1u, b);
+  philox_block(P, C, 3u * ray + 2u, c);
+  const float u1 = u01(a[1]);
+  float sn, cs;
+  __sincosf(__fmul_rn(6.2831853071795865f, u1), &sn, &cs);
+  Dir o;
+  if (D == 3) {
+    o.oz = __fmaf_rn(-2.0f, u01(a[0]), 1.0f);
+    const float st = sqrt_approx(__fmaf_rn(-o.oz, o.oz, 1.0f));
+    o.ox = __fmul_rn(st, cs);
+    o.oy = __fmul_rn(st, sn);
+  } else {
+    o.ox = cs;
+    o.oy = sn;
+    o.oz = 0.0f;
+  }
+  const uint32_t w[8] = {a[2], a[3], b[0], b[1], b[2], b[3], c[0], c[1]};
+#pragma unroll
+  for (int m = 0; m < 8; ++m) {
+    d[m] = o;
+    d[m].L = __fmul_rn(__fadd_rn((float)m, u01(w[m])), 0.125f);
+  }
+}
+
+// The image value a sample contributes (u16 units): I(k) (MC, grid), I(k) - I(c)
+// (control variate, G21), I(k) t^(d-1) (ray march, the polar volume element).
+template <int D, int EST>
+__device__ __forceinline__ float est_value(const CellIt& C, float tri, float t) {
+  if (EST == SNK_EST_MC_CV) return __fsub_rn(tri, C.ic);
+  if (EST == SNK_EST_RAY) return __fmul_rn(tri, D == 3 ? __fmul_rn(t, t) : t);
+  return tri;
 }
 
 template <int D>
@@ -332,15 +375,16 @@ __host__ __device__ constexpr int brick_sx(int S) { return (S + 2) & ~1; }
 // Gather modes
 enum { G_GLOBAL = 0, G_GLOBAL_SLAB = 1, G_BRICK_CLAMP = 2, G_BRICK_FAST = 3 };
 
+// d-linear lookup of the image at k (u16 units), through the brick or global memory.
 template <int D, int MODE, int S>
-__device__ __forceinline__ Acc sample_leaf(const EvoParams& P, const CellIt& C, const Draw& d,
-                                           const uint16_t* brick, uint32_t& halo) {
+__device__ __forceinline__ float gather_tri(const EvoParams& P, const CellIt& C, float kx, float ky, float kz,
+                                            const uint16_t* brick, uint32_t& halo) {
   constexpr bool CLAMP = MODE != G_BRICK_FAST;
   uint32_t rx, ry, rz = kMagicBits;
-  const float fx = split_axis<CLAMP>(__fmaf_rn(d.t, d.ox, C.cx), P.fnx1, P.mx2, &rx);
-  const float fy = split_axis<CLAMP>(__fmaf_rn(d.t, d.oy, C.cy), P.fny1, P.my2, &ry);
+  const float fx = split_axis<CLAMP>(kx, P.fnx1, P.mx2, &rx);
+  const float fy = split_axis<CLAMP>(ky, P.fny1, P.my2, &ry);
   float fz = 0.0f;
-  if (D == 3) fz = split_axis<CLAMP>(__fmaf_rn(d.t, d.oz, C.cz), P.fnz1, P.mz2, &rz);
+  if (D == 3) fz = split_axis<CLAMP>(kz, P.fnz1, P.mz2, &rz);
   float v000, v100, v010, v110, v001 = 0, v101 = 0, v011 = 0, v111 = 0;
   if (MODE == G_BRICK_CLAMP || MODE == G_BRICK_FAST) {
     // brick-local index; row stride SX and plane stride SX * S are immediates
@@ -387,7 +431,15 @@ __device__ __forceinline__ Acc sample_leaf(const EvoParams& P, const CellIt& C, 
   // trilinear: x, then y, then z (G17)
   float tri = lerp(lerp(v000, v100, fx), lerp(v010, v110, fx), fy);
   if (D == 3) tri = lerp(tri, lerp(lerp(v001, v101, fx), lerp(v011, v111, fx), fy), fz);
-  return leaves(P, C, d, tri, D == 3);
+  return tri;
+}
+
+template <int D, int MODE, int S, int EST = 0>
+__device__ __forceinline__ Acc sample_leaf(const EvoParams& P, const CellIt& C, const Draw& d,
+                                           const uint16_t* brick, uint32_t& halo) {
+  const float tri = gather_tri<D, MODE, S>(P, C, __fmaf_rn(d.t, d.ox, C.cx), __fmaf_rn(d.t, d.oy, C.cy),
+                                           D == 3 ? __fmaf_rn(d.t, d.oz, C.cz) : 0.0f, brick, halo);
+  return leaves(P, C, d, est_value<D, EST>(C, tri, d.t), D == 3);
 }
 
 // ---------------------------------------------------------------- f32x2 fast path
@@ -422,7 +474,7 @@ __device__ __forceinline__ float2 split2(float2 k, uint32_t* r0, uint32_t* r1) {
   return __fadd2_rn(k, neg2(__fadd2_rn(r, bc2(-kMagic))));
 }
 
-template <int D, int S>
+template <int D, int S, int EST = 0>
 __device__ __forceinline__ Acc2 sample_pair_fast(const EvoParams& P, const CellIt& C, const Draw& d0,
                                                  const Draw& d1, const uint16_t* brick) {
   constexpr int SX = brick_sx(S), SP = SX * S;
@@ -454,6 +506,8 @@ __device__ __forceinline__ Acc2 sample_pair_fast(const EvoParams& P, const CellI
     const float2 v111 = make_float2(mag(p[SP + SX + 1]), mag(q[SP + SX + 1]));
     tri = lerp2(tri, lerp2(lerp2(v001, v101, fx), lerp2(v011, v111, fx), fy), fz);
   }
+  if (EST == SNK_EST_MC_CV) tri = __fadd2_rn(tri, bc2(-C.ic));
+  if (EST == SNK_EST_RAY) tri = __fmul2_rn(tri, D == 3 ? __fmul2_rn(t, t) : t);
   // leaves(): the saturating ramps stay scalar (FFMA.SAT), the rest is paired
   const float2 uo = make_float2(__saturatef(__fmaf_rn(d0.t, P.inv_dR, C.a)),
                                 __saturatef(__fmaf_rn(d1.t, P.inv_dR, C.a)));
@@ -484,14 +538,15 @@ __device__ __forceinline__ Acc2 tree_sum2(const Acc2* l) {
   else return acc2_add(tree_sum2<N / 2>(l), tree_sum2<N / 2>(l + N / 2));
 }
 
-template <int D, int S, int CH>
+template <int D, int S, int CH, int EST = 0>
 __device__ __forceinline__ Acc chunk_fast_x2(const EvoParams& P, const CellIt& C, const Dir* d,
                                              const uint16_t* brick) {
   constexpr int H = CH / 2;
   Acc2 l[H];
 #pragma unroll
   for (int k = 0; k < H; ++k)
-    l[k] = sample_pair_fast<D, S>(P, C, finish_draw<D>(C, d[k]), finish_draw<D>(C, d[k + H]), brick);
+    l[k] = sample_pair_fast<D, S, EST>(P, C, finish_draw<D, EST>(C, d[k]), finish_draw<D, EST>(C, d[k + H]),
+                                       brick);
   const Acc2 h = tree_sum2<H>(l);
   return Acc{__fadd_rn(h.a0.x, h.a0.y), __fadd_rn(h.cx.x, h.cx.y), __fadd_rn(h.cy.x, h.cy.y),
              __fadd_rn(h.cz.x, h.cz.y), __fadd_rn(h.aR.x, h.aR.y)};
@@ -531,12 +586,13 @@ __device__ __forceinline__ Acc tree_sum(const Acc* l) {
   }
 }
 
-template <int D, int MODE, int S, int CH>
+template <int D, int MODE, int S, int CH, int EST = 0>
 __device__ __forceinline__ Acc chunk_sum_dirs(const EvoParams& P, const CellIt& C, const Dir* d,
                                               const uint16_t* brick, uint32_t& halo) {
   Acc l[CH];
 #pragma unroll
-  for (int k = 0; k < CH; ++k) l[k] = sample_leaf<D, MODE, S>(P, C, finish_draw<D>(C, d[k]), brick, halo);
+  for (int k = 0; k < CH; ++k)
+    l[k] = sample_leaf<D, MODE, S, EST>(P, C, finish_draw<D, EST>(C, d[k]), brick, halo);
   return tree_sum<CH>(l);
 }
 
@@ -716,12 +772,14 @@ __device__ __forceinline__ CellIt cell_iter(const EvoParams& P, const CellState&
 // Energy, gradient and the clipped descent step; returns true after E_final.
 // GRID: the sums are Eq. 5's voxel sums (unit voxel volume), scaled by iscale
 // alone; MC: each sample carries V/N = (4/3 pi | pi) rho_s^d / N.
-template <int D, bool GRID = false>
+// RAY (G27): each step carries |S^(d-1)| rho_s t^(d-1) / N, the t^(d-1) already
+// in the leaves, so the sums scale by vscale rho_s.
+template <int D, bool GRID = false, int EST = 0>
 __device__ __forceinline__ bool cell_update(const EvoParams& P, CellState& s, const CellIt& C,
                                             const Acc& sum, int it) {
   const float rs = C.rho_s;
   const float vol = D == 3 ? __fmul_rn(__fmul_rn(rs, rs), rs) : __fmul_rn(rs, rs);
-  const float scale = GRID ? P.vscale : __fmul_rn(P.vscale, vol);
+  const float scale = GRID ? P.vscale : (EST == SNK_EST_RAY ? __fmul_rn(P.vscale, rs) : __fmul_rn(P.vscale, vol));
   const float A0 = __fmul_rn(sum.a0, scale);
   const float twoR = __fmul_rn(2.0f, s.R);
   const float gden = D == 3 ? __fmul_rn(__fmul_rn(twoR, twoR), twoR) : __fmul_rn(twoR, twoR);
@@ -964,10 +1022,11 @@ struct BrickCtl {
   }
 };
 
-template <int D, int W, int S, bool SLAB, int CH, int L>
+template <int D, int W, int S, bool SLAB, int CH, int L, int EST = 0>
 __global__ void __launch_bounds__(32 * W, W == 4 ? 3 : SNK_BRICK_MINB8) evolve_brick_kernel(const __grid_constant__ EvoParams P) {
   constexpr int B = CH << L;
   constexpr bool PIPE = SNK_BRICK_PIPE && L == 0;
+  static_assert(EST == 0 || (PIPE && CH == 8), "CV / RAY estimators: 8 samples per thread, pipelined draws");
   extern __shared__ __align__(16) uint16_t brick[];
   __shared__ __align__(16) float xch[2][5][W];      // [parity][component][warp]
   __shared__ float bc[4];                           // PIPE: (cx, cy, cz, R) after warp 0's update
@@ -980,21 +1039,30 @@ __global__ void __launch_bounds__(32 * W, W == 4 ? 3 : SNK_BRICK_MINB8) evolve_b
   bk.init(P);
   const uint32_t j0 = (uint32_t)((wsub * 32 + lane) * B);
   Dir dir[PIPE ? CH : 1];
-  if constexpr (PIPE) draw_dirs<D, CH>(P, cell_iter(P, s, P.it0), j0, dir);
+  if constexpr (PIPE) {
+    if constexpr (EST == SNK_EST_RAY) draw_dirs_ray<D>(P, cell_iter(P, s, P.it0), j0 / 8u, dir);
+    else draw_dirs<D, CH>(P, cell_iter(P, s, P.it0), j0, dir);
+  }
   for (int it = P.it0; it <= P.it1; ++it) {
     CellIt C = cell_iter(P, s, it);
     const float c[3] = {s.cx, s.cy, s.cz};
     const int mode = bk.prepare(brick, P, c, C.rho_s);
     Acc part;
     C.boff = bk.boff;
+    if constexpr (EST == SNK_EST_MC_CV) {
+      // I(c): the same d-linear lookup as a sample at t = 0
+      if (mode == 0) C.ic = gather_tri<D, G_BRICK_FAST, S>(P, C, C.cx, C.cy, C.cz, brick, halo);
+      else if (mode == 1) C.ic = gather_tri<D, G_BRICK_CLAMP, S>(P, C, C.cx, C.cy, C.cz, brick, halo);
+      else C.ic = gather_tri<D, SLAB ? G_GLOBAL_SLAB : G_GLOBAL, S>(P, C, C.cx, C.cy, C.cz, brick, halo);
+    }
     if constexpr (PIPE) {
       if (mode == 0) {
-        if constexpr ((CH == 8 || CH == 4) && SNK_F32X2) part = chunk_fast_x2<D, S, CH>(P, C, dir, brick);
-        else part = chunk_sum_dirs<D, G_BRICK_FAST, S, CH>(P, C, dir, brick, halo);
+        if constexpr ((CH == 8 || CH == 4) && SNK_F32X2) part = chunk_fast_x2<D, S, CH, EST>(P, C, dir, brick);
+        else part = chunk_sum_dirs<D, G_BRICK_FAST, S, CH, EST>(P, C, dir, brick, halo);
       } else if (mode == 1) {
-        part = chunk_sum_dirs<D, G_BRICK_CLAMP, S, CH>(P, C, dir, brick, halo);
+        part = chunk_sum_dirs<D, G_BRICK_CLAMP, S, CH, EST>(P, C, dir, brick, halo);
       } else {
-        part = chunk_sum_dirs<D, SLAB ? G_GLOBAL_SLAB : G_GLOBAL, S, CH>(P, C, dir, brick, halo);
+        part = chunk_sum_dirs<D, SLAB ? G_GLOBAL_SLAB : G_GLOBAL, S, CH, EST>(P, C, dir, brick, halo);
         if (threadIdx.x == 0) atomicAdd(&g_evolve_stats[1], 1ull);
       }
     } else {
@@ -1020,12 +1088,13 @@ __global__ void __launch_bounds__(32 * W, W == 4 ? 3 : SNK_BRICK_MINB8) evolve_b
       sum.cy = comp_tree<W>(xo + 2 * W);
       sum.cz = comp_tree<W>(xo + 3 * W);
       sum.aR = comp_tree<W>(xo + 4 * W);
-      if (cell_update<D>(P, s, C, sum, it)) break;
+      if (cell_update<D, false, EST>(P, s, C, sum, it)) break;
       CellIt Cn;
       Cn.p0 = s.q0 ^ (uint32_t)(it + 1);
       Cn.p1 = s.q1;
       Cn.p3 = s.q3;
-      draw_dirs<D, CH>(P, Cn, j0, dir);
+      if constexpr (EST == SNK_EST_RAY) draw_dirs_ray<D>(P, Cn, j0 / 8u, dir);
+      else draw_dirs<D, CH>(P, Cn, j0, dir);
     } else if constexpr (PIPE) {
       const bool done = it == P.T + 1;
       if (wsub == 0) {
@@ -1035,7 +1104,7 @@ __global__ void __launch_bounds__(32 * W, W == 4 ? 3 : SNK_BRICK_MINB8) evolve_b
         sum.cy = comp_tree<W>(xo + 2 * W);
         sum.cz = comp_tree<W>(xo + 3 * W);
         sum.aR = comp_tree<W>(xo + 4 * W);
-        cell_update<D>(P, s, C, sum, it);
+        cell_update<D, false, EST>(P, s, C, sum, it);
         if (lane == 0) { bc[0] = s.cx; bc[1] = s.cy; bc[2] = s.cz; bc[3] = s.R; }
       }
       if (done) break;
@@ -1043,7 +1112,8 @@ __global__ void __launch_bounds__(32 * W, W == 4 ? 3 : SNK_BRICK_MINB8) evolve_b
       Cn.p0 = s.q0 ^ (uint32_t)(it + 1);
       Cn.p1 = s.q1;
       Cn.p3 = s.q3;
-      draw_dirs<D, CH>(P, Cn, j0, dir);
+      if constexpr (EST == SNK_EST_RAY) draw_dirs_ray<D>(P, Cn, j0 / 8u, dir);
+      else draw_dirs<D, CH>(P, Cn, j0, dir);
       __syncthreads();
       if (wsub != 0) { s.cx = bc[0]; s.cy = bc[1]; s.cz = bc[2]; s.R = bc[3]; }
     } else {
@@ -1159,9 +1229,9 @@ int32_t launch_warp(const EvoParams& P, cudaStream_t st) {
   return SNK_OK;
 }
 
-template <int D, int W, int S, bool SLAB, int CH, int L>
+template <int D, int W, int S, bool SLAB, int CH, int L, int EST = 0>
 int32_t launch_brick(const EvoParams& P, cudaStream_t st) {
-  auto k = evolve_brick_kernel<D, W, S, SLAB, CH, L>;
+  auto k = evolve_brick_kernel<D, W, S, SLAB, CH, L, EST>;
   const int smem = (D == 3 ? brick_sx(S) * S * S : brick_sx(S) * S) * 2;
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
@@ -1366,6 +1436,30 @@ int32_t evolve_impl(const snk_grid* g, const snk_params* p, const uint16_t* d_im
     P.vscale = (float)p->intensity_scale;
     if (D == 3) return slab ? launch_grid<3, 8, kS3, true>(P, st) : launch_grid<3, 8, kS3, false>(P, st);
     return launch_grid<2, 8, 64, false>(P, st);
+  }
+  if (p->estimator == SNK_EST_MC_CV || p->estimator == SNK_EST_RAY) {
+    // brick kernel with pipelined draws, 8 samples (one ray) per thread
+    const int W = p->cta_warps > 0 ? p->cta_warps : 4;
+    if (g->n[0] % 2 != 0 || (reinterpret_cast<uintptr_t>(d_image) & 3) != 0 || p->kernel_variant == 1 ||
+        !(W == 4 || W == 8) || p->n_samples != 8 * 32 * W)
+      return fail(SNK_CONFIG, "the CV / ray estimators need the brick kernel (even nx) with n_samples = 256 * warps "
+                              "per cell (4 warps: N = 1024, 8 warps: N = 2048)");
+    if (p->estimator == SNK_EST_RAY) {
+      const double pi = 3.14159265358979323846;
+      P.vscale = (float)(p->intensity_scale * (D == 3 ? 4.0 * pi : 2.0 * pi) / (double)p->n_samples);
+    }
+    constexpr int CV = SNK_EST_MC_CV, RY = SNK_EST_RAY;
+    const bool ray = p->estimator == SNK_EST_RAY;
+    if (D == 3) {
+      if (W == 4) {
+        if (slab) return ray ? launch_brick<3, 4, kS3, true, 8, 0, RY>(P, st) : launch_brick<3, 4, kS3, true, 8, 0, CV>(P, st);
+        return ray ? launch_brick<3, 4, kS3, false, 8, 0, RY>(P, st) : launch_brick<3, 4, kS3, false, 8, 0, CV>(P, st);
+      }
+      if (slab) return ray ? launch_brick<3, 8, kS3, true, 8, 0, RY>(P, st) : launch_brick<3, 8, kS3, true, 8, 0, CV>(P, st);
+      return ray ? launch_brick<3, 8, kS3, false, 8, 0, RY>(P, st) : launch_brick<3, 8, kS3, false, 8, 0, CV>(P, st);
+    }
+    if (W == 4) return ray ? launch_brick<2, 4, 64, false, 8, 0, RY>(P, st) : launch_brick<2, 4, 64, false, 8, 0, CV>(P, st);
+    return ray ? launch_brick<2, 8, 64, false, 8, 0, RY>(P, st) : launch_brick<2, 8, 64, false, 8, 0, CV>(P, st);
   }
   // kernel choice: 0 auto, 1 warp (global gathers), 2 brick (shared memory)
   const uint32_t variant = p->kernel_variant;

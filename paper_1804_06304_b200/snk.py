@@ -25,7 +25,7 @@ F_CONVERGED, F_COLLAPSED, F_RMAX, F_DOMAIN, F_LEASHED, F_CULLED_E0, F_CULLED_OVE
     1, 2, 4, 8, 16, 32, 64, 128)
 SEED_LATTICE, SEED_MAXIMA, SEED_GIVEN = 0, 1, 2
 IMAGE_INTENSITY, IMAGE_GRADMAG = 0, 1
-EST_MC, EST_GRID = 0, 1
+EST_MC, EST_GRID, EST_MC_CV, EST_RAY = 0, 1, 2, 3
 
 
 class SNKError(RuntimeError):

@@ -433,6 +433,59 @@ def test_evolve_grid_2d_and_slab(gpu):
     assert pipeline.as_cells(cells, len(sel)).tobytes() == full[sel].tobytes()
 
 
+# ---------------------------------------------------------------- CV and ray-march estimators (§8(f) 3-4)
+
+
+@pytest.mark.parametrize("est,mode,W,N", [("EST_MC_CV", 2, 4, 1024), ("EST_RAY", 3, 4, 1024),
+                                         ("EST_RAY", 3, 8, 2048)])
+def test_evolve_estimator_variants(gpu, est, mode, W, N):
+    """Control-variate MC (G21) and the stratified ray march (G27) vs the
+    oracle's modes 2 and 3 (same Philox words, fp32 vs fp64); a z-slab buffer
+    gives bit-identical cells; the 2D mode on a C2 crop."""
+    torch, snk, pipeline = gpu
+    e = getattr(snk, est)
+    cfg = synth.CONFIGS["C1"].with_(n_samples=N, max_iters=200)
+    P, raw, p = _gpu_smooth_seeds(torch, snk, pipeline, cfg, estimator=e, cta_warps=W)
+    P.evolve()
+    torch.cuda.synchronize()
+    g = P.cells_np()
+    B = oracle.blur(raw, 3, 1.0)
+    o = oracle.evolve(B, _ora_params(cfg, mode=mode), P.seeds_np(), ids=np.arange(P.n_seeds))
+    _assert_cells_close(g, o, est)
+    sel = np.nonzero(P.seeds_np()[:, 2] < 20)[0]
+    z1 = 20 + int(np.ceil(2 * cfg.r0 + 2 * cfg.r0 + 2 + 2))
+    gs = snk.make_grid(3, (64, 64, 64), z_lo=0, nz_buf=z1, own=(0, 20))
+    cells = torch.empty(len(sel) * 48, dtype=torch.uint8, device="cuda")
+    snk.snk_evolve(gs, p, P.smooth[:z1].contiguous(), P.seeds[sel].contiguous(),
+                   _t(torch, sel.astype(np.int64)), 0, len(sel), cells, None)
+    torch.cuda.synchronize()
+    assert pipeline.as_cells(cells, len(sel)).tobytes() == g[sel].tobytes()
+    if W == 4:
+        c2 = synth.CONFIGS["C2"]
+        sub = np.ascontiguousarray(synth.generate(c2)[0][:200, :256])
+        c2 = c2.with_(n=(256, 200, 1), max_iters=150, n_samples=N)
+        P = pipeline.Pipeline(2, c2.n, pipeline.params_for(c2, estimator=e))
+        P.upload(sub[None])
+        P.preprocess()
+        P.seed()
+        P.evolve()
+        torch.cuda.synchronize()
+        o = oracle.evolve(oracle.blur(sub[None], 2, 1.0), _ora_params(c2, mode=mode), P.seeds_np(),
+                          ids=np.arange(P.n_seeds))
+        assert P.n_seeds > 3
+        _assert_cells_close(P.cells_np(), o, est + " 2D")
+
+
+def test_estimator_variant_config_errors(gpu):
+    torch, snk, pipeline = gpu
+    cfg = synth.CONFIGS["C1"]
+    P, raw, p = _gpu_smooth_seeds(torch, snk, pipeline, cfg)
+    P.params = pipeline.params_for(cfg, estimator=snk.EST_RAY)   # N = 256: not 256 * warps
+    with pytest.raises(snk.SNKError) as ei:
+        P.evolve()
+    assert ei.value.status == snk.CONFIG
+
+
 # ---------------------------------------------------------------- periodic culling (SURVEY §8(f) 2, G25)
 
 
