@@ -35,6 +35,10 @@ UNIT = "ray-samples/s"
 # uniforms 6, direction + radius 12 (5 SFU), position 3, d-linear gather 8 loads + 26 ALU,
 # weights S, S_r, S_R 15, leaves 6, tree adds 5  ->  111 lane-ops per sample.
 OPS_PER_SAMPLE = 111
+# the estimator variants: control variate +1 (the subtraction);
+# ray march (G27): Philox 3 blocks per 8-step ray 15, uniforms 2.5, direction per
+# ray 1.25, step t 3, position 3, gather 34, t^2 weight 2, S 15, leaves 11 -> 87
+OPS_BY_ESTIMATOR = {"mc": OPS_PER_SAMPLE, "cv": OPS_PER_SAMPLE + 1, "ray": 87}
 SMS = 148
 LANES_PER_SM = 128
 
@@ -173,7 +177,8 @@ def run_ours(args):
     torch.cuda.set_device(local_rank)
     from paper_1804_06304_b200 import pipeline, snk
     p = pipeline.params_for(cfg, image_term=snk.IMAGE_INTENSITY, cta_warps=args.cta_warps,
-                            kernel_variant=args.kernel_variant, cull_every=args.cull_every)
+                            kernel_variant=args.kernel_variant, cull_every=args.cull_every,
+                            estimator={"mc": snk.EST_MC, "cv": snk.EST_MC_CV, "ray": snk.EST_RAY}[args.estimator])
     P = pipeline.Pipeline(cfg.dim, cfg.n, p, spacing=cfg.spacing, gradmag=True)
     h_raw = torch.empty((cfg.n[2], cfg.n[1], cfg.n[0]), dtype=torch.uint16, pin_memory=True)
     t = time.perf_counter()
@@ -230,13 +235,14 @@ def run_ours(args):
     f_clk = (clocks["sm_max_mhz"] or 1965.0) * 1e6
     peak = SMS * LANES_PER_SM * f_clk / 1e9            # G lane-ops/s
     ev_s = statistics.mean(evolve_ms) / 1e3
-    achieved = samples * OPS_PER_SAMPLE / ev_s / 1e9
+    ops = OPS_BY_ESTIMATOR[args.estimator]
+    achieved = samples * ops / ev_s / 1e9
     traffic, traffic_src = ncu_traffic(cfg.name) if not args.cull_every else (None, None)
     roofline = {"bound": "alu", "achieved": round(achieved, 1), "peak": round(peak, 1),
                 "unit": "Glane-op/s", "frac": round(achieved / peak, 4), "traffic": traffic,
                 "traffic_unit": "DRAM bytes per launch (ncu --set full)", "traffic_source": traffic_src,
                 "algorithmic_gather_bytes_per_launch": samples * 16,
-                "kernel": "evolve_brick_kernel" if args.kernel_variant != 1 else "evolve_warp_kernel", "ops_per_sample": OPS_PER_SAMPLE,
+                "kernel": "evolve_brick_kernel" if args.kernel_variant != 1 else "evolve_warp_kernel", "ops_per_sample": ops,
                 "samples_per_s_kernel": samples / ev_s,
                 "gather_GBps": round(samples * 16 / ev_s / 1e9, 1),
                 "peak_source": f"{SMS} SMs x {LANES_PER_SM} FP32 lanes x sm_max_mhz (B200_PROFILING.md)"}
@@ -296,6 +302,7 @@ def run_ours(args):
         "config": {"workload": workload_name(cfg), "volume_iso": n_iso_l, "cells": n_cells,
                    "detections": n_dets, "n_samples": cfg.n_samples, "iters": cfg.max_iters,
                    "seed_mode": cfg.seed_mode, "parallelism": "1 GPU", "cull_every": args.cull_every,
+                   "estimator": args.estimator,
                    "l2": "inputs larger than L2 (u16 volume %.1f GiB > 126 MB)" % (h_raw.numel() * 2 / 2**30)},
         "cells_per_s": cells_per_s, "phase_ms": phase, "gpu_launches": int(launches),
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
@@ -347,6 +354,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cta-warps", type=int, default=0, help="warps per cell (0: auto)")
     ap.add_argument("--kernel-variant", type=int, default=0, help="evolve kernel: 0 auto, 1 warp, 2 brick")
+    ap.add_argument("--estimator", default="mc", choices=["mc", "cv", "ray"],
+                    help="MC (the paper's), MC + control variate (G21) or stratified ray march (G27)")
     ap.add_argument("--cull-every", type=int, default=0,
                     help="periodic culling every k iterations (P:326, G25); 0 = the paper's end-of-run cull")
     ap.add_argument("--e2e-inflight", type=int, default=2, help="steps in flight in the end-to-end run")

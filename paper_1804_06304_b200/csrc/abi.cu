@@ -69,11 +69,11 @@ static int32_t validate_params(const snk_params* p, int dim) {
   if (p->image_term != SNK_IMAGE_INTENSITY && p->image_term != SNK_IMAGE_GRADMAG)
     return fail(SNK_CONFIG, "bad image_term");
   if (p->kernel_variant > 2) return fail(SNK_CONFIG, "kernel_variant must be 0, 1 or 2");
-  if (p->estimator != SNK_EST_MC && p->estimator != SNK_EST_GRID)
-    return fail(SNK_CONFIG, "estimator must be SNK_EST_MC or SNK_EST_GRID");
+  if (p->estimator < SNK_EST_MC || p->estimator > SNK_EST_RAY)
+    return fail(SNK_CONFIG, "estimator must be SNK_EST_MC, _GRID, _MC_CV or _RAY");
   if (p->cull_every < 0) return fail(SNK_CONFIG, "cull_every must be >= 0");
-  if (p->estimator == SNK_EST_GRID && p->kernel_variant == 1)
-    return fail(SNK_CONFIG, "the grid estimator runs in the brick kernel only (kernel_variant 0 or 2)");
+  if (p->estimator != SNK_EST_MC && p->kernel_variant == 1)
+    return fail(SNK_CONFIG, "the grid / CV / ray estimators run in the brick kernel only (kernel_variant 0 or 2)");
   (void)dim;
   return SNK_OK;
 }
