@@ -774,7 +774,10 @@ __device__ __forceinline__ CellIt cell_iter(const EvoParams& P, const CellState&
 // alone; MC: each sample carries V/N = (4/3 pi | pi) rho_s^d / N.
 // RAY (G27): each step carries |S^(d-1)| rho_s t^(d-1) / N, the t^(d-1) already
 // in the leaves, so the sums scale by vscale rho_s.
-template <int D, bool GRID = false, int EST = 0>
+// NB: branch-free form (selects instead of the early return and the uniform
+// branches, same arithmetic) so that the compiler can interleave the update
+// with independent work of the same basic block (PIPE 3).
+template <int D, bool GRID = false, int EST = 0, bool NB = false>
 __device__ __forceinline__ bool cell_update(const EvoParams& P, CellState& s, const CellIt& C,
                                             const Acc& sum, int it) {
   const float rs = C.rho_s;
@@ -785,7 +788,7 @@ __device__ __forceinline__ bool cell_update(const EvoParams& P, CellState& s, co
   const float gden = D == 3 ? __fmul_rn(__fmul_rn(twoR, twoR), twoR) : __fmul_rn(twoR, twoR);
   const float gamma = rcp_approx(gden);
   s.E = __fmul_rn(gamma, A0);
-  if (it == P.T + 1) return true;
+  if (!NB && it == P.T + 1) return true;
   const float gs = __fmul_rn(__fmul_rn(gamma, scale), P.k6_dR);   // the leaves' 6/dR
   const float gcx = -__fmul_rn(gs, sum.cx), gcy = -__fmul_rn(gs, sum.cy), gcz = -__fmul_rn(gs, sum.cz);
   const float gR = __fmul_rn(gamma, __fsub_rn(__fmul_rn(__fmul_rn(sum.aR, scale), P.k6_dR),
@@ -807,7 +810,13 @@ __device__ __forceinline__ bool cell_update(const EvoParams& P, CellState& s, co
   // n_a - 1 < 2m (P.dom_small: possible for some axis at all)
   const float m = __fadd_rn(R, P.half_dR);
   float dx, dy, dz = lz;
-  if (P.dom_small) {
+  if (NB) {
+    const float m2 = __fmul_rn(2.0f, m);
+    const bool small = P.dom_small != 0;
+    dx = (small && P.fnx1 < m2) ? __fmul_rn(0.5f, P.fnx1) : clampf(lx, m, __fsub_rn(P.fnx1, m));
+    dy = (small && P.fny1 < m2) ? __fmul_rn(0.5f, P.fny1) : clampf(ly, m, __fsub_rn(P.fny1, m));
+    if (D == 3) dz = (small && P.fnz1 < m2) ? __fmul_rn(0.5f, P.fnz1) : clampf(lz, m, __fsub_rn(P.fnz1, m));
+  } else if (P.dom_small) {
     const float m2 = __fmul_rn(2.0f, m);
     dx = P.fnx1 < m2 ? __fmul_rn(0.5f, P.fnx1) : clampf(lx, m, __fsub_rn(P.fnx1, m));
     dy = P.fny1 < m2 ? __fmul_rn(0.5f, P.fny1) : clampf(ly, m, __fsub_rn(P.fny1, m));
@@ -816,6 +825,23 @@ __device__ __forceinline__ bool cell_update(const EvoParams& P, CellState& s, co
     dx = clampf(lx, m, __fsub_rn(P.fnx1, m));
     dy = clampf(ly, m, __fsub_rn(P.fny1, m));
     if (D == 3) dz = clampf(lz, m, __fsub_rn(P.fnz1, m));
+  }
+  if (NB) {
+    const bool fin = it == P.T + 1;   // E_final only: no update
+    const bool last = it == P.T;
+    float mv = fabsf(__fsub_rn(R, oR));
+    mv = fmaxf(mv, fabsf(__fsub_rn(dx, ox)));
+    mv = fmaxf(mv, fabsf(__fsub_rn(dy, oy)));
+    mv = fmaxf(mv, fabsf(__fsub_rn(dz, oz)));
+    uint32_t f = (mv < P.conv_tol) ? SNK_F_CONVERGED : 0u;
+    f |= ((lx != cx) || (ly != cy) || (lz != cz)) ? SNK_F_LEASHED : 0u;
+    f |= ((dx != lx) || (dy != ly) || (dz != lz)) ? SNK_F_DOMAIN : 0u;
+    s.flags |= last ? f : 0u;
+    s.cx = fin ? ox : dx;
+    s.cy = fin ? oy : dy;
+    s.cz = fin ? oz : dz;
+    s.R = fin ? oR : R;
+    return fin;
   }
   s.cx = dx; s.cy = dy; s.cz = dz;
   s.R = R;
@@ -1078,7 +1104,23 @@ __global__ void __launch_bounds__(32 * W, W == 4 ? 3 : SNK_BRICK_MINB8) evolve_b
     float* xo = &xch[it & 1][0][0];
     warp_reduce_scatter(part, xo + wsub, lane, W);
     __syncthreads();   // also: every brick read of this iteration is done
-    if constexpr (PIPE && SNK_BRICK_PIPE == 2) {
+    if constexpr (PIPE && SNK_BRICK_PIPE == 3) {
+      // PIPE 2 with the next iteration's draws placed before a branch-free
+      // update in one basic block, so the two independent streams interleave
+      Acc sum;
+      sum.a0 = comp_tree<W>(xo + 0 * W);
+      sum.cx = comp_tree<W>(xo + 1 * W);
+      sum.cy = comp_tree<W>(xo + 2 * W);
+      sum.cz = comp_tree<W>(xo + 3 * W);
+      sum.aR = comp_tree<W>(xo + 4 * W);
+      CellIt Cn;
+      Cn.p0 = s.q0 ^ (uint32_t)(it + 1);
+      Cn.p1 = s.q1;
+      Cn.p3 = s.q3;
+      if constexpr (EST == SNK_EST_RAY) draw_dirs_ray<D>(P, Cn, j0 / 8u, dir);
+      else draw_dirs<D, CH>(P, Cn, j0, dir);
+      if (cell_update<D, false, EST, true>(P, s, C, sum, it)) break;
+    } else if constexpr (PIPE && SNK_BRICK_PIPE == 2) {
       // every warp takes the (identical) update itself: one barrier per
       // iteration; xch is double-buffered by parity, and the next brick reload
       // happens after this barrier, i.e. after every read of this iteration
