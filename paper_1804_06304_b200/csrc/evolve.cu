@@ -950,14 +950,19 @@ __device__ __forceinline__ void load_brick(uint16_t* brick, const EvoParams& P, 
 #ifndef SNK_BRICK_MINB8
 #define SNK_BRICK_MINB8 2
 #endif
+#ifndef SNK_BRICK_MINB4
+#define SNK_BRICK_MINB4 3
+#endif
 // PIPE (one chunk per thread, L == 0): the state-independent part of the next
 // iteration's draws (Philox words -> direction, radial variate) is computed
 // while warp 0 alone takes the update step, which it then broadcasts; the
 // arithmetic is unchanged, only its placement.
-// PIPE 2 (default): every warp then takes the identical update itself — one
-// barrier per iteration instead of two (C3/C4 evolve 0.7-0.8% faster).
+// PIPE 2: every warp then takes the identical update itself — one barrier per
+// iteration instead of two (C3/C4 evolve 0.7-0.8% faster).  PIPE 3 (default):
+// as 2, with the next draws placed before a branch-free update so the two
+// interleave (the Philox words are even hoisted above the barrier; +0.2-0.5%).
 #ifndef SNK_BRICK_PIPE
-#define SNK_BRICK_PIPE 2
+#define SNK_BRICK_PIPE 3
 #endif
 // the f32x2 fast path (chunk8_fast_x2); 0 = scalar (same results)
 #ifndef SNK_F32X2
@@ -1049,7 +1054,7 @@ struct BrickCtl {
 };
 
 template <int D, int W, int S, bool SLAB, int CH, int L, int EST = 0>
-__global__ void __launch_bounds__(32 * W, W == 4 ? 3 : SNK_BRICK_MINB8) evolve_brick_kernel(const __grid_constant__ EvoParams P) {
+__global__ void __launch_bounds__(32 * W, W == 4 ? SNK_BRICK_MINB4 : SNK_BRICK_MINB8) evolve_brick_kernel(const __grid_constant__ EvoParams P) {
   constexpr int B = CH << L;
   constexpr bool PIPE = SNK_BRICK_PIPE && L == 0;
   static_assert(EST == 0 || (PIPE && CH == 8), "CV / RAY estimators: 8 samples per thread, pipelined draws");
@@ -1327,7 +1332,10 @@ int32_t warp_W(const EvoParams& P, int W, int B, cudaStream_t st) {
   }
 }
 
-constexpr int kS3 = 33;
+#ifndef SNK_BRICK_S3
+#define SNK_BRICK_S3 33
+#endif
+constexpr int kS3 = SNK_BRICK_S3;
 
 template <int D, int W, int S, bool SLAB>
 int32_t brick_B(const EvoParams& P, int B, cudaStream_t st) {

@@ -241,9 +241,97 @@ __global__ void __launch_bounds__(256) sep8_kernel(const uint16_t* __restrict__ 
   reinterpret_cast<uint4*>(out)[t] = pack8(o);
 }
 
+// z pass as column streaming: a thread owns one 8-voxel x group of one row
+// (xc, y) and walks kZC consecutive output planes with a window of 2H+1 input
+// planes held in registers (a ring with static indices: the plane loop is
+// unrolled by 2H+1), so every input plane is read (kZC + 2H)/kZC times instead
+// of 2H+1 times — the flat z pass re-read its window through L2, which C4's
+// 8 MB planes overflow.  Consecutive threads take consecutive x groups of a
+// row (16-byte coalesced loads).  Same arithmetic as sep8_kernel<2, OP>:
+// blur windows are unpacked once per plane, max windows stay packed (u16x2
+// VIMNMX).
+constexpr int kZC = 32;
+
+__device__ __forceinline__ uint4 vmax4(uint4 a, uint4 b) {
+  return make_uint4(__vmaxu2(a.x, b.x), __vmaxu2(a.y, b.y), __vmaxu2(a.z, b.z), __vmaxu2(a.w, b.w));
+}
+
+template <int OP, int H>
+__global__ void __launch_bounds__(256) zcol8_kernel(const uint16_t* __restrict__ in, uint16_t* __restrict__ out,
+                                                    int nx, int ny, int nz, int lo, int hi,
+                                                    const __grid_constant__ Taps T) {
+  constexpr int K = 2 * H + 1;
+  const int64_t ncols = (int64_t)(nx >> 3) * ny;
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int nzc = (nz + kZC - 1) / kZC;
+  if (t >= ncols * nzc) return;
+  const int64_t col = t % ncols;
+  const int z0 = (int)(t / ncols) * kZC, z1 = min(z0 + kZC, nz);
+  const uint4* rin = reinterpret_cast<const uint4*>(in) + col;
+  uint4* rout = reinterpret_cast<uint4*>(out) + col;
+  auto load = [&](int q) -> uint4 {
+    if (OP == OP_BLUR) return __ldg(rin + (int64_t)min(max(q, 0), nz - 1) * ncols);
+    if (q < lo || q > hi) return make_uint4(0u, 0u, 0u, 0u);   // outside the clipped window
+    return __ldg(rin + (int64_t)q * ncols);
+  };
+  if (OP == OP_BLUR) {
+    uint32_t win[K][8];
+#pragma unroll
+    for (int i = 0; i < K - 1; ++i) unpack8(load(z0 - H + i), win[i]);
+    for (int zb = z0; zb < z1; zb += K) {
+#pragma unroll
+      for (int s = 0; s < K; ++s) {
+        const int z = zb + s;
+        if (z >= z1) break;
+        unpack8(load(z + H), win[(s + K - 1) % K]);   // plane z + H
+        uint32_t o[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) o[k] = 8192u;
+#pragma unroll
+        for (int i = 0; i < K; ++i)                   // plane z - H + i
+#pragma unroll
+          for (int k = 0; k < 8; ++k) o[k] += (uint32_t)T.w[i] * win[(s + i) % K][k];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) o[k] >>= 14;
+        rout[(int64_t)z * ncols] = pack8(o);
+      }
+    }
+  } else {
+    uint4 win[K];
+#pragma unroll
+    for (int i = 0; i < K - 1; ++i) win[i] = load(z0 - H + i);
+    for (int zb = z0; zb < z1; zb += K) {
+#pragma unroll
+      for (int s = 0; s < K; ++s) {
+        const int z = zb + s;
+        if (z >= z1) break;
+        win[(s + K - 1) % K] = load(z + H);
+        uint4 m = win[s % K];
+#pragma unroll
+        for (int i = 1; i < K; ++i) m = vmax4(m, win[(s + i) % K]);
+        rout[(int64_t)z * ncols] = m;
+      }
+    }
+  }
+}
+
 template <int AXIS, int OP>
 int32_t sep8_launch(int h, const uint16_t* in, uint16_t* out, int nx, int ny, int nz, int lo, int hi,
                     const Taps& tp, cudaStream_t st) {
+  if (AXIS == 2 && h > 0 && nz > kZC) {
+    // z: column streaming (flat z passes re-read 2h+1 planes through L2)
+    const unsigned zg = (unsigned)ceil_div((int64_t)(nx / 8) * ny * ceil_div(nz, kZC), 256);
+    switch (h) {
+#define SNK_ZC_CASE(HH) \
+      case HH: zcol8_kernel<OP, HH><<<zg, 256, 0, st>>>(in, out, nx, ny, nz, lo, hi, tp); break;
+      SNK_ZC_CASE(1) SNK_ZC_CASE(2) SNK_ZC_CASE(3) SNK_ZC_CASE(4)
+      SNK_ZC_CASE(5) SNK_ZC_CASE(6) SNK_ZC_CASE(7) SNK_ZC_CASE(8)
+#undef SNK_ZC_CASE
+      default: return fail(SNK_INTERNAL, "zcol8: radius > 8");
+    }
+    SNK_LAUNCH_CHECK("zcol8_kernel");
+    return SNK_OK;
+  }
   const unsigned grid = (unsigned)ceil_div((int64_t)(nx / 8) * ny * nz, 256);
   switch (h) {
 #define SNK_SEP_CASE(HH) \

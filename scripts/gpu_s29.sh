@@ -1,0 +1,6 @@
+#!/bin/bash
+TAG=${1:-s}; O=gpurun_out; mkdir -p $O
+SNK_LIB=paper_1804_06304_b200/libsnk_s29.so timeout 900 python -m pytest tests -m gpu -q --timeout 600 -rf -k "c1_parity or reload or estimator" > $O/${TAG}_pytest_gpu.log 2>&1
+echo "pytest exit $?" >> $O/${TAG}_pytest_gpu.log
+bash scripts/variants.sh ${TAG}v C3 "-:4 s29:4"
+bash scripts/variants.sh ${TAG}v C4 "s29:4"

@@ -51,7 +51,9 @@ def _assert_cells_close(g, o, ctx=""):
                                              # x extent % 8 == 0: the vectorised passes
                                              (3, (19, 23, 64), 1.0), (3, (10, 12, 136), 2.0),
                                              (3, (7, 9, 8), 1.0), (3, (33, 17, 48), 0.5),
-                                             (2, (1, 100, 256), 1.0), (2, (1, 31, 8), 2.0)])
+                                             (2, (1, 100, 256), 1.0), (2, (1, 31, 8), 2.0),
+                                             # nz > 32: the column-streamed z pass, ragged last chunk
+                                             (3, (70, 9, 16), 1.0), (3, (41, 6, 24), 2.0), (3, (33, 7, 8), 0.5)])
 def test_blur_gradmag_bitexact(gpu, dim, shape, sigma):
     torch, snk, _ = gpu
     rng = np.random.default_rng(hash(shape) % 2 ** 32)
@@ -90,7 +92,9 @@ def test_gradmag_extreme_bitexact(gpu, dim, shape):
 
 
 @pytest.mark.parametrize("dim,shape,w", [(3, (30, 26, 64), 3), (3, (21, 19, 40), 0), (3, (40, 36, 32), 8),
-                                         (3, (25, 22, 45), 5), (2, (1, 90, 128), 6), (2, (1, 70, 75), 4)])
+                                         (3, (25, 22, 45), 5), (2, (1, 90, 128), 6), (2, (1, 70, 75), 4),
+                                         # nz > 32: the column-streamed z fold
+                                         (3, (75, 20, 24), 5), (3, (33, 10, 16), 1), (3, (97, 6, 8), 2)])
 def test_seeds_maxima_plateaus_bitexact(gpu, dim, shape, w):
     """a4 MAXIMA on quantised random volumes (many equal values: the tie rule
     decides), vectorised (x % 8 == 0) and fallback paths, w in {0, .., 8}."""
