@@ -94,10 +94,13 @@ __global__ void __launch_bounds__(kThreads) label_kernel(const snk_cell* __restr
     yv[k] = D == 3 ? ty * G.ty + ly : ty * G.ty + ly + k * kTY;
     zv[k] = D == 3 ? G.z0 + tz * G.tz + k : G.z0;
   }
+  // the best candidate so far as (d2, thr): its key d2/thr (an IEEE division)
+  // is only needed when a second detection contains the voxel (rare: overlaps
+  // of inner balls), so most voxels never divide
   int best[NV];
-  double best_key[NV];
+  double best_d2[NV], best_thr[NV];
 #pragma unroll
-  for (int k = 0; k < NV; ++k) { best[k] = -1; best_key[k] = 0.0; }
+  for (int k = 0; k < NV; ++k) { best[k] = -1; best_d2[k] = 0.0; best_thr[k] = 1.0; }
   const double px = (double)x;
   const int64_t e0 = offsets[tile], e1 = offsets[tile + 1];
   for (int64_t s = e0; s < e1; s += kStage) {
@@ -127,10 +130,15 @@ __global__ void __launch_bounds__(kThreads) label_kernel(const snk_cell* __restr
           const double dz = __dsub_rn((double)zv[v], s_c[2][k]);
           const double d2 = __dadd_rn(dxy, __dmul_rn(dz, dz));
           if (d2 <= thr) {
-            const double key = __ddiv_rn(d2, thr);
-            if (best[v] < 0 || key < best_key[v] || (key == best_key[v] && i < best[v])) {
+            bool take = best[v] < 0;
+            if (!take) {
+              const double key = __ddiv_rn(d2, thr), bkey = __ddiv_rn(best_d2[v], best_thr[v]);
+              take = key < bkey || (key == bkey && i < best[v]);
+            }
+            if (take) {
               best[v] = i;
-              best_key[v] = key;
+              best_d2[v] = d2;
+              best_thr[v] = thr;
             }
           }
         }
@@ -140,10 +148,15 @@ __global__ void __launch_bounds__(kThreads) label_kernel(const snk_cell* __restr
           const double dy = __dsub_rn((double)yv[v], s_c[1][k]);
           const double d2 = __dadd_rn(dx2, __dmul_rn(dy, dy));
           if (d2 <= thr) {
-            const double key = __ddiv_rn(d2, thr);
-            if (best[v] < 0 || key < best_key[v] || (key == best_key[v] && i < best[v])) {
+            bool take = best[v] < 0;
+            if (!take) {
+              const double key = __ddiv_rn(d2, thr), bkey = __ddiv_rn(best_d2[v], best_thr[v]);
+              take = key < bkey || (key == bkey && i < best[v]);
+            }
+            if (take) {
               best[v] = i;
-              best_key[v] = key;
+              best_d2[v] = d2;
+              best_thr[v] = thr;
             }
           }
         }

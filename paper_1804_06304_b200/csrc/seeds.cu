@@ -460,31 +460,39 @@ __global__ void __launch_bounds__(256) maxima_predz_kernel(MaxArgs A, const uint
     if (q < 0 || q >= A.nz_glob) return make_uint4(0u, 0u, 0u, 0u);
     return __ldg(xy + (int64_t)(q - A.z_lo) * ncols);
   };
-  uint4 win[K];
+  uint4 win[K - 1];   // win[j] = plane zb - W + j; a block's K new planes load together
 #pragma unroll
-  for (int i = 0; i < K - 1; ++i) win[i] = load(z0 - W + i);
+  for (int j = 0; j < K - 1; ++j) win[j] = load(z0 - W + j);
   for (int zb = z0; zb < z1; zb += K) {
+    uint4 nxt[K];
+#pragma unroll
+    for (int s = 0; s < K; ++s) nxt[s] = load(zb + W + s);
 #pragma unroll
     for (int s = 0; s < K; ++s) {
       const int zo = zb + s;
-      if (zo >= z1) break;
-      win[(s + K - 1) % K] = load(zo + W);
-      uint4 mq = win[s % K];
+      if (zo < z1) {
+        uint4 mq = s < K - 1 ? win[s] : nxt[s - (K - 1)];
 #pragma unroll
-      for (int i = 1; i < K; ++i) mq = vmax4s(mq, win[(s + i) % K]);
-      uint32_t b[8], m[8];
-      unpack8s(__ldg(bb + (int64_t)(zo - A.z_lo) * ncols), b);
-      unpack8s(mq, m);
-      uint32_t bits = 0;
+        for (int i = 1; i < K; ++i) {
+          const int j = s + i;
+          mq = vmax4s(mq, j < K - 1 ? win[j] : nxt[j - (K - 1)]);
+        }
+        uint32_t b[8], m[8];
+        unpack8s(__ldg(bb + (int64_t)(zo - A.z_lo) * ncols), b);
+        unpack8s(mq, m);
+        uint32_t bits = 0;
 #pragma unroll
-      for (int k = 0; k < 8; ++k)
-        if (b[k] >= A.thr && b[k] == m[k]) bits |= 1u << k;
-      if (bits) {
         for (int k = 0; k < 8; ++k)
-          if ((bits >> k & 1u) && !tie_free(A, xc * 8 + k, y, zo, (uint16_t)b[k])) bits &= ~(1u << k);
+          if (b[k] >= A.thr && b[k] == m[k]) bits |= 1u << k;
+        if (bits) {
+          for (int k = 0; k < 8; ++k)
+            if ((bits >> k & 1u) && !tie_free(A, xc * 8 + k, y, zo, (uint16_t)b[k])) bits &= ~(1u << k);
+        }
+        mask[(int64_t)(zo - own_z0) * ncols + col] = (uint8_t)bits;
       }
-      mask[(int64_t)(zo - own_z0) * ncols + col] = (uint8_t)bits;
     }
+#pragma unroll
+    for (int j = 0; j < K - 1; ++j) win[j] = nxt[j + 1];
   }
 }
 

@@ -274,44 +274,48 @@ __global__ void __launch_bounds__(256) zcol8_kernel(const uint16_t* __restrict__
     if (q < lo || q > hi) return make_uint4(0u, 0u, 0u, 0u);   // outside the clipped window
     return __ldg(rin + (int64_t)q * ncols);
   };
-  if (OP == OP_BLUR) {
-    uint32_t win[K][8];
+  // win[j] = plane zb - H + j (j < K - 1); the K planes zb + H .. zb + H + K - 1
+  // of a block are loaded together (K loads in flight per thread)
+  uint4 win[K - 1];
 #pragma unroll
-    for (int i = 0; i < K - 1; ++i) unpack8(load(z0 - H + i), win[i]);
-    for (int zb = z0; zb < z1; zb += K) {
+  for (int j = 0; j < K - 1; ++j) win[j] = load(z0 - H + j);
+  for (int zb = z0; zb < z1; zb += K) {
+    uint4 nxt[K];
 #pragma unroll
-      for (int s = 0; s < K; ++s) {
-        const int z = zb + s;
-        if (z >= z1) break;
-        unpack8(load(z + H), win[(s + K - 1) % K]);   // plane z + H
-        uint32_t o[8];
+    for (int s = 0; s < K; ++s) nxt[s] = load(zb + H + s);
 #pragma unroll
-        for (int k = 0; k < 8; ++k) o[k] = 8192u;
+    for (int s = 0; s < K; ++s) {
+      const int z = zb + s;
+      if (z < z1) {
+        if (OP == OP_BLUR) {
+          uint32_t o[8];
 #pragma unroll
-        for (int i = 0; i < K; ++i)                   // plane z - H + i
+          for (int k = 0; k < 8; ++k) o[k] = 8192u;
 #pragma unroll
-          for (int k = 0; k < 8; ++k) o[k] += (uint32_t)T.w[i] * win[(s + i) % K][k];
+          for (int i = 0; i < K; ++i) {     // plane z - H + i
+            const int j = s + i;
+            uint32_t v[8];
+            unpack8(j < K - 1 ? win[j] : nxt[j - (K - 1)], v);
 #pragma unroll
-        for (int k = 0; k < 8; ++k) o[k] >>= 14;
-        rout[(int64_t)z * ncols] = pack8(o);
+            for (int k = 0; k < 8; ++k) o[k] += (uint32_t)T.w[i] * v[k];
+          }
+#pragma unroll
+          for (int k = 0; k < 8; ++k) o[k] >>= 14;
+          rout[(int64_t)z * ncols] = pack8(o);
+        } else {
+          uint4 m = win[s < K - 1 ? s : 0];
+          if (s >= K - 1) m = nxt[s - (K - 1)];
+#pragma unroll
+          for (int i = 1; i < K; ++i) {
+            const int j = s + i;
+            m = vmax4(m, j < K - 1 ? win[j] : nxt[j - (K - 1)]);
+          }
+          rout[(int64_t)z * ncols] = m;
+        }
       }
     }
-  } else {
-    uint4 win[K];
 #pragma unroll
-    for (int i = 0; i < K - 1; ++i) win[i] = load(z0 - H + i);
-    for (int zb = z0; zb < z1; zb += K) {
-#pragma unroll
-      for (int s = 0; s < K; ++s) {
-        const int z = zb + s;
-        if (z >= z1) break;
-        win[(s + K - 1) % K] = load(z + H);
-        uint4 m = win[s % K];
-#pragma unroll
-        for (int i = 1; i < K; ++i) m = vmax4(m, win[(s + i) % K]);
-        rout[(int64_t)z * ncols] = m;
-      }
-    }
+    for (int j = 0; j < K - 1; ++j) win[j] = nxt[j + 1];
   }
 }
 
