@@ -57,7 +57,8 @@ class ora_params(C.Structure):
                 ("e0", C.c_double), ("iscale", C.c_double), ("max_step", C.c_double),
                 ("r_min", C.c_double), ("r_max", C.c_double), ("leash", C.c_double),
                 ("conv_tol", C.c_double), ("max_iters", C.c_int32), ("n_samples", C.c_int32),
-                ("dim", C.c_int32), ("mode", C.c_int32), ("seed", C.c_uint64)]
+                ("dim", C.c_int32), ("mode", C.c_int32), ("seed", C.c_uint64),
+                ("scale", C.c_double * 3)]
 
 
 class ora_cell(C.Structure):
@@ -87,8 +88,9 @@ class Params:
     max_iters: int = 400
     n_samples: int = 1024
     dim: int = 3
-    mode: int = 0                  # 0 MC, 1 grid (Eq. 5)
+    mode: int = 0                  # 0 MC, 1 grid (Eq. 5, isotropic only), 2 MC + CV, 3 ray march
     seed: int = 1804063040
+    scale: tuple = (1.0, 1.0, 1.0)  # physical voxel size per axis (G28): anisotropic sampling
 
     def c(self) -> ora_params:
         return ora_params(self.r0, self.delta_R, self.eps0, self.e0, self.iscale,
@@ -96,7 +98,7 @@ class Params:
                           2 * self.r0 if self.r_max is None else self.r_max,
                           2 * self.r0 if self.leash is None else self.leash,
                           self.conv_tol, self.max_iters, self.n_samples, self.dim, self.mode,
-                          self.seed & 0xFFFFFFFFFFFFFFFF)
+                          self.seed & 0xFFFFFFFFFFFFFFFF, (C.c_double * 3)(*self.scale))
 
 
 def _p(a):
@@ -111,6 +113,10 @@ def _declare(L):
         "ora_weight": (None, [d, d, d, i32, vp]),
         "ora_q14_taps": (i32, [d, vp, i32]),
         "ora_blur": (i32, [vp, vp, i32, d, vp]),
+        "ora_blur3": (i32, [vp, vp, i32, vp, vp]),
+        "ora_seeds_lattice3": (i32, [vp, i32, d, d, vp, vp, i64, vp]),
+        "ora_seeds_maxima3": (i32, [vp, vp, vp, vp, vp, vp, i32, vp, vp, u32, vp, i64, vp]),
+        "ora_label3": (i32, [vp, i32, i64, i64, vp, vp, vp, i64, vp]),
         "ora_gradmag": (i32, [vp, vp, i32, vp]),
         "ora_resample_dims": (None, [vp, vp, i32, vp]),
         "ora_resample": (i32, [vp, vp, vp, i32, vp]),
@@ -177,9 +183,14 @@ def q14_taps(sigma):
 
 
 def blur(vol, dim=3, sigma=1.0):
+    """O2; sigma may be a per-axis triple (anisotropic grid, G28: sigma / scale_a)."""
     v = _u16(vol)
     out = np.empty_like(v)
-    st = lib().ora_blur(_p(v), _p(_dims(v)), dim, sigma, _p(out))
+    if np.ndim(sigma) == 0:
+        st = lib().ora_blur(_p(v), _p(_dims(v)), dim, float(sigma), _p(out))
+    else:
+        s3 = np.asarray(sigma, np.float64).copy()
+        st = lib().ora_blur3(_p(v), _p(_dims(v)), dim, _p(s3), _p(out))
     assert st == OK
     return out
 
@@ -209,13 +220,15 @@ def resample(vol, spacing, dim=3):
     return out if vol.ndim == 3 else out[0]
 
 
-def seeds_lattice(n_xyz, dim, r0, dR=2.0):
+def seeds_lattice(n_xyz, dim, r0, dR=2.0, scale=(1.0, 1.0, 1.0)):
+    """O4 LATTICE; on an anisotropic grid (G28) in physical coordinates."""
     n = np.asarray(n_xyz, np.int64).copy()
+    sc = np.asarray(scale, np.float64).copy()
     cnt = C.c_int64()
-    lib().ora_seeds_lattice(_p(n), dim, r0, dR, None, 0, C.byref(cnt))
+    lib().ora_seeds_lattice3(_p(n), dim, r0, dR, _p(sc), None, 0, C.byref(cnt))
     cap = max(int(cnt.value), 1)
     out = np.zeros((cap, 3), np.float32)
-    st = lib().ora_seeds_lattice(_p(n), dim, r0, dR, _p(out), cap, C.byref(cnt))
+    st = lib().ora_seeds_lattice3(_p(n), dim, r0, dR, _p(sc), _p(out), cap, C.byref(cnt))
     return st, out[:cnt.value] if st == OK else out[:0]
 
 
@@ -238,18 +251,21 @@ def is_maxima_seed(vol, dim, w, thr, x, y, z, org=None, n_global=None):
     return bool(r)
 
 
-def seeds_maxima(vol, dim, w, thr, org=None, n_global=None, lo=None, hi=None):
-    """Seeds of the (global) box lo..hi (inclusive; default: the whole buffer)."""
+def seeds_maxima(vol, dim, w, thr, org=None, n_global=None, lo=None, hi=None, scale=(1.0, 1.0, 1.0)):
+    """Seeds of the (global) box lo..hi (inclusive; default: the whole buffer).
+    w may be a per-axis triple; seeds come out in physical coordinates (index x scale, G28)."""
     v = _u16(vol)
     n, o, nb = _box(v, org, n_global)
     lo = o.copy() if lo is None else np.asarray(lo, np.int64).copy()
     hi = (o + nb - 1) if hi is None else np.asarray(hi, np.int64).copy()
+    w3 = np.asarray([w, w, w] if np.ndim(w) == 0 else w, np.int32).copy()
+    sc = np.asarray(scale, np.float64).copy()
     cnt = C.c_int64()
     cap = 1 << 16
     while True:
         out = np.zeros((cap, 3), np.float32)
-        st = lib().ora_seeds_maxima(_p(v), _p(n), _p(o), _p(nb), _p(lo), _p(hi), dim, w, thr, _p(out),
-                                    cap, C.byref(cnt))
+        st = lib().ora_seeds_maxima3(_p(v), _p(n), _p(o), _p(nb), _p(lo), _p(hi), dim, _p(w3), _p(sc), thr,
+                                     _p(out), cap, C.byref(cnt))
         if st == CAPACITY:
             cap = int(cnt.value)
             continue
@@ -364,13 +380,15 @@ def cull(c, R, E, flags, ids, dim, e0):
     return keep[:nk.value].copy()
 
 
-def label(n_xyz, dim, c, R, z0=0, nz=None):
+def label(n_xyz, dim, c, R, z0=0, nz=None, scale=(1.0, 1.0, 1.0)):
+    """O7; voxel (x, y, z) at the physical point (x, y, z) * scale (G28)."""
     n = np.asarray(n_xyz, np.int64).copy()
     nz = int(n[2]) - z0 if nz is None else nz
     c = np.ascontiguousarray(c, np.float32).reshape(-1, 3)
     R = np.ascontiguousarray(R, np.float32)
+    sc = np.asarray(scale, np.float64).copy()
     out = np.zeros((nz, n[1], n[0]), np.int32)
-    lib().ora_label(_p(n), dim, z0, nz, _p(c), _p(R), len(R), _p(out))
+    lib().ora_label3(_p(n), dim, z0, nz, _p(sc), _p(c), _p(R), len(R), _p(out))
     return out
 
 

@@ -158,6 +158,7 @@ struct Image {
   int64_t org[3], nb[3];
   int dim;
   double iscale;
+  double scale[3];   // physical voxel size per axis (G28); the lookup point is k / scale
 
   double voxel(int64_t x, int64_t y, int64_t z, bool* halo) const {
     int64_t p[3] = {x - org[0], y - org[1], z - org[2]};
@@ -168,9 +169,10 @@ struct Image {
 
   // trilinear (bilinear in 2D): clamp k to [0, n-1], i0 = min(floor(k), n-2),
   // f = k - i0, interpolate in x, then y, then z (§8(c) O5 step 4).
-  double interp(const double k[3], bool* halo) const {
+  double interp(const double kp[3], bool* halo) const {
     int64_t i0[3] = {0, 0, 0};
     double f[3] = {0.0, 0.0, 0.0};
+    const double k[3] = {kp[0] / scale[0], kp[1] / scale[1], kp[2] / scale[2]};
     for (int a = 0; a < dim; ++a) {
       const double kc = clampd(k[a], 0.0, (double)(n[a] - 1));
       if (n[a] == 1) { i0[a] = 0; f[a] = 0.0; continue; }
@@ -201,6 +203,10 @@ struct ora_params {
   double r0, delta_R, eps0, e0, iscale, max_step, r_min, r_max, leash, conv_tol;
   int32_t max_iters, n_samples, dim, mode;   // mode 0 MC, 1 grid (Eq. 5), 2 MC + control variate, 3 ray march
   uint64_t seed;
+  // physical size of a voxel along each axis in the contour's units (SURVEY
+  // §8(f) 4, reading G28): 1 = isotropic; an anisotropic volume is sampled at
+  // raw coordinate k_a / scale_a without resampling (MC modes only)
+  double scale[3];
 };
 
 struct ora_cell {
@@ -315,14 +321,21 @@ int ora_q14_taps(double sigma, int32_t* taps, int cap) {
 }
 
 // Passes x, then y, then z (3D only): out = (sum_i w_i in[clamp(x + i)] + 8192) >> 14.
-int ora_blur(const uint16_t* in, const int64_t n[3], int dim, double sigma, uint16_t* out) {
-  int32_t taps[257];
-  const int h = ora_q14_taps(sigma, taps, 257);
-  if (h < 0) return ORA_CONFIG;
+// ora_blur3: a sigma per axis (in voxels of that axis) — on an anisotropic grid
+// sampled without resampling the physical sigma becomes sigma / scale_a (G28).
+int ora_blur3(const uint16_t* in, const int64_t n[3], int dim, const double sigma[3], uint16_t* out) {
+  int32_t taps[3][257];
+  int h[3];
+  for (int a = 0; a < 3; ++a) {
+    h[a] = ora_q14_taps(sigma[a], taps[a], 257);
+    if (h[a] < 0) return ORA_CONFIG;
+  }
   const int64_t N = n[0] * n[1] * n[2];
   std::vector<uint16_t> cur(in, in + N), nxt(N);
   const int64_t stride[3] = {1, n[0], n[0] * n[1]};
   for (int a = 0; a < dim; ++a) {
+    const int ha = h[a];
+    const int32_t* ta = taps[a];
 #pragma omp parallel for schedule(static)
     for (int64_t z = 0; z < n[2]; ++z)
       for (int64_t y = 0; y < n[1]; ++y)
@@ -330,9 +343,9 @@ int ora_blur(const uint16_t* in, const int64_t n[3], int dim, double sigma, uint
           const int64_t p[3] = {x, y, z};
           const int64_t base = x + y * stride[1] + z * stride[2] - p[a] * stride[a];
           int64_t acc = 0;
-          for (int i = -h; i <= h; ++i) {
+          for (int i = -ha; i <= ha; ++i) {
             const int64_t q = clampi(p[a] + i, 0, n[a] - 1);
-            acc += (int64_t)taps[i + h] * (int64_t)cur[base + q * stride[a]];
+            acc += (int64_t)ta[i + ha] * (int64_t)cur[base + q * stride[a]];
           }
           nxt[x + y * stride[1] + z * stride[2]] = (uint16_t)((acc + 8192) >> 14);
         }
@@ -340,6 +353,11 @@ int ora_blur(const uint16_t* in, const int64_t n[3], int dim, double sigma, uint
   }
   std::memcpy(out, cur.data(), N * sizeof(uint16_t));
   return ORA_OK;
+}
+
+int ora_blur(const uint16_t* in, const int64_t n[3], int dim, double sigma, uint16_t* out) {
+  const double s3[3] = {sigma, sigma, sigma};
+  return ora_blur3(in, n, dim, s3, out);
 }
 
 // ---------------------------------------------------------------------------
@@ -379,14 +397,16 @@ int ora_gradmag(const uint16_t* B, const int64_t n[3], int dim, uint16_t* out) {
 // centred in each axis: with L = n - 1, k = floor((L - 2m)/s) + 1 and offset
 // o = m + ((L - 2m) - (k - 1) s)/2.  Ids z-major, x fastest.  Status EMPTY if
 // any lattice axis has L - 2m < 0 ("reported as a distinct condition").
-int ora_seeds_lattice(const int64_t n[3], int dim, double r0, double dR, float* out_xyz,
-                      int64_t cap, int64_t* count) {
+// ora_seeds_lattice3: on an anisotropic grid (G28) the lattice lives in
+// physical units: axis extent L = (n - 1) scale, output in physical coordinates.
+int ora_seeds_lattice3(const int64_t n[3], int dim, double r0, double dR, const double scale[3],
+                       float* out_xyz, int64_t cap, int64_t* count) {
   const double m = r0 + dR / 2.0;
   const double s = std::sqrt(1.5) * r0;
   int64_t k[3] = {1, 1, 1};
   double o[3] = {0.0, 0.0, 0.0};
   for (int a = 0; a < dim; ++a) {
-    const double span = (double)(n[a] - 1) - 2.0 * m;
+    const double span = (double)(n[a] - 1) * scale[a] - 2.0 * m;
     if (span < 0.0) { *count = 0; return ORA_EMPTY; }
     k[a] = (int64_t)std::floor(span / s) + 1;
     o[a] = m + (span - (double)(k[a] - 1) * s) / 2.0;
@@ -405,6 +425,12 @@ int ora_seeds_lattice(const int64_t n[3], int dim, double r0, double dR, float* 
   return ORA_OK;
 }
 
+int ora_seeds_lattice(const int64_t n[3], int dim, double r0, double dR, float* out_xyz,
+                      int64_t cap, int64_t* count) {
+  const double one[3] = {1.0, 1.0, 1.0};
+  return ora_seeds_lattice3(n, dim, r0, dR, one, out_xyz, cap, count);
+}
+
 // §8(c) O4 MAXIMA — seed detection (north_star; reading G20, "any method
 // that reliably places initial contours").  x is a seed iff B(x) >= thr and no
 // y in the (2w+1)^d box W(x) (clipped to the volume) has B(y) > B(x), or
@@ -421,17 +447,18 @@ struct Box {
   }
 };
 
-static bool is_maxima_seed(const Box& b, int dim, int w, uint32_t thr, int64_t x, int64_t y,
+// per-axis half-widths w[a] (an anisotropic grid: w / scale_a voxels, G28)
+static bool is_maxima_seed(const Box& b, int dim, const int w[3], uint32_t thr, int64_t x, int64_t y,
                            int64_t z) {
   const int64_t nx = b.n[0], ny = b.n[1];
   const uint16_t v = b.at(x, y, z);
   if ((uint32_t)v < thr) return false;
   const int64_t lin = (z * ny + y) * nx + x;
-  const int64_t z0 = dim == 3 ? std::max<int64_t>(z - w, 0) : z;
-  const int64_t z1 = dim == 3 ? std::min<int64_t>(z + w, b.n[2] - 1) : z;
+  const int64_t z0 = dim == 3 ? std::max<int64_t>(z - w[2], 0) : z;
+  const int64_t z1 = dim == 3 ? std::min<int64_t>(z + w[2], b.n[2] - 1) : z;
   for (int64_t zz = z0; zz <= z1; ++zz)
-    for (int64_t yy = std::max<int64_t>(y - w, 0); yy <= std::min<int64_t>(y + w, ny - 1); ++yy)
-      for (int64_t xx = std::max<int64_t>(x - w, 0); xx <= std::min<int64_t>(x + w, nx - 1); ++xx) {
+    for (int64_t yy = std::max<int64_t>(y - w[1], 0); yy <= std::min<int64_t>(y + w[1], ny - 1); ++yy)
+      for (int64_t xx = std::max<int64_t>(x - w[0], 0); xx <= std::min<int64_t>(x + w[0], nx - 1); ++xx) {
         const uint16_t u = b.at(xx, yy, zz);
         if (u > v) return false;
         if (u == v && (zz * ny + yy) * nx + xx < lin) return false;
@@ -439,9 +466,9 @@ static bool is_maxima_seed(const Box& b, int dim, int w, uint32_t thr, int64_t x
   return true;
 }
 
-static bool window_inside(const Box& b, int dim, int w, const int64_t lo[3], const int64_t hi[3]) {
+static bool window_inside(const Box& b, int dim, const int w[3], const int64_t lo[3], const int64_t hi[3]) {
   for (int a = 0; a < dim; ++a) {
-    const int64_t wl = std::max<int64_t>(lo[a] - w, 0), wh = std::min<int64_t>(hi[a] + w, b.n[a] - 1);
+    const int64_t wl = std::max<int64_t>(lo[a] - w[a], 0), wh = std::min<int64_t>(hi[a] + w[a], b.n[a] - 1);
     if (wl < b.org[a] || wh >= b.org[a] + b.nb[a]) return false;
   }
   return true;
@@ -452,13 +479,18 @@ int ora_is_maxima_seed(const uint16_t* B, const int64_t n[3], const int64_t org[
                        int64_t z) {
   Box b{B, {n[0], n[1], n[2]}, {org[0], org[1], org[2]}, {nb[0], nb[1], nb[2]}};
   const int64_t p[3] = {x, y, z};
-  if (!window_inside(b, dim, w, p, p)) return -1;
-  return is_maxima_seed(b, dim, w, thr, x, y, z) ? 1 : 0;
+  const int w3[3] = {w, w, w};
+  if (!window_inside(b, dim, w3, p, p)) return -1;
+  return is_maxima_seed(b, dim, w3, thr, x, y, z) ? 1 : 0;
 }
 
-int ora_seeds_maxima(const uint16_t* B, const int64_t n[3], const int64_t org[3],
-                     const int64_t nb[3], const int64_t lo[3], const int64_t hi[3], int dim, int w,
-                     uint32_t thr, float* out_xyz, int64_t cap, int64_t* count) {
+// ora_seeds_maxima3: per-axis half-widths w3 and output in physical
+// coordinates (voxel index x scale, G28); ora_seeds_maxima: w3 = (w, w, w), scale 1.
+int ora_seeds_maxima3(const uint16_t* B, const int64_t n[3], const int64_t org[3],
+                      const int64_t nb[3], const int64_t lo[3], const int64_t hi[3], int dim,
+                      const int w3[3], const double scale[3], uint32_t thr, float* out_xyz,
+                      int64_t cap, int64_t* count) {
+  const int* w = w3;
   Box b{B, {n[0], n[1], n[2]}, {org[0], org[1], org[2]}, {nb[0], nb[1], nb[2]}};
   if (!window_inside(b, dim, w, lo, hi)) return ORA_SHAPE;
   const int64_t nplanes = hi[2] - lo[2] + 1;
@@ -478,12 +510,20 @@ int ora_seeds_maxima(const uint16_t* B, const int64_t n[3], const int64_t org[3]
   int64_t i = 0;
   for (auto& v : per_plane)
     for (int64_t lin : v) {
-      out_xyz[3 * i + 0] = (float)(lin % n[0]);
-      out_xyz[3 * i + 1] = (float)((lin / n[0]) % n[1]);
-      out_xyz[3 * i + 2] = (float)(lin / (n[0] * n[1]));
+      out_xyz[3 * i + 0] = (float)((double)(lin % n[0]) * scale[0]);
+      out_xyz[3 * i + 1] = (float)((double)((lin / n[0]) % n[1]) * scale[1]);
+      out_xyz[3 * i + 2] = (float)((double)(lin / (n[0] * n[1])) * scale[2]);
       ++i;
     }
   return ORA_OK;
+}
+
+int ora_seeds_maxima(const uint16_t* B, const int64_t n[3], const int64_t org[3],
+                     const int64_t nb[3], const int64_t lo[3], const int64_t hi[3], int dim, int w,
+                     uint32_t thr, float* out_xyz, int64_t cap, int64_t* count) {
+  const int w3[3] = {w, w, w};
+  const double one[3] = {1.0, 1.0, 1.0};
+  return ora_seeds_maxima3(B, n, org, nb, lo, hi, dim, w3, one, thr, out_xyz, cap, count);
 }
 
 // ---------------------------------------------------------------------------
@@ -638,6 +678,7 @@ static Image make_image(const uint16_t* v, const int64_t n[3], const int64_t org
   }
   img.dim = p->dim;
   img.iscale = p->iscale;
+  for (int a = 0; a < 3; ++a) img.scale[a] = p->scale[a] > 0.0 ? p->scale[a] : 1.0;
   return img;
 }
 
@@ -737,9 +778,11 @@ static void evolve_cell(const Image& img, const ora_params* p, const int64_t n[3
     }
     const double m = R + p->delta_R / 2.0;
     for (int a = 0; a < 3; ++a) {
+      // the domain in physical units: [0, (n_a - 1) scale_a] (G28)
+      const double L = (double)(n[a] - 1) * img.scale[a];
       double cd;
-      if ((double)(n[a] - 1) < 2.0 * m) cd = (double)(n[a] - 1) / 2.0;
-      else cd = clampd(c[a], m, (double)(n[a] - 1) - m);
+      if (L < 2.0 * m) cd = L / 2.0;
+      else cd = clampd(c[a], m, L - m);
       if (cd != c[a] && a < d) domained = true;
       c[a] = cd;
     }
@@ -855,15 +898,23 @@ static int32_t label_of(int dim, double x, double y, double z, const float* c_xy
   return (int32_t)(best + 1);
 }
 
-int ora_label(const int64_t n[3], int dim, int64_t z0, int64_t nz, const float* c_xyz,
-              const float* R, int64_t k, int32_t* labels) {
+// ora_label3: voxel (x, y, z) sits at the physical point (x sx, y sy, z sz) (G28).
+int ora_label3(const int64_t n[3], int dim, int64_t z0, int64_t nz, const double scale[3],
+               const float* c_xyz, const float* R, int64_t k, int32_t* labels) {
 #pragma omp parallel for schedule(dynamic, 1)
   for (int64_t zi = 0; zi < nz; ++zi)
     for (int64_t y = 0; y < n[1]; ++y)
       for (int64_t x = 0; x < n[0]; ++x)
         labels[(zi * n[1] + y) * n[0] + x] =
-            label_of(dim, (double)x, (double)y, (double)(z0 + zi), c_xyz, R, k);
+            label_of(dim, (double)x * scale[0], (double)y * scale[1], (double)(z0 + zi) * scale[2],
+                     c_xyz, R, k);
   return ORA_OK;
+}
+
+int ora_label(const int64_t n[3], int dim, int64_t z0, int64_t nz, const float* c_xyz,
+              const float* R, int64_t k, int32_t* labels) {
+  const double one[3] = {1.0, 1.0, 1.0};
+  return ora_label3(n, dim, z0, nz, one, c_xyz, R, k, labels);
 }
 
 int ora_label_points(int dim, const int64_t* pts_xyz, int64_t npts, const float* c_xyz,
