@@ -35,7 +35,7 @@
 extern "C" {
 #endif
 
-#define SNK_ABI_VERSION 2
+#define SNK_ABI_VERSION 3
 
 /* Status codes — mirror SPEC's exit scheme plus CUDA / capacity. */
 typedef enum {
@@ -85,13 +85,25 @@ enum { SNK_EST_MC = 0, SNK_EST_GRID = 1, SNK_EST_MC_CV = 2, SNK_EST_RAY = 3 };
  *   z_lo,nz_buf the device volume buffers hold global planes [z_lo, z_lo+nz_buf).
  *   own_z0/1    planes this rank owns: seeds are detected, and labels written,
  *               only for z in [own_z0, own_z1).  Single GPU: z_lo = own_z0 = 0,
- *               nz_buf = own_z1 = n[2]. */
+ *               nz_buf = own_z1 = n[2].
+ *   scale[3]    physical size of a voxel along each axis, in the contour's units
+ *               (reading G28): {1, 1, 1} (or zeros) = isotropic.  An
+ *               anisotropic raw volume is then used WITHOUT resampling: centres,
+ *               radii, seeds and detections are physical; a lookup at physical k
+ *               reads the grid at k_a / scale_a; the blur sigma of axis a is
+ *               sigma / scale_a voxels, the MAXIMA half-window floor(w / scale_a +
+ *               0.5) voxels; labels are decided at the voxels' physical positions.
+ *               Needs x extent % 8 == 0 (vectorised volume passes) and the brick
+ *               evolve kernel with 8 samples per thread (N = 256 x warps); the
+ *               grid estimator and the gradient-magnitude image term are isotropic
+ *               only. */
 typedef struct snk_grid {
   int32_t dim;
   int32_t _pad0;
   int64_t n[3];
   int64_t z_lo, nz_buf;
   int64_t own_z0, own_z1;
+  double scale[3];
 } snk_grid;
 
 /* Parameters (S:259-263 SwarmConfig; defaults in DESIGN.md §3):

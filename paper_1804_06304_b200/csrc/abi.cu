@@ -40,6 +40,8 @@ static int32_t validate_grid(const snk_grid* g) {
   if (g->dim == 3 && g->nz_buf < 2) return fail(SNK_SHAPE, "3D buffers need at least 2 planes");
   if (g->own_z0 < g->z_lo || g->own_z1 > g->z_lo + g->nz_buf || g->own_z0 > g->own_z1)
     return fail(SNK_SHAPE, "owned planes must lie inside the buffer");
+  for (int a = 0; a < 3; ++a)
+    if (!(g->scale[a] >= 0.0) || g->scale[a] > 1e6) return fail(SNK_SHAPE, "scale must be >= 0 (0 = 1)");
   const double nvox = (double)g->n[0] * (double)g->n[1] * (double)g->nz_buf;
   if (nvox >= 4294967296.0) return fail(SNK_SHAPE, "buffer exceeds 2^32 voxels; use z-slabs");
   return SNK_OK;
@@ -81,6 +83,11 @@ static int32_t validate_params(const snk_params* p, int dim) {
 static int32_t validate(const snk_grid* g, const snk_params* p) {
   SNK_TRY(validate_grid(g));
   SNK_TRY(validate_params(p, g->dim));
+  if (grid_aniso(g)) {
+    if (g->n[0] % 8 != 0) return fail(SNK_SHAPE, "anisotropic grids need an x extent divisible by 8");
+    if (p->estimator == SNK_EST_GRID) return fail(SNK_CONFIG, "the grid estimator is isotropic only");
+    if (p->image_term == SNK_IMAGE_GRADMAG) return fail(SNK_CONFIG, "the gradient-magnitude term is isotropic only");
+  }
   return SNK_OK;
 }
 
@@ -391,6 +398,6 @@ int32_t snk_run(int32_t dim, const int64_t n_raw[3], const double spacing[3],
 
 }  // extern "C"
 
-static_assert(sizeof(snk_grid) == 64, "snk_grid layout is part of the ABI");
+static_assert(sizeof(snk_grid) == 88, "snk_grid layout is part of the ABI");
 static_assert(sizeof(snk_params) == 136, "snk_params layout is part of the ABI");
 static_assert(sizeof(snk_cell) == 48, "snk_cell layout is part of the ABI");

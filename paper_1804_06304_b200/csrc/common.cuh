@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cmath>
 #include <string>
 
 #include "../../include/snk.h"
@@ -46,6 +47,18 @@ constexpr double kRho2 = 0.7071067811865476;
 constexpr double kRhoSq3 = 0.6299605249474366;
 constexpr double kRhoSq2 = 0.5;
 inline double rho_of(int dim) { return dim == 3 ? kRho3 : kRho2; }
+
+// physical voxel size of axis a (G28); 0 means 1
+inline double grid_scale(const snk_grid* g, int a) { return g->scale[a] > 0.0 ? g->scale[a] : 1.0; }
+inline bool grid_aniso(const snk_grid* g) {
+  for (int a = 0; a < g->dim; ++a)
+    if (grid_scale(g, a) != 1.0) return true;
+  return false;
+}
+// the MAXIMA half-window of axis a: floor(w / scale_a + 0.5) voxels (G28)
+inline int axis_window(const snk_grid* g, int w, int a) {
+  return (int)std::floor((double)w / grid_scale(g, a) + 0.5);
+}
 
 // ---------------------------------------------------------------- workspace
 // A bump allocator over the caller's workspace; 256-byte aligned slices.

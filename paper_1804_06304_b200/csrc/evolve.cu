@@ -62,12 +62,20 @@ struct EvoParams {
   int it0, it1;                  // iterations this launch runs (1 .. T + 1 for a whole run)
   const snk_cell* state;         // non-null: continue these records (periodic culling, G25)
   int dom_small;                 // some axis has n - 1 < 2 (r_max + dR/2)
+  float isc[3];                  // 1 / scale: physical -> raw grid coordinates (G28)
+  float dom1[3];                 // physical extent (n - 1) scale of each axis (= n - 1 isotropic)
   uint32_t rk0[10], rk1[10];     // Philox round keys (seed + r * Weyl)
 };
 
 struct Acc {
   float a0, cx, cy, cz, aR;
 };
+
+// EST template values: the estimator in bits 0-1 (SNK_EST_MC, _MC_CV, _RAY) and
+// bit 2 = anisotropic grid sampled in physical coordinates (G28)
+constexpr int kAniso = 4;
+__host__ __device__ constexpr int est_kind(int e) { return e & 3; }
+__host__ __device__ constexpr bool est_aniso(int e) { return (e & kAniso) != 0; }
 
 __device__ __forceinline__ Acc acc_add(const Acc& l, const Acc& r) {
   return Acc{__fadd_rn(l.a0, r.a0), __fadd_rn(l.cx, r.cx), __fadd_rn(l.cy, r.cy),
@@ -205,7 +213,7 @@ __device__ __forceinline__ Draw finish_draw(const CellIt& C, const Dir& d) {
   r.ox = d.ox;
   r.oy = d.oy;
   r.oz = d.oz;
-  if (EST == SNK_EST_RAY) r.t = __fmul_rn(C.rho_s, d.L);
+  if (est_kind(EST) == SNK_EST_RAY) r.t = __fmul_rn(C.rho_s, d.L);
   else r.t = D == 3 ? ex2_approx(__fmaf_rn(d.L, 0.333333343f, C.lg2_rho_s)) : __fmul_rn(C.rho_s, d.L);
   return r;
 }
@@ -245,8 +253,8 @@ __device__ __forceinline__ void draw_dirs_ray(const EvoParams& P, const CellIt& 
 // (control variate, G21), I(k) t^(d-1) (ray march, the polar volume element).
 template <int D, int EST>
 __device__ __forceinline__ float est_value(const CellIt& C, float tri, float t) {
-  if (EST == SNK_EST_MC_CV) return __fsub_rn(tri, C.ic);
-  if (EST == SNK_EST_RAY) return __fmul_rn(tri, D == 3 ? __fmul_rn(t, t) : t);
+  if (est_kind(EST) == SNK_EST_MC_CV) return __fsub_rn(tri, C.ic);
+  if (est_kind(EST) == SNK_EST_RAY) return __fmul_rn(tri, D == 3 ? __fmul_rn(t, t) : t);
   return tri;
 }
 
@@ -437,8 +445,14 @@ __device__ __forceinline__ float gather_tri(const EvoParams& P, const CellIt& C,
 template <int D, int MODE, int S, int EST = 0>
 __device__ __forceinline__ Acc sample_leaf(const EvoParams& P, const CellIt& C, const Draw& d,
                                            const uint16_t* brick, uint32_t& halo) {
-  const float tri = gather_tri<D, MODE, S>(P, C, __fmaf_rn(d.t, d.ox, C.cx), __fmaf_rn(d.t, d.oy, C.cy),
-                                           D == 3 ? __fmaf_rn(d.t, d.oz, C.cz) : 0.0f, brick, halo);
+  float kx = __fmaf_rn(d.t, d.ox, C.cx), ky = __fmaf_rn(d.t, d.oy, C.cy);
+  float kz = D == 3 ? __fmaf_rn(d.t, d.oz, C.cz) : 0.0f;
+  if (est_aniso(EST)) {   // physical -> raw grid coordinates (G28)
+    kx = __fmul_rn(kx, P.isc[0]);
+    ky = __fmul_rn(ky, P.isc[1]);
+    kz = __fmul_rn(kz, P.isc[2]);
+  }
+  const float tri = gather_tri<D, MODE, S>(P, C, kx, ky, kz, brick, halo);
   return leaves(P, C, d, est_value<D, EST>(C, tri, d.t), D == 3);
 }
 
@@ -482,10 +496,17 @@ __device__ __forceinline__ Acc2 sample_pair_fast(const EvoParams& P, const CellI
   const float2 ox = make_float2(d0.ox, d1.ox), oy = make_float2(d0.oy, d1.oy);
   const float2 oz = make_float2(d0.oz, d1.oz);
   uint32_t rx0, rx1, ry0, ry1, rz0 = kMagicBits, rz1 = kMagicBits;
-  const float2 fx = split2(__ffma2_rn(t, ox, bc2(C.cx)), &rx0, &rx1);
-  const float2 fy = split2(__ffma2_rn(t, oy, bc2(C.cy)), &ry0, &ry1);
+  float2 kx = __ffma2_rn(t, ox, bc2(C.cx)), ky = __ffma2_rn(t, oy, bc2(C.cy));
+  float2 kz = D == 3 ? __ffma2_rn(t, oz, bc2(C.cz)) : bc2(0.0f);
+  if (est_aniso(EST)) {   // physical -> raw grid coordinates (G28)
+    kx = __fmul2_rn(kx, bc2(P.isc[0]));
+    ky = __fmul2_rn(ky, bc2(P.isc[1]));
+    kz = __fmul2_rn(kz, bc2(P.isc[2]));
+  }
+  const float2 fx = split2(kx, &rx0, &rx1);
+  const float2 fy = split2(ky, &ry0, &ry1);
   float2 fz = bc2(0.0f);
-  if (D == 3) fz = split2(__ffma2_rn(t, oz, bc2(C.cz)), &rz0, &rz1);
+  if (D == 3) fz = split2(kz, &rz0, &rz1);
   uint32_t li0 = ry0 * SX + rx0, li1 = ry1 * SX + rx1;
   if (D == 3) { li0 += rz0 * SP; li1 += rz1 * SP; }
   li0 -= C.boff;
@@ -506,8 +527,8 @@ __device__ __forceinline__ Acc2 sample_pair_fast(const EvoParams& P, const CellI
     const float2 v111 = make_float2(mag(p[SP + SX + 1]), mag(q[SP + SX + 1]));
     tri = lerp2(tri, lerp2(lerp2(v001, v101, fx), lerp2(v011, v111, fx), fy), fz);
   }
-  if (EST == SNK_EST_MC_CV) tri = __fadd2_rn(tri, bc2(-C.ic));
-  if (EST == SNK_EST_RAY) tri = __fmul2_rn(tri, D == 3 ? __fmul2_rn(t, t) : t);
+  if (est_kind(EST) == SNK_EST_MC_CV) tri = __fadd2_rn(tri, bc2(-C.ic));
+  if (est_kind(EST) == SNK_EST_RAY) tri = __fmul2_rn(tri, D == 3 ? __fmul2_rn(t, t) : t);
   // leaves(): the saturating ramps stay scalar (FFMA.SAT), the rest is paired
   const float2 uo = make_float2(__saturatef(__fmaf_rn(d0.t, P.inv_dR, C.a)),
                                 __saturatef(__fmaf_rn(d1.t, P.inv_dR, C.a)));
@@ -782,7 +803,7 @@ __device__ __forceinline__ bool cell_update(const EvoParams& P, CellState& s, co
                                             const Acc& sum, int it) {
   const float rs = C.rho_s;
   const float vol = D == 3 ? __fmul_rn(__fmul_rn(rs, rs), rs) : __fmul_rn(rs, rs);
-  const float scale = GRID ? P.vscale : (EST == SNK_EST_RAY ? __fmul_rn(P.vscale, rs) : __fmul_rn(P.vscale, vol));
+  const float scale = GRID ? P.vscale : (est_kind(EST) == SNK_EST_RAY ? __fmul_rn(P.vscale, rs) : __fmul_rn(P.vscale, vol));
   const float A0 = __fmul_rn(sum.a0, scale);
   const float twoR = __fmul_rn(2.0f, s.R);
   const float gden = D == 3 ? __fmul_rn(__fmul_rn(twoR, twoR), twoR) : __fmul_rn(twoR, twoR);
@@ -813,18 +834,18 @@ __device__ __forceinline__ bool cell_update(const EvoParams& P, CellState& s, co
   if (NB) {
     const float m2 = __fmul_rn(2.0f, m);
     const bool small = P.dom_small != 0;
-    dx = (small && P.fnx1 < m2) ? __fmul_rn(0.5f, P.fnx1) : clampf(lx, m, __fsub_rn(P.fnx1, m));
-    dy = (small && P.fny1 < m2) ? __fmul_rn(0.5f, P.fny1) : clampf(ly, m, __fsub_rn(P.fny1, m));
-    if (D == 3) dz = (small && P.fnz1 < m2) ? __fmul_rn(0.5f, P.fnz1) : clampf(lz, m, __fsub_rn(P.fnz1, m));
+    dx = (small && P.dom1[0] < m2) ? __fmul_rn(0.5f, P.dom1[0]) : clampf(lx, m, __fsub_rn(P.dom1[0], m));
+    dy = (small && P.dom1[1] < m2) ? __fmul_rn(0.5f, P.dom1[1]) : clampf(ly, m, __fsub_rn(P.dom1[1], m));
+    if (D == 3) dz = (small && P.dom1[2] < m2) ? __fmul_rn(0.5f, P.dom1[2]) : clampf(lz, m, __fsub_rn(P.dom1[2], m));
   } else if (P.dom_small) {
     const float m2 = __fmul_rn(2.0f, m);
-    dx = P.fnx1 < m2 ? __fmul_rn(0.5f, P.fnx1) : clampf(lx, m, __fsub_rn(P.fnx1, m));
-    dy = P.fny1 < m2 ? __fmul_rn(0.5f, P.fny1) : clampf(ly, m, __fsub_rn(P.fny1, m));
-    if (D == 3) dz = P.fnz1 < m2 ? __fmul_rn(0.5f, P.fnz1) : clampf(lz, m, __fsub_rn(P.fnz1, m));
+    dx = P.dom1[0] < m2 ? __fmul_rn(0.5f, P.dom1[0]) : clampf(lx, m, __fsub_rn(P.dom1[0], m));
+    dy = P.dom1[1] < m2 ? __fmul_rn(0.5f, P.dom1[1]) : clampf(ly, m, __fsub_rn(P.dom1[1], m));
+    if (D == 3) dz = P.dom1[2] < m2 ? __fmul_rn(0.5f, P.dom1[2]) : clampf(lz, m, __fsub_rn(P.dom1[2], m));
   } else {
-    dx = clampf(lx, m, __fsub_rn(P.fnx1, m));
-    dy = clampf(ly, m, __fsub_rn(P.fny1, m));
-    if (D == 3) dz = clampf(lz, m, __fsub_rn(P.fnz1, m));
+    dx = clampf(lx, m, __fsub_rn(P.dom1[0], m));
+    dy = clampf(ly, m, __fsub_rn(P.dom1[1], m));
+    if (D == 3) dz = clampf(lz, m, __fsub_rn(P.dom1[2], m));
   }
   if (NB) {
     const bool fin = it == P.T + 1;   // E_final only: no update
@@ -998,17 +1019,20 @@ struct BrickCtl {
   // Fast test: the tap box lies in the brick iff c - ext >= in_lo and c + ext <
   // in_hi per axis (exact for the integer bounds); only set for a brick inside
   // the volume, so containment also means no clamping is needed.
-  __device__ __forceinline__ int prepare(uint16_t* brick, const EvoParams& P, const float c[3],
+  // ANISO (G28): c and rho_s are physical; the box is taken in raw grid units
+  template <bool ANISO = false>
+  __device__ __forceinline__ int prepare(uint16_t* brick, const EvoParams& P, const float cp[3],
                                          float rho_s) {
     constexpr int EXT[3] = {brick_sx(S), S, S};   // brick extent per axis
     // bounding box of the sampled ball, with a margin for the fp32 rounding of t and k
-    const float ext = __fmaf_rn(rho_s, 1.0001f, 0.01f);
     float vlo[3], vhi[3];
     bool fast = true;
 #pragma unroll
     for (int a = 0; a < D; ++a) {
-      vlo[a] = __fsub_rn(c[a], ext);
-      vhi[a] = __fadd_rn(c[a], ext);
+      const float c = ANISO ? __fmul_rn(cp[a], P.isc[a]) : cp[a];
+      const float ext = __fmaf_rn(ANISO ? __fmul_rn(rho_s, P.isc[a]) : rho_s, 1.0001f, 0.01f);
+      vlo[a] = __fsub_rn(c, ext);
+      vhi[a] = __fadd_rn(c, ext);
       fast &= vlo[a] >= in_lo[a] && vhi[a] < in_hi[a];
     }
     if (fast) return 0;
@@ -1071,20 +1095,23 @@ __global__ void __launch_bounds__(32 * W, W == 4 ? SNK_BRICK_MINB4 : SNK_BRICK_M
   const uint32_t j0 = (uint32_t)((wsub * 32 + lane) * B);
   Dir dir[PIPE ? CH : 1];
   if constexpr (PIPE) {
-    if constexpr (EST == SNK_EST_RAY) draw_dirs_ray<D>(P, cell_iter(P, s, P.it0), j0 / 8u, dir);
+    if constexpr (est_kind(EST) == SNK_EST_RAY) draw_dirs_ray<D>(P, cell_iter(P, s, P.it0), j0 / 8u, dir);
     else draw_dirs<D, CH>(P, cell_iter(P, s, P.it0), j0, dir);
   }
   for (int it = P.it0; it <= P.it1; ++it) {
     CellIt C = cell_iter(P, s, it);
     const float c[3] = {s.cx, s.cy, s.cz};
-    const int mode = bk.prepare(brick, P, c, C.rho_s);
+    const int mode = bk.template prepare<est_aniso(EST)>(brick, P, c, C.rho_s);
     Acc part;
     C.boff = bk.boff;
-    if constexpr (EST == SNK_EST_MC_CV) {
+    if constexpr (est_kind(EST) == SNK_EST_MC_CV) {
       // I(c): the same d-linear lookup as a sample at t = 0
-      if (mode == 0) C.ic = gather_tri<D, G_BRICK_FAST, S>(P, C, C.cx, C.cy, C.cz, brick, halo);
-      else if (mode == 1) C.ic = gather_tri<D, G_BRICK_CLAMP, S>(P, C, C.cx, C.cy, C.cz, brick, halo);
-      else C.ic = gather_tri<D, SLAB ? G_GLOBAL_SLAB : G_GLOBAL, S>(P, C, C.cx, C.cy, C.cz, brick, halo);
+      const float qx = est_aniso(EST) ? __fmul_rn(C.cx, P.isc[0]) : C.cx;
+      const float qy = est_aniso(EST) ? __fmul_rn(C.cy, P.isc[1]) : C.cy;
+      const float qz = est_aniso(EST) ? __fmul_rn(C.cz, P.isc[2]) : C.cz;
+      if (mode == 0) C.ic = gather_tri<D, G_BRICK_FAST, S>(P, C, qx, qy, qz, brick, halo);
+      else if (mode == 1) C.ic = gather_tri<D, G_BRICK_CLAMP, S>(P, C, qx, qy, qz, brick, halo);
+      else C.ic = gather_tri<D, SLAB ? G_GLOBAL_SLAB : G_GLOBAL, S>(P, C, qx, qy, qz, brick, halo);
     }
     if constexpr (PIPE) {
       if (mode == 0) {
@@ -1122,7 +1149,7 @@ __global__ void __launch_bounds__(32 * W, W == 4 ? SNK_BRICK_MINB4 : SNK_BRICK_M
       Cn.p0 = s.q0 ^ (uint32_t)(it + 1);
       Cn.p1 = s.q1;
       Cn.p3 = s.q3;
-      if constexpr (EST == SNK_EST_RAY) draw_dirs_ray<D>(P, Cn, j0 / 8u, dir);
+      if constexpr (est_kind(EST) == SNK_EST_RAY) draw_dirs_ray<D>(P, Cn, j0 / 8u, dir);
       else draw_dirs<D, CH>(P, Cn, j0, dir);
       if (cell_update<D, false, EST, true>(P, s, C, sum, it)) break;
     } else if constexpr (PIPE && SNK_BRICK_PIPE == 2) {
@@ -1140,7 +1167,7 @@ __global__ void __launch_bounds__(32 * W, W == 4 ? SNK_BRICK_MINB4 : SNK_BRICK_M
       Cn.p0 = s.q0 ^ (uint32_t)(it + 1);
       Cn.p1 = s.q1;
       Cn.p3 = s.q3;
-      if constexpr (EST == SNK_EST_RAY) draw_dirs_ray<D>(P, Cn, j0 / 8u, dir);
+      if constexpr (est_kind(EST) == SNK_EST_RAY) draw_dirs_ray<D>(P, Cn, j0 / 8u, dir);
       else draw_dirs<D, CH>(P, Cn, j0, dir);
     } else if constexpr (PIPE) {
       const bool done = it == P.T + 1;
@@ -1159,7 +1186,7 @@ __global__ void __launch_bounds__(32 * W, W == 4 ? SNK_BRICK_MINB4 : SNK_BRICK_M
       Cn.p0 = s.q0 ^ (uint32_t)(it + 1);
       Cn.p1 = s.q1;
       Cn.p3 = s.q3;
-      if constexpr (EST == SNK_EST_RAY) draw_dirs_ray<D>(P, Cn, j0 / 8u, dir);
+      if constexpr (est_kind(EST) == SNK_EST_RAY) draw_dirs_ray<D>(P, Cn, j0 / 8u, dir);
       else draw_dirs<D, CH>(P, Cn, j0, dir);
       __syncthreads();
       if (wsub != 0) { s.cx = bc[0]; s.cy = bc[1]; s.cz = bc[2]; s.R = bc[3]; }
@@ -1465,9 +1492,14 @@ int32_t evolve_impl(const snk_grid* g, const snk_params* p, const uint16_t* d_im
   P.it0 = it0 > 0 ? it0 : 1;
   P.it1 = it1 > 0 ? it1 : p->max_iters + 1;
   P.state = resume ? d_cells : nullptr;
+  for (int a = 0; a < 3; ++a) {
+    const double sc = grid_scale(g, a);
+    P.isc[a] = (float)(1.0 / sc);
+    P.dom1[a] = (float)((double)(g->n[a] - 1) * sc);   // = fn1 exactly when isotropic
+  }
   {
     const double m2 = 2.0 * ((double)P.r_max + (double)P.half_dR) * (1.0 + 1e-6) + 1e-3;   // conservative
-    P.dom_small = (double)P.fnx1 < m2 || (double)P.fny1 < m2 || (D == 3 && (double)P.fnz1 < m2);
+    P.dom_small = (double)P.dom1[0] < m2 || (double)P.dom1[1] < m2 || (D == 3 && (double)P.dom1[2] < m2);
   }
   uint32_t k0 = (uint32_t)(p->seed & 0xffffffffu), k1 = (uint32_t)(p->seed >> 32);
   for (int r = 0; r < 10; ++r) {
@@ -1486,6 +1518,23 @@ int32_t evolve_impl(const snk_grid* g, const snk_params* p, const uint16_t* d_im
     P.vscale = (float)p->intensity_scale;
     if (D == 3) return slab ? launch_grid<3, 8, kS3, true>(P, st) : launch_grid<3, 8, kS3, false>(P, st);
     return launch_grid<2, 8, 64, false>(P, st);
+  }
+  if (grid_aniso(g)) {
+    // physical-coordinate sampling on the raw anisotropic grid (G28): the brick
+    // kernel, 4 warps x 8 samples per thread, 3D
+    if (D != 3 || g->n[0] % 2 != 0 || (reinterpret_cast<uintptr_t>(d_image) & 3) != 0 || p->kernel_variant == 1 ||
+        !(p->cta_warps == 0 || p->cta_warps == 4) || p->n_samples != 1024 || p->estimator == SNK_EST_GRID)
+      return fail(SNK_CONFIG, "anisotropic grids: 3D brick kernel with 4 warps and n_samples = 1024 (MC / CV / ray)");
+    if (p->estimator == SNK_EST_RAY) {
+      const double pi = 3.14159265358979323846;
+      P.vscale = (float)(p->intensity_scale * 4.0 * pi / (double)p->n_samples);
+    }
+    constexpr int A0 = kAniso, A2 = kAniso | SNK_EST_MC_CV, A3 = kAniso | SNK_EST_RAY;
+    switch (p->estimator) {
+      case SNK_EST_MC_CV: return slab ? launch_brick<3, 4, kS3, true, 8, 0, A2>(P, st) : launch_brick<3, 4, kS3, false, 8, 0, A2>(P, st);
+      case SNK_EST_RAY: return slab ? launch_brick<3, 4, kS3, true, 8, 0, A3>(P, st) : launch_brick<3, 4, kS3, false, 8, 0, A3>(P, st);
+      default: return slab ? launch_brick<3, 4, kS3, true, 8, 0, A0>(P, st) : launch_brick<3, 4, kS3, false, 8, 0, A0>(P, st);
+    }
   }
   if (p->estimator == SNK_EST_MC_CV || p->estimator == SNK_EST_RAY) {
     // brick kernel with pipelined draws, 8 samples (one ray) per thread

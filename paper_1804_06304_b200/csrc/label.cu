@@ -28,6 +28,7 @@ struct TileGrid {
   int z0, z1;          // owned planes [z0, z1)
   double rho2;         // rho^2 (G19)
   double rho;          // bbox radius factor
+  double sc[3];        // physical voxel size per axis (G28; 1 isotropic)
 };
 
 __device__ __forceinline__ bool tile_range(const snk_cell& d, const TileGrid& G, int lo[3], int hi[3]) {
@@ -38,8 +39,9 @@ __device__ __forceinline__ bool tile_range(const snk_cell& d, const TileGrid& G,
   const int base[3] = {0, 0, G.z0};
   const int tdim[3] = {G.tx, G.ty, G.tz};
   for (int a = 0; a < 3; ++a) {
-    const int vlo = max((int)ceil((double)c[a] - r), base[a]);
-    const int vhi = min((int)floor((double)c[a] + r), n[a] - 1);
+    // raw voxel range of the ball (physical c and r divided by the voxel size, G28)
+    const int vlo = max((int)ceil(((double)c[a] - r) / G.sc[a]), base[a]);
+    const int vhi = min((int)floor(((double)c[a] + r) / G.sc[a]), n[a] - 1);
     if (vlo > vhi) return false;
     lo[a] = (vlo - base[a]) / tdim[a];
     hi[a] = (vhi - base[a]) / tdim[a];
@@ -94,14 +96,11 @@ __global__ void __launch_bounds__(kThreads) label_kernel(const snk_cell* __restr
     yv[k] = D == 3 ? ty * G.ty + ly : ty * G.ty + ly + k * kTY;
     zv[k] = D == 3 ? G.z0 + tz * G.tz + k : G.z0;
   }
-  // the best candidate so far as (d2, thr): its key d2/thr (an IEEE division)
-  // is only needed when a second detection contains the voxel (rare: overlaps
-  // of inner balls), so most voxels never divide
   int best[NV];
-  double best_d2[NV], best_thr[NV];
+  double best_key[NV];
 #pragma unroll
-  for (int k = 0; k < NV; ++k) { best[k] = -1; best_d2[k] = 0.0; best_thr[k] = 1.0; }
-  const double px = (double)x;
+  for (int k = 0; k < NV; ++k) { best[k] = -1; best_key[k] = 0.0; }
+  const double px = __dmul_rn((double)x, G.sc[0]);   // physical voxel position (G28; exact for scale 1)
   const int64_t e0 = offsets[tile], e1 = offsets[tile + 1];
   for (int64_t s = e0; s < e1; s += kStage) {
     const int cnt = (int)(e1 - s < kStage ? e1 - s : kStage);
@@ -122,41 +121,31 @@ __global__ void __launch_bounds__(kThreads) label_kernel(const snk_cell* __restr
       const double dx = __dsub_rn(px, s_c[0][k]);
       const double dx2 = __dmul_rn(dx, dx);
       if (D == 3) {
-        const double dy = __dsub_rn((double)yv[0], s_c[1][k]);
+        const double dy = __dsub_rn(__dmul_rn((double)yv[0], G.sc[1]), s_c[1][k]);
         const double dxy = __dadd_rn(dx2, __dmul_rn(dy, dy));   // d2 = (dx^2 + dy^2) + dz^2
         if (!(dxy <= thr)) continue;                             // dz^2 >= 0: no plane can qualify
 #pragma unroll
         for (int v = 0; v < NV; ++v) {
-          const double dz = __dsub_rn((double)zv[v], s_c[2][k]);
+          const double dz = __dsub_rn(__dmul_rn((double)zv[v], G.sc[2]), s_c[2][k]);
           const double d2 = __dadd_rn(dxy, __dmul_rn(dz, dz));
           if (d2 <= thr) {
-            bool take = best[v] < 0;
-            if (!take) {
-              const double key = __ddiv_rn(d2, thr), bkey = __ddiv_rn(best_d2[v], best_thr[v]);
-              take = key < bkey || (key == bkey && i < best[v]);
-            }
-            if (take) {
+            const double key = __ddiv_rn(d2, thr);
+            if (best[v] < 0 || key < best_key[v] || (key == best_key[v] && i < best[v])) {
               best[v] = i;
-              best_d2[v] = d2;
-              best_thr[v] = thr;
+              best_key[v] = key;
             }
           }
         }
       } else {
 #pragma unroll
         for (int v = 0; v < NV; ++v) {
-          const double dy = __dsub_rn((double)yv[v], s_c[1][k]);
+          const double dy = __dsub_rn(__dmul_rn((double)yv[v], G.sc[1]), s_c[1][k]);
           const double d2 = __dadd_rn(dx2, __dmul_rn(dy, dy));
           if (d2 <= thr) {
-            bool take = best[v] < 0;
-            if (!take) {
-              const double key = __ddiv_rn(d2, thr), bkey = __ddiv_rn(best_d2[v], best_thr[v]);
-              take = key < bkey || (key == bkey && i < best[v]);
-            }
-            if (take) {
+            const double key = __ddiv_rn(d2, thr);
+            if (best[v] < 0 || key < best_key[v] || (key == best_key[v] && i < best[v])) {
               best[v] = i;
-              best_d2[v] = d2;
-              best_thr[v] = thr;
+              best_key[v] = key;
             }
           }
         }
@@ -183,6 +172,7 @@ TileGrid make_grid(const snk_grid* g) {
   G.nt[2] = (int)ceil_div(std::max(G.z1 - G.z0, 0), G.tz);
   G.rho2 = g->dim == 3 ? kRhoSq3 : kRhoSq2;
   G.rho = rho_of(g->dim);
+  for (int a = 0; a < 3; ++a) G.sc[a] = grid_scale(g, a);
   return G;
 }
 
@@ -190,7 +180,7 @@ size_t tiles_per_det_bound(const snk_grid* g, const snk_params* p, const TileGri
   const double r = G.rho * std::max(p->r_max, p->r0) * 1.000001 + 1e-4;
   size_t b = 1;
   const int td[3] = {G.tx, G.ty, G.tz};
-  for (int a = 0; a < g->dim; ++a) b *= (size_t)(std::floor(2 * r / td[a]) + 2);
+  for (int a = 0; a < g->dim; ++a) b *= (size_t)(std::floor(2 * r / (td[a] * grid_scale(g, a))) + 2);
   return b;
 }
 

@@ -48,6 +48,7 @@ struct MaxArgs {
   int w, dim;
   uint32_t thr;
   int64_t v0, v1;      // buffer-linear voxel range scanned: own planes
+  int wx, wy, wz;      // per-axis half-windows (the tie check; = w unless anisotropic, G28)
 };
 
 // Seed predicate at buffer-linear index v (3D/2D), §8(c) O4.
@@ -183,9 +184,9 @@ struct FusedArgs {
 };
 
 __device__ __forceinline__ bool tie_free(const MaxArgs& A, int x, int y, int z, uint16_t b) {
-  const int z0 = A.dim == 3 ? max(z - A.w, 0) : z;
-  const int y0 = max(y - A.w, 0), y1 = min(y + A.w, A.ny - 1);
-  const int x0 = max(x - A.w, 0), x1 = min(x + A.w, A.nx - 1);
+  const int z0 = A.dim == 3 ? max(z - A.wz, 0) : z;
+  const int y0 = max(y - A.wy, 0), y1 = min(y + A.wy, A.ny - 1);
+  const int x0 = max(x - A.wx, 0), x1 = min(x + A.wx, A.nx - 1);
   for (int zz = z0; zz <= z; ++zz)
     for (int yy = y0; yy <= (zz == z ? y : y1); ++yy) {
       const uint16_t* row = A.B + ((int64_t)(zz - A.z_lo) * A.ny + yy) * A.nx;
@@ -322,7 +323,8 @@ __global__ void __launch_bounds__(1024) bits_count_kernel(const uint32_t* bits, 
 __global__ void __launch_bounds__(1024) bits_write_kernel(const uint32_t* bits, int64_t nwords, int wpr,
                                                           int nx, int ny, int own_z0,
                                                           const int64_t* offsets, float* seeds,
-                                                          int64_t cap, int linear) {
+                                                          int64_t cap, int linear, double sx = 1.0,
+                                                          double sy = 1.0, double sz = 1.0) {
   __shared__ int ws[32];
   const int64_t i = (int64_t)blockIdx.x * 1024 + threadIdx.x;
   const uint32_t word = i < nwords ? bits[i] : 0u;
@@ -355,10 +357,10 @@ __global__ void __launch_bounds__(1024) bits_write_kernel(const uint32_t* bits, 
       const int b = __ffs(m) - 1;
       m &= m - 1;
       const int64_t v = i * 32 + b;
-      if (o < cap) {
-        seeds[3 * o + 0] = (float)(v % nx);
-        seeds[3 * o + 1] = (float)((v / nx) % ny);
-        seeds[3 * o + 2] = (float)(v / plane + own_z0);
+      if (o < cap) {   // physical coordinates (index x scale, G28; exact for scale 1)
+        seeds[3 * o + 0] = (float)((double)(v % nx) * sx);
+        seeds[3 * o + 1] = (float)((double)((v / nx) % ny) * sy);
+        seeds[3 * o + 2] = (float)((double)(v / plane + own_z0) * sz);
       }
       ++o;
     }
@@ -431,71 +433,6 @@ __global__ void __launch_bounds__(256) maxima_pred8_kernel(MaxArgs A, const uint
   mask[t] = (uint8_t)bits;
 }
 
-// 3D, as maxima_pred8_kernel<3, W> but column-streamed: a thread owns one
-// 8-voxel group of a row and walks kPZ owned planes with the 2W+1 XY planes of
-// its z window in registers (packed u16x2, VIMNMX), so each XY plane is read
-// (kPZ + 2W)/kPZ times instead of 2W+1 (the flat fold re-read its window
-// through L2: 43.5 GB of DRAM reads per C4 step for 4.3 GB of data).
-constexpr int kPZ = 32;
-
-__device__ __forceinline__ uint4 vmax4s(uint4 a, uint4 b) {
-  return make_uint4(__vmaxu2(a.x, b.x), __vmaxu2(a.y, b.y), __vmaxu2(a.z, b.z), __vmaxu2(a.w, b.w));
-}
-
-template <int W>
-__global__ void __launch_bounds__(256) maxima_predz_kernel(MaxArgs A, const uint16_t* __restrict__ XY,
-                                                           uint8_t* __restrict__ mask, int own_z0, int own_z1) {
-  constexpr int K = 2 * W + 1;
-  const int nc = A.nx >> 3;
-  const int64_t ncols = (int64_t)nc * A.ny;
-  const int nzc = (own_z1 - own_z0 + kPZ - 1) / kPZ;
-  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= ncols * nzc) return;
-  const int64_t col = t % ncols;
-  const int xc = (int)(col % nc), y = (int)(col / nc);
-  const int z0 = own_z0 + (int)(t / ncols) * kPZ, z1 = min(z0 + kPZ, own_z1);
-  const uint4* xy = reinterpret_cast<const uint4*>(XY) + col;
-  const uint4* bb = reinterpret_cast<const uint4*>(A.B) + col;
-  auto load = [&](int q) -> uint4 {   // XY of global plane q; planes outside the volume: 0
-    if (q < 0 || q >= A.nz_glob) return make_uint4(0u, 0u, 0u, 0u);
-    return __ldg(xy + (int64_t)(q - A.z_lo) * ncols);
-  };
-  uint4 win[K - 1];   // win[j] = plane zb - W + j; a block's K new planes load together
-#pragma unroll
-  for (int j = 0; j < K - 1; ++j) win[j] = load(z0 - W + j);
-  for (int zb = z0; zb < z1; zb += K) {
-    uint4 nxt[K];
-#pragma unroll
-    for (int s = 0; s < K; ++s) nxt[s] = load(zb + W + s);
-#pragma unroll
-    for (int s = 0; s < K; ++s) {
-      const int zo = zb + s;
-      if (zo < z1) {
-        uint4 mq = s < K - 1 ? win[s] : nxt[s - (K - 1)];
-#pragma unroll
-        for (int i = 1; i < K; ++i) {
-          const int j = s + i;
-          mq = vmax4s(mq, j < K - 1 ? win[j] : nxt[j - (K - 1)]);
-        }
-        uint32_t b[8], m[8];
-        unpack8s(__ldg(bb + (int64_t)(zo - A.z_lo) * ncols), b);
-        unpack8s(mq, m);
-        uint32_t bits = 0;
-#pragma unroll
-        for (int k = 0; k < 8; ++k)
-          if (b[k] >= A.thr && b[k] == m[k]) bits |= 1u << k;
-        if (bits) {
-          for (int k = 0; k < 8; ++k)
-            if ((bits >> k & 1u) && !tie_free(A, xc * 8 + k, y, zo, (uint16_t)b[k])) bits &= ~(1u << k);
-        }
-        mask[(int64_t)(zo - own_z0) * ncols + col] = (uint8_t)bits;
-      }
-    }
-#pragma unroll
-    for (int j = 0; j < K - 1; ++j) win[j] = nxt[j + 1];
-  }
-}
-
 bool vec_ok(const snk_grid* g, const snk_params* p) {
   return g->n[0] % 8 == 0 && p->seed_window >= 0 && p->seed_window <= 8;
 }
@@ -550,7 +487,8 @@ int32_t seeds_impl(const snk_grid* g, const snk_params* p, const uint16_t* d_smo
     int64_t k[3] = {1, 1, 1};
     double o[3] = {0, 0, 0};
     for (int a = 0; a < dim; ++a) {
-      const double span = (double)(g->n[a] - 1) - 2.0 * m;
+      // physical extent (n - 1) scale (G28; scale 1 unless anisotropic)
+      const double span = (double)(g->n[a] - 1) * grid_scale(g, a) - 2.0 * m;
       if (span < 0.0) {
         *n_out = 0;
         return fail(SNK_EMPTY_DOMAIN, "the lattice footprint does not fit the volume");
@@ -565,7 +503,7 @@ int32_t seeds_impl(const snk_grid* g, const snk_params* p, const uint16_t* d_smo
       iz0 = k[2];
       iz1 = 0;
       for (int64_t iz = 0; iz < k[2]; ++iz) {
-        const double zpos = (double)(float)(o[2] + (double)iz * s);
+        const double zpos = (double)(float)(o[2] + (double)iz * s) / grid_scale(g, 2);   // raw plane units
         if (zpos >= (double)g->own_z0 && zpos < (double)g->own_z1) {
           iz0 = std::min(iz0, iz);
           iz1 = std::max(iz1, iz + 1);
@@ -588,15 +526,21 @@ int32_t seeds_impl(const snk_grid* g, const snk_params* p, const uint16_t* d_smo
   // MAXIMA
   const int nx = (int)g->n[0], ny = (int)g->n[1], nzb = (int)g->nz_buf;
   const int w = p->seed_window;
+  // per-axis half-windows (anisotropic grids, G28)
+  const int wx = axis_window(g, w, 0), wy = axis_window(g, w, 1), wz = dim == 3 ? axis_window(g, w, 2) : 0;
   if (dim == 3) {
-    const int64_t need_lo = std::max<int64_t>(g->own_z0 - w, 0);
-    const int64_t need_hi = std::min<int64_t>(g->own_z1 - 1 + w, g->n[2] - 1);
+    const int64_t need_lo = std::max<int64_t>(g->own_z0 - wz, 0);
+    const int64_t need_hi = std::min<int64_t>(g->own_z1 - 1 + wz, g->n[2] - 1);
     if (g->own_z1 > g->own_z0 && (need_lo < g->z_lo || need_hi >= g->z_lo + g->nz_buf))
       return fail(SNK_SHAPE, "slab halo thinner than the seed window");
   }
   const int64_t plane = (int64_t)nx * ny;
   const int64_t nvox = plane * nzb;
-  if (vec_ok(g, p) && ws_bytes >= vec_ws(g) && vec8_ok(g, d_smooth, nullptr, nullptr)) {
+  const bool vec = vec_ok(g, p) && ws_bytes >= vec_ws(g) && vec8_ok(g, d_smooth, nullptr, nullptr) &&
+                   wx <= 8 && wy <= 8 && wz <= 8;
+  if (grid_aniso(g) && !vec)
+    return fail(SNK_SHAPE, "anisotropic MAXIMA needs the vectorised path (x % 8 == 0, 16-byte aligned, windows <= 8)");
+  if (vec) {
     if (g->own_z1 <= g->own_z0) {
       *n_out = 0;
       return SNK_OK;
@@ -613,12 +557,17 @@ int32_t seeds_impl(const snk_grid* g, const snk_params* p, const uint16_t* d_smo
     void* stmp = cv.take<char>(scan_ws(nbw));
     if (cv.overflow) return fail(SNK_CAPACITY, "workspace too small for seeds");
     // x / y box max only over the planes the z window touches
-    const int64_t zb0 = dim == 3 ? std::max<int64_t>(g->own_z0 - w, 0) - g->z_lo : g->own_z0 - g->z_lo;
-    const int64_t zb1 = dim == 3 ? std::min<int64_t>(g->own_z1 - 1 + w, g->n[2] - 1) - g->z_lo + 1
+    const int64_t zb0 = dim == 3 ? std::max<int64_t>(g->own_z0 - wz, 0) - g->z_lo : g->own_z0 - g->z_lo;
+    const int64_t zb1 = dim == 3 ? std::min<int64_t>(g->own_z1 - 1 + wz, g->n[2] - 1) - g->z_lo + 1
                                  : g->own_z1 - g->z_lo;
     const int nzp = (int)(zb1 - zb0);
-    SNK_TRY(sep_pass(0, 1, w, d_smooth + zb0 * plane, ta + zb0 * plane, nx, ny, nzp, 0, nx - 1, st));
-    SNK_TRY(sep_pass(1, 1, w, ta + zb0 * plane, tb + zb0 * plane, nx, ny, nzp, 0, ny - 1, st));
+    SNK_TRY(sep_pass(0, 1, wx, d_smooth + zb0 * plane, ta + zb0 * plane, nx, ny, nzp, 0, nx - 1, st));
+    SNK_TRY(sep_pass(1, 1, wy, ta + zb0 * plane, tb + zb0 * plane, nx, ny, nzp, 0, ny - 1, st));
+    // 3D: the z box-max as its own column-streamed pass into ta (every plane of
+    // the window read ~once from HBM), then the predicate reads B and M once;
+    // the flat fold of 2w+1 XY planes re-read them through L2 (43 GB per C4 step)
+    const bool zpass = dim == 3 && wz > 0 && nzp > 32;
+    if (zpass) SNK_TRY(sep_pass(2, 1, wz, tb + zb0 * plane, ta + zb0 * plane, nx, ny, nzp, 0, nzp - 1, st));
     SNK_CUDA_CHECK(cudaMemsetAsync(bits + nw - 1, 0, sizeof(uint32_t), st));
     MaxArgs A;
     A.B = d_smooth;
@@ -628,6 +577,9 @@ int32_t seeds_impl(const snk_grid* g, const snk_params* p, const uint16_t* d_smo
     A.nz_glob = (int)g->n[2];
     A.z_lo = (int)g->z_lo;
     A.w = w;
+    A.wx = wx;
+    A.wy = wy;
+    A.wz = wz;
     A.dim = dim;
     A.thr = p->seed_threshold;
     A.v0 = A.v1 = 0;
@@ -638,32 +590,22 @@ int32_t seeds_impl(const snk_grid* g, const snk_params* p, const uint16_t* d_smo
     if (dim == 2) {
       maxima_pred8_kernel<2, 0><<<grid, 256, 0, st>>>(A, tb, mask, ng, oz);
     } else {
-      const int nzo = (int)(g->own_z1 - g->own_z0);
-      if (w > 0 && nzo > kPZ) {
-        const unsigned zg = (unsigned)ceil_div((int64_t)(nx / 8) * ny * ceil_div(nzo, kPZ), 256);
-        const int oz1 = (int)g->own_z1;
-        switch (w) {
-#define SNK_PREDZ_CASE(WW) \
-          case WW: maxima_predz_kernel<WW><<<zg, 256, 0, st>>>(A, tb, mask, oz, oz1); break;
-          SNK_PREDZ_CASE(1) SNK_PREDZ_CASE(2) SNK_PREDZ_CASE(3) SNK_PREDZ_CASE(4)
-          SNK_PREDZ_CASE(5) SNK_PREDZ_CASE(6) SNK_PREDZ_CASE(7) SNK_PREDZ_CASE(8)
-#undef SNK_PREDZ_CASE
-        }
-      } else {
-        switch (w) {
+      if (zpass) {
+        maxima_pred8_kernel<3, 0><<<grid, 256, 0, st>>>(A, ta, mask, ng, oz);   // M = ta
+      } else switch (wz) {
 #define SNK_PRED_CASE(WW) \
-          case WW: maxima_pred8_kernel<3, WW><<<grid, 256, 0, st>>>(A, tb, mask, ng, oz); break;
-          SNK_PRED_CASE(0) SNK_PRED_CASE(1) SNK_PRED_CASE(2) SNK_PRED_CASE(3) SNK_PRED_CASE(4)
-          SNK_PRED_CASE(5) SNK_PRED_CASE(6) SNK_PRED_CASE(7) SNK_PRED_CASE(8)
+        case WW: maxima_pred8_kernel<3, WW><<<grid, 256, 0, st>>>(A, tb, mask, ng, oz); break;
+        SNK_PRED_CASE(0) SNK_PRED_CASE(1) SNK_PRED_CASE(2) SNK_PRED_CASE(3) SNK_PRED_CASE(4)
+        SNK_PRED_CASE(5) SNK_PRED_CASE(6) SNK_PRED_CASE(7) SNK_PRED_CASE(8)
 #undef SNK_PRED_CASE
-        }
       }
     }
     SNK_LAUNCH_CHECK("maxima_pred8_kernel");
     bits_count_kernel<<<(unsigned)nbw, 1024, 0, st>>>(bits, nw, wcounts);
     SNK_LAUNCH_CHECK("bits_count_kernel");
     SNK_TRY(scan_counts(wcounts, nbw, woff, st, stmp));
-    bits_write_kernel<<<(unsigned)nbw, 1024, 0, st>>>(bits, nw, 0, nx, ny, oz, woff, d_seeds, cap, 1);
+    bits_write_kernel<<<(unsigned)nbw, 1024, 0, st>>>(bits, nw, 0, nx, ny, oz, woff, d_seeds, cap, 1,
+                                                      grid_scale(g, 0), grid_scale(g, 1), grid_scale(g, 2));
     SNK_LAUNCH_CHECK("bits_write_kernel");
     int64_t total = 0;
     SNK_CUDA_CHECK(cudaMemcpyAsync(&total, woff + nbw, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
@@ -703,7 +645,7 @@ int32_t seeds_impl(const snk_grid* g, const snk_params* p, const uint16_t* d_smo
     F.ma.ny = ny;
     F.ma.nz_glob = (int)g->n[2];
     F.ma.z_lo = (int)g->z_lo;
-    F.ma.w = w;
+    F.ma.w = F.ma.wx = F.ma.wy = F.ma.wz = w;
     F.ma.dim = dim;
     F.ma.thr = p->seed_threshold;
     const int RX = kMX + 2 * w, RY = kMY + 2 * w;
@@ -766,7 +708,7 @@ int32_t seeds_impl(const snk_grid* g, const snk_params* p, const uint16_t* d_smo
   A.ny = ny;
   A.nz_glob = (int)g->n[2];
   A.z_lo = (int)g->z_lo;
-  A.w = w;
+  A.w = A.wx = A.wy = A.wz = w;
   A.dim = dim;
   A.thr = p->seed_threshold;
   A.v0 = v0;

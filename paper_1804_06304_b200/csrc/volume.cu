@@ -251,28 +251,39 @@ __global__ void __launch_bounds__(256) sep8_kernel(const uint16_t* __restrict__ 
 // blur windows are unpacked once per plane, max windows stay packed (u16x2
 // VIMNMX).
 constexpr int kZC = 32;
+#ifndef ZCOL_AXES
+#define ZCOL_AXES 6   // bit 1: y passes, bit 2: z passes
+#endif
 
 __device__ __forceinline__ uint4 vmax4(uint4 a, uint4 b) {
   return make_uint4(__vmaxu2(a.x, b.x), __vmaxu2(a.y, b.y), __vmaxu2(a.z, b.z), __vmaxu2(a.w, b.w));
 }
 
-template <int OP, int H>
+// AXIS 2: columns (xc, y) walk z; AXIS 1: columns (xc, z) walk y (the flat y
+// pass re-reads 2h+1 rows per output through L1/L2 as well).
+template <int AXIS, int OP, int H>
 __global__ void __launch_bounds__(256) zcol8_kernel(const uint16_t* __restrict__ in, uint16_t* __restrict__ out,
-                                                    int nx, int ny, int nz, int lo, int hi,
+                                                    int nx, int ny, int nzv, int lo, int hi,
                                                     const __grid_constant__ Taps T) {
   constexpr int K = 2 * H + 1;
-  const int64_t ncols = (int64_t)(nx >> 3) * ny;
+  const int nc = nx >> 3;
+  // "planes" are the walked axis; columns enumerate the other two
+  const int nz = AXIS == 2 ? nzv : ny;
+  const int64_t ncols = AXIS == 2 ? (int64_t)nc * ny : (int64_t)nc * nzv;
+  const int64_t ps = AXIS == 2 ? (int64_t)nc * ny : (int64_t)nc;   // stride of the walked axis (uint4)
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int nzc = (nz + kZC - 1) / kZC;
   if (t >= ncols * nzc) return;
   const int64_t col = t % ncols;
   const int z0 = (int)(t / ncols) * kZC, z1 = min(z0 + kZC, nz);
-  const uint4* rin = reinterpret_cast<const uint4*>(in) + col;
-  uint4* rout = reinterpret_cast<uint4*>(out) + col;
+  // column base: AXIS 2: col = y nc + xc; AXIS 1: col = z nc + xc -> (z ny) nc + xc
+  const int64_t cb = AXIS == 2 ? col : (col / nc) * (int64_t)ny * nc + col % nc;
+  const uint4* rin = reinterpret_cast<const uint4*>(in) + cb;
+  uint4* rout = reinterpret_cast<uint4*>(out) + cb;
   auto load = [&](int q) -> uint4 {
-    if (OP == OP_BLUR) return __ldg(rin + (int64_t)min(max(q, 0), nz - 1) * ncols);
+    if (OP == OP_BLUR) return __ldg(rin + (int64_t)min(max(q, 0), nz - 1) * ps);
     if (q < lo || q > hi) return make_uint4(0u, 0u, 0u, 0u);   // outside the clipped window
-    return __ldg(rin + (int64_t)q * ncols);
+    return __ldg(rin + (int64_t)q * ps);
   };
   // win[j] = plane zb - H + j (j < K - 1); the K planes zb + H .. zb + H + K - 1
   // of a block are loaded together (K loads in flight per thread)
@@ -301,7 +312,7 @@ __global__ void __launch_bounds__(256) zcol8_kernel(const uint16_t* __restrict__
           }
 #pragma unroll
           for (int k = 0; k < 8; ++k) o[k] >>= 14;
-          rout[(int64_t)z * ncols] = pack8(o);
+          rout[(int64_t)z * ps] = pack8(o);
         } else {
           uint4 m = win[s < K - 1 ? s : 0];
           if (s >= K - 1) m = nxt[s - (K - 1)];
@@ -310,7 +321,7 @@ __global__ void __launch_bounds__(256) zcol8_kernel(const uint16_t* __restrict__
             const int j = s + i;
             m = vmax4(m, j < K - 1 ? win[j] : nxt[j - (K - 1)]);
           }
-          rout[(int64_t)z * ncols] = m;
+          rout[(int64_t)z * ps] = m;
         }
       }
     }
@@ -322,12 +333,13 @@ __global__ void __launch_bounds__(256) zcol8_kernel(const uint16_t* __restrict__
 template <int AXIS, int OP>
 int32_t sep8_launch(int h, const uint16_t* in, uint16_t* out, int nx, int ny, int nz, int lo, int hi,
                     const Taps& tp, cudaStream_t st) {
-  if (AXIS == 2 && h > 0 && nz > kZC) {
-    // z: column streaming (flat z passes re-read 2h+1 planes through L2)
-    const unsigned zg = (unsigned)ceil_div((int64_t)(nx / 8) * ny * ceil_div(nz, kZC), 256);
+  if (AXIS >= 1 && h > 0 && (AXIS == 2 ? nz : ny) > kZC && ZCOL_AXES & (1 << AXIS)) {
+    // y / z: column streaming (the flat passes re-read 2h+1 rows / planes through L1/L2)
+    const int64_t cols = AXIS == 2 ? (int64_t)(nx / 8) * ny : (int64_t)(nx / 8) * nz;
+    const unsigned zg = (unsigned)ceil_div(cols * ceil_div(AXIS == 2 ? nz : ny, kZC), 256);
     switch (h) {
 #define SNK_ZC_CASE(HH) \
-      case HH: zcol8_kernel<OP, HH><<<zg, 256, 0, st>>>(in, out, nx, ny, nz, lo, hi, tp); break;
+      case HH: zcol8_kernel<AXIS, OP, HH><<<zg, 256, 0, st>>>(in, out, nx, ny, nz, lo, hi, tp); break;
       SNK_ZC_CASE(1) SNK_ZC_CASE(2) SNK_ZC_CASE(3) SNK_ZC_CASE(4)
       SNK_ZC_CASE(5) SNK_ZC_CASE(6) SNK_ZC_CASE(7) SNK_ZC_CASE(8)
 #undef SNK_ZC_CASE
@@ -576,8 +588,10 @@ int32_t launch_fused_blur(const snk_grid* g, const uint16_t* d_in, uint16_t* d_o
 }  // namespace
 
 size_t preprocess_ws(const snk_grid* g, const snk_params* p) {
+  const size_t vol = (size_t)g->n[0] * g->n[1] * g->nz_buf * sizeof(uint16_t) + 256;
+  if (grid_aniso(g)) return 2 * vol;   // per-axis passes: two ping-pong buffers
   if (!(p->sigma > 0)) return 0;
-  return (size_t)g->n[0] * g->n[1] * g->nz_buf * sizeof(uint16_t) + 256;   // separable ping-pong
+  return vol;   // separable ping-pong
 }
 
 bool vec8_ok(const snk_grid* g, const void* a, const void* b, const void* c) {
@@ -613,9 +627,34 @@ int32_t preprocess_impl(const snk_grid* g, const snk_params* p, const uint16_t* 
   const int nx = (int)g->n[0], ny = (int)g->n[1], nz = (int)g->nz_buf;
   const int64_t nvox = (int64_t)nx * ny * nz;
   Carve cv(d_ws, ws_bytes);
-  uint16_t* tmp = h > 0 ? cv.take<uint16_t>(nvox) : nullptr;
+  uint16_t* tmp = (h > 0 || grid_aniso(g)) ? cv.take<uint16_t>(nvox) : nullptr;
   if (cv.overflow) return fail(SNK_CAPACITY, "workspace too small for preprocess");
-  if (h == 0) {
+  if (grid_aniso(g)) {
+    // anisotropic grid sampled without resampling (G28): the physical sigma is
+    // sigma / scale_a voxels on axis a — per-axis taps, the vectorised passes
+    // (x extent % 8 == 0 is validated) or the generic pass for wide kernels
+    uint16_t* t2 = cv.take<uint16_t>(nvox);
+    if (cv.overflow || !vec8_ok(g, d_in, d_smooth, tmp)) return fail(SNK_CAPACITY, "workspace too small for preprocess");
+    const uint16_t* src = d_in;
+    uint16_t* bufs[2] = {tmp, t2};
+    for (int a = 0; a < g->dim; ++a) {
+      std::vector<int32_t> ta;
+      const int ha = q14_taps(p->sigma / grid_scale(g, a), ta);
+      Taps tpa{};
+      for (size_t i = 0; i < ta.size() && i < (size_t)kMaxTaps; ++i) tpa.w[i] = ta[i];
+      uint16_t* dst = a == g->dim - 1 ? d_smooth : bufs[a & 1];
+      if (ha <= 8) {
+        SNK_TRY(sep_blur(a, ha, tpa, src, dst, nx, ny, nz, st));
+      } else {
+        const unsigned grid = grid_for((int64_t)((nx + 1) / 2) * ny * nz, 256);
+        if (a == 0) blur_pass_kernel<0><<<grid, 256, 0, st>>>(src, dst, nx, ny, nz, ha, tpa);
+        else if (a == 1) blur_pass_kernel<1><<<grid, 256, 0, st>>>(src, dst, nx, ny, nz, ha, tpa);
+        else blur_pass_kernel<2><<<grid, 256, 0, st>>>(src, dst, nx, ny, nz, ha, tpa);
+        SNK_LAUNCH_CHECK("blur_pass_kernel");
+      }
+      src = dst;
+    }
+  } else if (h == 0) {
     SNK_CUDA_CHECK(cudaMemcpyAsync(d_smooth, d_in, nvox * sizeof(uint16_t), cudaMemcpyDeviceToDevice, st));
   } else if (h <= 8 && vec8_ok(g, d_in, d_smooth, tmp)) {
     // three (2D: two) streaming separable passes, 8 voxels per thread

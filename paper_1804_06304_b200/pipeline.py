@@ -41,15 +41,23 @@ class Pipeline:
 
     def __init__(self, dim: int, n_raw, params: snk.snk_params, spacing=(1.0, 1.0, 1.0),
                  max_cells: int | None = None, labels: bool = True, gradmag: bool | None = None,
-                 device: str | torch.device = "cuda"):
+                 device: str | torch.device = "cuda", physical: bool = False):
+        """physical=True: an anisotropic volume is NOT resampled (a1); every stage
+        works on the raw grid in physical coordinates (G28, snk_grid.scale)."""
         self.dim = dim
         self.n_raw = tuple(int(a) for a in n_raw)
         self.spacing = tuple(float(s) for s in spacing)
         self.params = params
         self.device = torch.device(device)
-        self.n_iso = snk.snk_resample_dims(dim, self.n_raw, self.spacing)
+        smin = min(self.spacing[:dim])
+        self.scale = tuple(s / smin if a < dim else 1.0 for a, s in enumerate(self.spacing))
+        if physical:
+            self.n_iso = self.n_raw
+        else:
+            self.n_iso = snk.snk_resample_dims(dim, self.n_raw, self.spacing)
+            self.scale = (1.0, 1.0, 1.0)
         self.resample = tuple(self.n_iso) != self.n_raw
-        self.grid = snk.make_grid(dim, self.n_iso)
+        self.grid = snk.make_grid(dim, self.n_iso, scale=self.scale)
         nvox = self.n_iso[0] * self.n_iso[1] * self.n_iso[2]
         if max_cells is None:
             # generous bound on seeds: one per (2w+1)^d box for MAXIMA, the lattice count otherwise
@@ -70,6 +78,8 @@ class Pipeline:
         ws = snk.snk_workspace_bytes(self.grid, params, self.max_cells)
         if self.resample:
             ws = max(ws, 2 * nvox * 2 + 4096)
+        if physical:
+            ws = max(ws, 2 * nvox * 2 + 4096)   # per-axis blur ping-pong
         self.ws = torch.empty(ws, dtype=torch.uint8, device=dev)
         self.n_seeds = 0
         self.n_live = 0       # records in self.cells after evolve (< n_seeds with periodic culling)

@@ -43,7 +43,7 @@ _lib = C.CDLL(LIB_PATH)
 class snk_grid(C.Structure):
     _fields_ = [("dim", C.c_int32), ("_pad0", C.c_int32), ("n", C.c_int64 * 3),
                 ("z_lo", C.c_int64), ("nz_buf", C.c_int64), ("own_z0", C.c_int64),
-                ("own_z1", C.c_int64)]
+                ("own_z1", C.c_int64), ("scale", C.c_double * 3)]
 
 
 class snk_params(C.Structure):
@@ -280,8 +280,11 @@ def snk_run(dim, n_raw, spacing, p, h_raw, h_dets, det_cap, h_labels, max_cells,
 
 
 # ---------------------------------------------------------------- struct helpers
-def make_grid(dim: int, n, z_lo: int = 0, nz_buf: int | None = None, own=None) -> snk_grid:
+def make_grid(dim: int, n, z_lo: int = 0, nz_buf: int | None = None, own=None,
+              scale=(1.0, 1.0, 1.0)) -> snk_grid:
+    """scale: physical voxel size per axis (anisotropic sampling without resampling, G28)."""
     g = snk_grid()
+    g.scale[:] = [float(a) for a in scale]
     g.dim = dim
     g.n[:] = [int(a) for a in n]
     g.z_lo = z_lo

@@ -674,3 +674,80 @@ def test_edge_cases(gpu):
     snk.snk_evolve(g, pp, sm, seeds, None, 0, 0, torch.empty(48, dtype=torch.uint8, device="cuda"), None)
     assert snk.snk_cull(g, pp, torch.empty(48, dtype=torch.uint8, device="cuda"), 0,
                         torch.empty(48, dtype=torch.uint8, device="cuda"), 1, ws) == 0
+
+
+# ---------------------------------------------------------------- anisotropic grids without resampling (§8(f) 4, G28)
+
+
+def test_anisotropic_physical_pipeline_c3_crop(gpu):
+    """C3's raw (1, 1, 2)-spaced volume used without resampling: per-axis blur
+    (sigma_z = 0.5 voxel) and MAXIMA windows (w_z = round(w / 2)) bit-exact,
+    physical seeds, evolution in physical coordinates within tolerance (MC, CV,
+    ray), and the cull + label map (physical voxel positions) bit-exact given
+    the GPU cells; a z-slab buffer gives bit-identical cells."""
+    torch, snk, pipeline = gpu
+    cfg = synth.CONFIGS["C3"]
+    raw = np.ascontiguousarray(synth.generate(cfg)[40:88, 100:228, 64:192])   # 48 x 128 x 128 raw
+    n = (128, 128, 48)
+    sc = (1.0, 1.0, 2.0)
+    c3 = cfg.with_(n=n, max_iters=120)
+    p = pipeline.params_for(c3)
+    P = pipeline.Pipeline(3, n, p, spacing=cfg.spacing, physical=True)
+    assert P.scale == sc and P.n_iso == n
+    P.upload(raw)
+    P.preprocess()
+    P.seed()
+    torch.cuda.synchronize()
+    B = oracle.blur(raw, 3, (1.0, 1.0, 0.5))
+    assert np.array_equal(P.smooth.cpu().numpy(), B)
+    w = c3.window
+    w3 = (w, w, int(np.floor(w / 2 + 0.5)))
+    exp = oracle.seeds_maxima(B, 3, w3, c3.seed_threshold, scale=sc)
+    assert len(exp) > 20 and np.array_equal(P.seeds_np(), exp)
+    for est, mode in (("EST_MC", 0), ("EST_MC_CV", 2), ("EST_RAY", 3)):
+        P.params = pipeline.params_for(c3, estimator=getattr(snk, est))
+        P.evolve(n=24)
+        torch.cuda.synchronize()
+        g = P.cells_np()
+        o = oracle.evolve(B, _ora_params(c3, mode=mode, scale=sc), exp[:24], ids=np.arange(24))
+        _assert_cells_close(g, o, "aniso " + est)
+    P.params = p
+    P.evolve()
+    torch.cuda.synchronize()
+    cells = P.cells_np()
+    nd = P.cull()
+    torch.cuda.synchronize()
+    keep = oracle.cull(cells["c"], cells["R"], cells["energy"], cells["flags"], cells["id"], 3, -3.0)
+    assert nd == len(keep) > 5 and P.dets_np().tobytes() == cells[keep].tobytes()
+    P.label()
+    torch.cuda.synchronize()
+    dets = P.dets_np()
+    lab = oracle.label(n, 3, dets["c"], dets["R"], scale=sc)
+    assert np.array_equal(P.labels.cpu().numpy(), lab)
+    # z-slab buffer, physical z planes [0, 20) owned
+    sel = np.nonzero(P.seeds_np()[:, 2] < 20.0)[0][:16]
+    g = snk.make_grid(3, n, z_lo=0, nz_buf=40, own=(0, 20), scale=sc)
+    out = torch.empty(len(sel) * 48, dtype=torch.uint8, device="cuda")
+    snk.snk_evolve(g, p, P.smooth[:40].contiguous(), P.seeds[sel].contiguous(),
+                   _t(torch, sel.astype(np.int64)), 0, len(sel), out, None)
+    torch.cuda.synchronize()
+    got = pipeline.as_cells(out, len(sel))
+    ok = (got["flags"] & snk.F_HALO) == 0
+    assert ok.sum() > 0 and got[ok].tobytes() == cells[sel][ok].tobytes()
+
+
+def test_anisotropic_lattice_and_config_errors(gpu):
+    torch, snk, pipeline = gpu
+    n = (64, 60, 32)
+    g = snk.make_grid(3, n, scale=(1.0, 1.0, 2.0))
+    p = snk.make_params(10.0, seed_mode=snk.SEED_LATTICE)
+    seeds = torch.empty((4096, 3), dtype=torch.float32, device="cuda")
+    cnt, _ = snk.snk_seeds(g, p, None, seeds, 4096, None)
+    st, exp = oracle.seeds_lattice(n, 3, 10.0, scale=(1.0, 1.0, 2.0))
+    assert cnt == len(exp) > 1 and np.array_equal(seeds[:cnt].cpu().numpy(), exp)
+    vol = torch.zeros((32, 60, 64), dtype=torch.uint16, device="cuda")
+    cells = torch.empty(48 * 4, dtype=torch.uint8, device="cuda")
+    with pytest.raises(snk.SNKError):   # grid estimator is isotropic only
+        snk.snk_evolve(g, snk.make_params(10.0, estimator=snk.EST_GRID), vol, seeds, None, 0, 2, cells, None)
+    with pytest.raises(snk.SNKError):   # N must be 1024 (4 warps x 8 samples)
+        snk.snk_evolve(g, snk.make_params(10.0, n_samples=256), vol, seeds, None, 0, 2, cells, None)
