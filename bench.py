@@ -179,7 +179,8 @@ def run_ours(args):
     p = pipeline.params_for(cfg, image_term=snk.IMAGE_INTENSITY, cta_warps=args.cta_warps,
                             kernel_variant=args.kernel_variant, cull_every=args.cull_every,
                             estimator={"mc": snk.EST_MC, "cv": snk.EST_MC_CV, "ray": snk.EST_RAY}[args.estimator])
-    P = pipeline.Pipeline(cfg.dim, cfg.n, p, spacing=cfg.spacing, gradmag=True)
+    P = pipeline.Pipeline(cfg.dim, cfg.n, p, spacing=cfg.spacing, gradmag=not args.physical,
+                          physical=args.physical)
     h_raw = torch.empty((cfg.n[2], cfg.n[1], cfg.n[0]), dtype=torch.uint16, pin_memory=True)
     t = time.perf_counter()
     synth.generate_into_ptr(cfg, h_raw.data_ptr())
@@ -248,7 +249,7 @@ def run_ours(args):
                 "peak_source": f"{SMS} SMs x {LANES_PER_SM} FP32 lanes x sm_max_mhz (B200_PROFILING.md)"}
     # end to end through the public host-buffer call (snk_run)
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and not args.physical:   # snk_run resamples anisotropic input (a1)
         # end to end through the public host-buffer call (snk_run): every step
         # copies its raw volume in and its detections + label map out.  Steps
         # are issued from `inflight` host threads, each with its own runner and
@@ -302,7 +303,7 @@ def run_ours(args):
         "config": {"workload": workload_name(cfg), "volume_iso": n_iso_l, "cells": n_cells,
                    "detections": n_dets, "n_samples": cfg.n_samples, "iters": cfg.max_iters,
                    "seed_mode": cfg.seed_mode, "parallelism": "1 GPU", "cull_every": args.cull_every,
-                   "estimator": args.estimator,
+                   "estimator": args.estimator, "physical": bool(args.physical),
                    "l2": "inputs larger than L2 (u16 volume %.1f GiB > 126 MB)" % (h_raw.numel() * 2 / 2**30)},
         "cells_per_s": cells_per_s, "phase_ms": phase, "gpu_launches": int(launches),
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
@@ -356,6 +357,8 @@ def main():
     ap.add_argument("--kernel-variant", type=int, default=0, help="evolve kernel: 0 auto, 1 warp, 2 brick")
     ap.add_argument("--estimator", default="mc", choices=["mc", "cv", "ray"],
                     help="MC (the paper's), MC + control variate (G21) or stratified ray march (G27)")
+    ap.add_argument("--physical", action="store_true",
+                    help="anisotropic configs: sample the raw grid in physical coordinates, no resampling (G28)")
     ap.add_argument("--cull-every", type=int, default=0,
                     help="periodic culling every k iterations (P:326, G25); 0 = the paper's end-of-run cull")
     ap.add_argument("--e2e-inflight", type=int, default=2, help="steps in flight in the end-to-end run")
