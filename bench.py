@@ -39,6 +39,10 @@ OPS_PER_SAMPLE = 111
 # ray march (G27): Philox 3 blocks per 8-step ray 15, uniforms 2.5, direction per
 # ray 1.25, step t 3, position 3, gather 34, t^2 weight 2, S 15, leaves 11 -> 87
 OPS_BY_ESTIMATOR = {"mc": OPS_PER_SAMPLE, "cv": OPS_PER_SAMPLE + 1, "ray": 87}
+# 2D (C2): Philox 1/2 block per sample 20, uniforms 4, direction + radius (sin, cos,
+# sqrt) 8, position 2, bilinear gather 2 axes x 6 + 1 index + 4 conversions + 3 lerps x 2
+# = 23 (+ 4 loads), S/S_r/S_R 15, leaves 4 + tree adds 4  ->  80
+OPS_PER_SAMPLE_2D = 80
 SMS = 148
 LANES_PER_SM = 128
 
@@ -236,7 +240,7 @@ def run_ours(args):
     f_clk = (clocks["sm_max_mhz"] or 1965.0) * 1e6
     peak = SMS * LANES_PER_SM * f_clk / 1e9            # G lane-ops/s
     ev_s = statistics.mean(evolve_ms) / 1e3
-    ops = OPS_BY_ESTIMATOR[args.estimator]
+    ops = OPS_BY_ESTIMATOR[args.estimator] if cfg.dim == 3 else OPS_PER_SAMPLE_2D
     achieved = samples * ops / ev_s / 1e9
     traffic, traffic_src = ncu_traffic(cfg.name) if not args.cull_every else (None, None)
     roofline = {"bound": "alu", "achieved": round(achieved, 1), "peak": round(peak, 1),
