@@ -849,19 +849,19 @@ __device__ __forceinline__ bool cell_update(const EvoParams& P, CellState& s, co
   }
   if (NB) {
     const bool fin = it == P.T + 1;   // E_final only: no update
-    const bool last = it == P.T;
-    float mv = fabsf(__fsub_rn(R, oR));
-    mv = fmaxf(mv, fabsf(__fsub_rn(dx, ox)));
-    mv = fmaxf(mv, fabsf(__fsub_rn(dy, oy)));
-    mv = fmaxf(mv, fabsf(__fsub_rn(dz, oz)));
-    uint32_t f = (mv < P.conv_tol) ? SNK_F_CONVERGED : 0u;
-    f |= ((lx != cx) || (ly != cy) || (lz != cz)) ? SNK_F_LEASHED : 0u;
-    f |= ((dx != lx) || (dy != ly) || (dz != lz)) ? SNK_F_DOMAIN : 0u;
-    s.flags |= last ? f : 0u;
     s.cx = fin ? ox : dx;
     s.cy = fin ? oy : dy;
     s.cz = fin ? oz : dz;
     s.R = fin ? oR : R;
+    if (it == P.T) {   // the flags of the last step (a uniform branch after the update)
+      float mv = fabsf(__fsub_rn(R, oR));
+      mv = fmaxf(mv, fabsf(__fsub_rn(dx, ox)));
+      mv = fmaxf(mv, fabsf(__fsub_rn(dy, oy)));
+      mv = fmaxf(mv, fabsf(__fsub_rn(dz, oz)));
+      if (mv < P.conv_tol) s.flags |= SNK_F_CONVERGED;
+      if ((lx != cx) || (ly != cy) || (lz != cz)) s.flags |= SNK_F_LEASHED;
+      if ((dx != lx) || (dy != ly) || (dz != lz)) s.flags |= SNK_F_DOMAIN;
+    }
     return fin;
   }
   s.cx = dx; s.cy = dy; s.cz = dz;
