@@ -1,7 +1,7 @@
 """DRAM traffic per launch of the evolve kernel from ncu --set full reports ->
 profiles/traffic.json (read by bench.py for roofline.traffic).
 
-    python scripts/ncu_traffic.py CONFIG REPORT.ncu-rep [CONFIG REPORT ...]
+    python scripts/ncu_traffic.py CONFIG REPORT.ncu-rep|RAW.csv [CONFIG REPORT ...]
 """
 import csv
 import io
@@ -15,7 +15,10 @@ out_path = os.path.join(ROOT, "profiles", "traffic.json")
 t = json.load(open(out_path)) if os.path.exists(out_path) else {}
 args = sys.argv[1:]
 for cfg, rep in zip(args[::2], args[1::2]):
-    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    if rep.endswith(".csv"):   # an exported `--page raw --csv`
+        raw = open(rep).read()
+    else:
+        raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
     h, u = rows[0], rows[1]
     for r in rows[2:]:

@@ -20,5 +20,8 @@ ls -la $O
 python scripts/ncu_summary.py $O/${TAG}_evolve_c3.ncu-rep $O/${TAG}_evolve_c4.ncu-rep --launches $O/${TAG}_launches_c4.csv --title "${TAG}: evolve kernel + C4 launch list" --out $O/${TAG}_evolve_summary.md
 python scripts/ncu_summary.py $O/${TAG}_volume_c4.ncu-rep --title "${TAG}: volume passes on C4" --out $O/${TAG}_volume_summary.md
 ncu -i $O/${TAG}_evolve_c4.ncu-rep --page source --csv > $O/${TAG}_evolve_c4_source.csv 2>/dev/null
-rm -f $O/${TAG}_volume_c4.ncu-rep
+# raw counters travel back as csv (gpurun copies back at most 64 MiB)
+ncu -i $O/${TAG}_evolve_c3.ncu-rep --page raw --csv > $O/${TAG}_evolve_c3_raw.csv 2>/dev/null
+ncu -i $O/${TAG}_evolve_c4.ncu-rep --page raw --csv > $O/${TAG}_evolve_c4_raw.csv 2>/dev/null
+rm -f $O/${TAG}_volume_c4.ncu-rep $O/${TAG}_evolve_c3.ncu-rep $O/${TAG}_evolve_c4.ncu-rep
 du -sh $O
