@@ -266,7 +266,12 @@ def run_ours(args):
         k = max(1, min(args.e2e_inflight, args.steps))
         runners = [pipeline.HostRunner(cfg.dim, cfg.n, p, spacing=cfg.spacing, max_cells=max_cells)
                    for _ in range(k)]
-        streams = [torch.cuda.Stream() for _ in range(k)]
+        # distinct priorities: the runners' kernels would otherwise share the GPU,
+        # finish together and leave it idle during their host copies; with
+        # priorities one step computes while the other copies
+        lo, hi = torch.cuda.Stream.priority_range() if hasattr(torch.cuda.Stream, "priority_range") else (0, -1)
+        streams = [torch.cuda.Stream(priority=(hi if i == 0 else lo) if args.e2e_priorities else 0)
+                   for i in range(k)]
         nds = [0] * k
 
         def work(i, nsteps, delay=0.0):
@@ -365,6 +370,7 @@ def main():
                     help="anisotropic configs: sample the raw grid in physical coordinates, no resampling (G28)")
     ap.add_argument("--cull-every", type=int, default=0,
                     help="periodic culling every k iterations (P:326, G25); 0 = the paper's end-of-run cull")
+    ap.add_argument("--e2e-priorities", type=int, default=1, help="distinct stream priorities per in-flight step")
     ap.add_argument("--e2e-inflight", type=int, default=2, help="steps in flight in the end-to-end run")
     args = ap.parse_args()
     if args.warmup < 3:
