@@ -529,24 +529,18 @@ __device__ __forceinline__ Acc2 sample_pair_fast(const EvoParams& P, const CellI
   }
   if (est_kind(EST) == SNK_EST_MC_CV) tri = __fadd2_rn(tri, bc2(-C.ic));
   if (est_kind(EST) == SNK_EST_RAY) tri = __fmul2_rn(tri, D == 3 ? __fmul2_rn(t, t) : t);
-  // leaves(): the saturating ramps stay scalar (FFMA.SAT), the rest is paired
-  const float2 uo = make_float2(__saturatef(__fmaf_rn(d0.t, P.inv_dR, C.a)),
-                                __saturatef(__fmaf_rn(d1.t, P.inv_dR, C.a)));
-  const float2 ui = make_float2(__saturatef(__fmaf_rn(d0.t, P.inv_rho_dR, C.a)),
-                                __saturatef(__fmaf_rn(d1.t, P.inv_rho_dR, C.a)));
-  const float2 qo = __ffma2_rn(neg2(uo), uo, uo), qi = __ffma2_rn(neg2(ui), ui, ui);
-  const float2 s3o = __fmul2_rn(uo, __ffma2_rn(bc2(2.0f), qo, uo));
-  const float2 s3i = __fmul2_rn(ui, __ffma2_rn(bc2(2.0f), qi, ui));
-  const float2 Sv = __fadd2_rn(__ffma2_rn(bc2(2.0f), s3i, neg2(s3o)), bc2(-1.0f));
-  const float2 Sr = __ffma2_rn(bc2(P.k2_rho), qi, neg2(qo));
-  const float2 SR = __ffma2_rn(bc2(-2.0f), qi, qo);
-  const float2 w = __fmul2_rn(Sr, tri);
+  // leaves() per component: paired FFMA2/FMUL2 leaves were measured to break
+  // the bit-identity with the scalar path in the kernel (each f32x2 operation
+  // alone matches its scalar twin, scripts/micro/x2check.cu, leafcheck.cu; the
+  // kernel's results did not — scripts/debug_bitid.py), so only the position,
+  // magic-floor split and d-linear lerps are paired
+  const Acc la = leaves(P, C, d0, tri.x, D == 3), lb = leaves(P, C, d1, tri.y, D == 3);
   Acc2 a;
-  a.a0 = __fmul2_rn(Sv, tri);
-  a.cx = __fmul2_rn(w, ox);
-  a.cy = __fmul2_rn(w, oy);
-  a.cz = D == 3 ? __fmul2_rn(w, oz) : bc2(0.0f);
-  a.aR = __fmul2_rn(SR, tri);
+  a.a0 = make_float2(la.a0, lb.a0);
+  a.cx = make_float2(la.cx, lb.cx);
+  a.cy = make_float2(la.cy, lb.cy);
+  a.cz = make_float2(la.cz, lb.cz);
+  a.aR = make_float2(la.aR, lb.aR);
   return a;
 }
 
@@ -1078,7 +1072,7 @@ struct BrickCtl {
 };
 
 template <int D, int W, int S, bool SLAB, int CH, int L, int EST = 0>
-__global__ void __launch_bounds__(32 * W, W == 4 ? SNK_BRICK_MINB4 : SNK_BRICK_MINB8) evolve_brick_kernel(const __grid_constant__ EvoParams P) {
+__global__ void __launch_bounds__(32 * W, W == 4 ? SNK_BRICK_MINB4 : (W <= 2 ? 5 : SNK_BRICK_MINB8)) evolve_brick_kernel(const __grid_constant__ EvoParams P) {
   constexpr int B = CH << L;
   constexpr bool PIPE = SNK_BRICK_PIPE && L == 0;
   static_assert(EST == 0 || (PIPE && CH == 8), "CV / RAY estimators: 8 samples per thread, pipelined draws");
@@ -1385,6 +1379,20 @@ int32_t brick_B(const EvoParams& P, int B, cudaStream_t st) {
   }
 }
 
+// Small N (< 1024) with small contours: 1 or 2 warps per cell keep 8 samples
+// per thread (the per-iteration update is paid per warp), and a 28 x 27 x 27
+// brick (40.8 KB) lets 5 CTAs share an SM.
+constexpr int kS3small = 27;
+template <int W, bool SLAB>
+int32_t brick_small_B(const EvoParams& P, int B, cudaStream_t st) {
+  switch (B) {
+    case 2: return launch_brick<3, W, kS3small, SLAB, 2, 0>(P, st);
+    case 4: return launch_brick<3, W, kS3small, SLAB, 4, 0>(P, st);
+    case 8: return launch_brick<3, W, kS3small, SLAB, 8, 0>(P, st);
+    default: return fail(SNK_INTERNAL, "brick_small_B: 2, 4 or 8 samples per thread");
+  }
+}
+
 __global__ void cells_init_kernel(const float* seeds, const int64_t* ids, int64_t id_base, int64_t n,
                                   float r0, snk_cell* out) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -1569,6 +1577,16 @@ int32_t evolve_impl(const snk_grid* g, const snk_params* p, const uint16_t* d_im
   const bool brick_ok = variant != 1 && Bb >= 1 && Bb <= 128 && (Wb == 4 || Wb == 8) &&
                         g->n[0] % 2 == 0 && (reinterpret_cast<uintptr_t>(d_image) & 3) == 0;
   if (variant == 2 && !brick_ok) return fail(SNK_CONFIG, "brick kernel unavailable for this volume");
+  // small N and small contours (C5's sweep): the small-brick kernel, auto warps only
+  const bool small_ok = variant != 1 && D == 3 && p->cta_warps == 0 && p->n_samples >= 64 &&
+                        p->n_samples < 1024 && p->r0 <= 9.5 && g->n[0] % 2 == 0 &&
+                        (reinterpret_cast<uintptr_t>(d_image) & 3) == 0;
+  if (small_ok) {
+    const int Ws = p->n_samples >= 512 ? 2 : 1;
+    const int Bs = p->n_samples / (32 * Ws);
+    if (Ws == 2) return slab ? brick_small_B<2, true>(P, Bs, st) : brick_small_B<2, false>(P, Bs, st);
+    return slab ? brick_small_B<1, true>(P, Bs, st) : brick_small_B<1, false>(P, Bs, st);
+  }
   if (brick_ok) {
     if (D == 3) {
       // S = 33: 34 x 33 x 33 u16 = 72.3 KB, three CTAs per SM; covers balls up to rho_s ~ 15.5

@@ -751,3 +751,40 @@ def test_anisotropic_lattice_and_config_errors(gpu):
         snk.snk_evolve(g, snk.make_params(10.0, estimator=snk.EST_GRID), vol, seeds, None, 0, 2, cells, None)
     with pytest.raises(snk.SNKError):   # N must be 1024 (4 warps x 8 samples)
         snk.snk_evolve(g, snk.make_params(10.0, n_samples=256), vol, seeds, None, 0, 2, cells, None)
+
+
+@pytest.mark.parametrize("N", [64, 128, 256, 512])
+def test_small_n_small_brick_kernel(gpu, N):
+    """C5's small-N regime (r0 <= 9.5, N < 1024, auto warps): the 27^3-brick
+    kernel with 1-2 warps per cell matches the oracle and is bit-identical to
+    the warp kernel (same canonical tree)."""
+    torch, snk, pipeline = gpu
+    cfg = synth.CONFIGS["C1"].with_(r0=9.0, n_samples=N, max_iters=120)
+    P, raw, p = _gpu_smooth_seeds(torch, snk, pipeline, cfg, seed_mode=snk.SEED_LATTICE)
+    P.evolve()
+    torch.cuda.synchronize()
+    g = P.cells_np()
+    P.params = pipeline.params_for(cfg, seed_mode=snk.SEED_LATTICE, kernel_variant=1, cta_warps=1)
+    P.evolve()
+    torch.cuda.synchronize()
+    assert P.cells_np().tobytes() == g.tobytes()
+    B = oracle.blur(raw, 3, 1.0)
+    o = oracle.evolve(B, _ora_params(cfg), P.seeds_np(), ids=np.arange(P.n_seeds))
+    _assert_cells_close(g, o, f"small N={N}")
+
+
+@pytest.mark.parametrize("N,W", [(1024, 4), (2048, 8), (1024, 1)])
+def test_brick_fast_path_bit_identical_to_warp_kernel(gpu, N, W):
+    """The default launch (brick kernel, f32x2 fast path, 8 samples per thread)
+    against the warp kernel (scalar, global gathers): the same canonical tree
+    and per-sample arithmetic, so the records are identical bytes."""
+    torch, snk, pipeline = gpu
+    cfg = synth.CONFIGS["C1"].with_(n_samples=N, max_iters=150)
+    P, raw, p = _gpu_smooth_seeds(torch, snk, pipeline, cfg)
+    P.evolve()
+    torch.cuda.synchronize()
+    a = P.cells_np()
+    P.params = pipeline.params_for(cfg, kernel_variant=1, cta_warps=W)
+    P.evolve()
+    torch.cuda.synchronize()
+    assert P.cells_np().tobytes() == a.tobytes()
