@@ -1578,7 +1578,7 @@ int32_t evolve_impl(const snk_grid* g, const snk_params* p, const uint16_t* d_im
                         g->n[0] % 2 == 0 && (reinterpret_cast<uintptr_t>(d_image) & 3) == 0;
   if (variant == 2 && !brick_ok) return fail(SNK_CONFIG, "brick kernel unavailable for this volume");
   // small N and small contours (C5's sweep): the small-brick kernel, auto warps only
-  const bool small_ok = variant != 1 && D == 3 && p->cta_warps == 0 && p->n_samples >= 64 &&
+  const bool small_ok = variant != 1 && D == 3 && p->cta_warps == 0 && p->n_samples >= 128 &&
                         p->n_samples < 1024 && p->r0 <= 9.5 && g->n[0] % 2 == 0 &&
                         (reinterpret_cast<uintptr_t>(d_image) & 3) == 0;
   if (small_ok) {

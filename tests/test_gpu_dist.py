@@ -26,7 +26,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, q):
+def _worker(rank, world, port, q, k=0):
     import torch
     import torch.distributed as tdist
     from paper_1804_06304_b200 import dist as D, pipeline, snk
@@ -34,15 +34,15 @@ def _worker(rank, world, port, q):
     torch.cuda.set_device(0)
     tdist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        p = pipeline.params_for(CFG, image_term=snk.IMAGE_INTENSITY)
+        p = pipeline.params_for(CFG, image_term=snk.IMAGE_INTENSITY, cull_every=k)
         plan = D.plan_slabs(CFG.n, world, rank, p)
         raw = synth.generate(CFG)
         own = torch.from_numpy(raw[plan.own[0]:plan.own[1]].copy()).cuda()
         be = D.CudaBackend(plan, p, max_cells=4096)
-        r = D.SlabRun(plan, be, torch.device("cuda", 0)).step(own)
+        r = D.SlabRun(plan, be, torch.device("cuda", 0), cull_every=k, max_iters=CFG.max_iters).step(own)
         torch.cuda.synchronize()
-        ns, nd = r["n_seeds"], r["n_dets"]
-        q.put((rank, {"seeds": r["seeds"][:ns].cpu().numpy(), "cells": r["cells"][:ns * 48].cpu().numpy(),
+        ns, nd, nl = r["n_seeds"], r["n_dets"], r["n_live"]
+        q.put((rank, {"seeds": r["seeds"][:ns].cpu().numpy(), "cells": r["cells"][:nl * 48].cpu().numpy(),
                       "dets": r["dets"][:nd * 48].cpu().numpy(), "labels": r["labels"].cpu().numpy(),
                       "id_base": r["id_base"], "n_total": r["n_total"]}))
     except Exception as e:  # surface the failure in the parent
@@ -84,3 +84,42 @@ def test_slabs_match_single_gpu(single, world):
     for r in range(world):
         assert np.array_equal(out[r]["dets"], single["dets"])
     assert np.array_equal(np.concatenate([out[r]["labels"] for r in range(world)]), single["labels"])
+
+
+@pytest.fixture(scope="module")
+def single_periodic(gpu):
+    torch, snk, pipeline = gpu
+    p = pipeline.params_for(CFG, image_term=snk.IMAGE_INTENSITY, cull_every=15)
+    P = pipeline.Pipeline(3, CFG.n, p, gradmag=False)
+    P.upload(synth.generate(CFG))
+    res = P.step()
+    torch.cuda.synchronize()
+    return {"cells": P.cells_np(), "dets": P.dets[:res.n_dets * 48].cpu().numpy(),
+            "labels": P.labels.cpu().numpy(), "n_seeds": res.n_seeds}
+
+
+def test_slabs_periodic_culling_match_single_gpu(single_periodic):
+    """Periodic culling (G25) with the N6 checkpoint exchange on 2 ranks: the
+    live cells (as a set), the detections and the label map equal one GPU's."""
+    import torch.multiprocessing as mp
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q, 15)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    out = dict(q.get(timeout=600) for _ in range(world))
+    for pr in procs:
+        pr.join(timeout=120)
+    for r in range(world):
+        assert not isinstance(out[r], str), out[r]
+    rec = np.dtype([("c", "<f4", 3), ("R", "<f4"), ("seed", "<f4", 3), ("energy", "<f4"),
+                    ("flags", "<u4"), ("iters", "<i4"), ("id", "<i8")])
+    got = np.concatenate([out[r]["cells"] for r in range(world)]).view(rec)
+    exp = single_periodic["cells"]
+    assert len(exp) < single_periodic["n_seeds"]
+    assert got[np.argsort(got["id"])].tobytes() == exp[np.argsort(exp["id"])].tobytes()
+    for r in range(world):
+        assert np.array_equal(out[r]["dets"], single_periodic["dets"])
+    assert np.array_equal(np.concatenate([out[r]["labels"] for r in range(world)]), single_periodic["labels"])

@@ -753,7 +753,7 @@ def test_anisotropic_lattice_and_config_errors(gpu):
         snk.snk_evolve(g, snk.make_params(10.0, n_samples=256), vol, seeds, None, 0, 2, cells, None)
 
 
-@pytest.mark.parametrize("N", [64, 128, 256, 512])
+@pytest.mark.parametrize("N", [64, 128, 256, 512])   # 64: the warp kernel (faster there)
 def test_small_n_small_brick_kernel(gpu, N):
     """C5's small-N regime (r0 <= 9.5, N < 1024, auto warps): the 27^3-brick
     kernel with 1-2 warps per cell matches the oracle and is bit-identical to
