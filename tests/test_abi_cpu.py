@@ -63,6 +63,31 @@ def test_validation_errors(snk):
     assert snk.snk_validate(snk.make_grid(2, (64, 64, 1)), p) == snk.OK
 
 
+def test_validation_of_round_one_features(snk):
+    """Estimators, periodic culling and anisotropic grids (G25-G28): host-side checks."""
+    g = snk.make_grid(3, (64, 64, 64))
+    for e in (snk.EST_MC, snk.EST_GRID, snk.EST_MC_CV, snk.EST_RAY):
+        assert snk.snk_validate(g, snk.make_params(10.0, estimator=e)) == snk.OK
+    assert snk.snk_validate(g, snk.make_params(10.0, estimator=4)) == snk.CONFIG
+    assert snk.snk_validate(g, snk.make_params(10.0, estimator=snk.EST_GRID, kernel_variant=1)) == snk.CONFIG
+    assert snk.snk_validate(g, snk.make_params(10.0, cull_every=-1)) == snk.CONFIG
+    assert snk.snk_validate(g, snk.make_params(10.0, cull_every=50)) == snk.OK
+    ga = snk.make_grid(3, (64, 64, 32), scale=(1.0, 1.0, 2.0))
+    assert snk.snk_validate(ga, snk.make_params(10.0)) == snk.OK
+    assert snk.snk_validate(ga, snk.make_params(10.0, estimator=snk.EST_GRID)) == snk.CONFIG
+    assert snk.snk_validate(ga, snk.make_params(10.0, image_term=snk.IMAGE_GRADMAG)) == snk.CONFIG
+    assert snk.snk_validate(snk.make_grid(3, (60, 64, 32), scale=(1.0, 1.0, 2.0)), snk.make_params(10.0)) == snk.SHAPE
+    assert snk.snk_validate(snk.make_grid(3, (64, 64, 32), scale=(1.0, -1.0, 2.0)), snk.make_params(10.0)) == snk.SHAPE
+    assert snk.snk_validate(snk.make_grid(3, (60, 64, 32), scale=(0.0, 0.0, 0.0)), snk.make_params(10.0)) == snk.OK
+    # the periodic-culling segments: the binding's list equals the driver's
+    from paper_1804_06304_b200 import dist
+    for T, k in ((400, 50), (400, 0), (400, 400), (40, 15), (7, 3), (1, 1)):
+        assert snk.checkpoints(T, k) == dist.checkpoints(T, k)
+        segs = snk.checkpoints(T, k)
+        assert segs[0][0] == 1 and segs[-1][1] == T + 1
+        assert all(b + 1 == a for (_, b), (a, _) in zip(segs, segs[1:]))
+
+
 def test_workspace_and_resample_dims(snk):
     import oracle
     for n, sp in [((512, 512, 128), (1, 1, 2)), ((4, 4, 4), (0.5, 0.5, 1.0)), ((30, 20, 10), (3, 1.5, 1)),
