@@ -254,50 +254,57 @@ def run_ours(args):
     # end to end through the public host-buffer call (snk_run)
     e2e = None
     if not args.no_e2e and not args.physical:   # snk_run resamples anisotropic input (a1)
-        # end to end through the public host-buffer call (snk_run): every step
-        # copies its raw volume in and its detections + label map out.  Steps
-        # are issued from `inflight` host threads, each with its own runner and
-        # stream, so one step's copies overlap another step's kernels.
-        import concurrent.futures as cf
         niso = int(np.prod(n_iso_l))
         max_cells = P.max_cells
         del P
         torch.cuda.empty_cache()
-        k = max(1, min(args.e2e_inflight, args.steps))
-        runners = [pipeline.HostRunner(cfg.dim, cfg.n, p, spacing=cfg.spacing, max_cells=max_cells)
-                   for _ in range(k)]
-        # distinct priorities: the runners' kernels would otherwise share the GPU,
-        # finish together and leave it idle during their host copies; with
-        # priorities one step computes while the other copies
-        lo, hi = torch.cuda.Stream.priority_range() if hasattr(torch.cuda.Stream, "priority_range") else (0, -1)
-        streams = [torch.cuda.Stream(priority=(hi if i == 0 else lo) if args.e2e_priorities else 0)
-                   for i in range(k)]
-        nds = [0] * k
+        if args.e2e_mode == "batch":
+            # the end-to-end call for a stream of volumes (snk_run_batch): each of
+            # the K steps uploads its raw volume from pinned host memory and
+            # downloads its detections + label map; the next upload and the
+            # previous download overlap the current step's kernels
+            br = pipeline.BatchRunner(cfg.dim, cfg.n, p, spacing=cfg.spacing, max_cells=max_cells)
+            br.run([h_raw] * max(2, args.warmup))
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            nds = br.run([h_raw] * args.steps)
+            e2e_s = time.perf_counter() - t0
+            nd, k = nds[-1], 2
+            del br
+        else:
+            # snk_run (one volume per call) from `inflight` host threads, each with
+            # its own runner and a stream of distinct priority
+            import concurrent.futures as cf
+            k = max(1, min(args.e2e_inflight, args.steps))
+            runners = [pipeline.HostRunner(cfg.dim, cfg.n, p, spacing=cfg.spacing, max_cells=max_cells)
+                       for _ in range(k)]
+            lo, hi = torch.cuda.Stream.priority_range()
+            streams = [torch.cuda.Stream(priority=(hi if i == 0 else lo) if args.e2e_priorities else 0)
+                       for i in range(k)]
+            nds = [0] * k
 
-        def work(i, nsteps, delay=0.0):
-            torch.cuda.set_device(local_rank)
-            time.sleep(delay)
-            for _ in range(nsteps):
-                nds[i] = runners[i].run(h_raw, streams[i])
+            def work(i, nsteps, delay=0.0):
+                torch.cuda.set_device(local_rank)
+                time.sleep(delay)
+                for _ in range(nsteps):
+                    nds[i] = runners[i].run(h_raw, streams[i])
 
-        for i in range(k):
-            for _ in range(max(1, args.warmup // k)):
-                work(i, 1)
-        torch.cuda.synchronize()
-        share = [args.steps // k + (1 if i < args.steps % k else 0) for i in range(k)]
-        # stagger the threads by a fraction of a step so that one step's copies
-        # meet another step's kernels instead of the threads running in lockstep
-        delays = [i * (total_ms / args.steps) / 1e3 / k for i in range(k)]
-        t0 = time.perf_counter()
-        with cf.ThreadPoolExecutor(k) as ex:
-            list(ex.map(work, range(k), share, delays))
-        e2e_s = time.perf_counter() - t0
-        nd = nds[0]
+            for i in range(k):
+                for _ in range(max(1, args.warmup // k)):
+                    work(i, 1)
+            torch.cuda.synchronize()
+            share = [args.steps // k + (1 if i < args.steps % k else 0) for i in range(k)]
+            delays = [i * (total_ms / args.steps) / 1e3 / k for i in range(k)]
+            t0 = time.perf_counter()
+            with cf.ThreadPoolExecutor(k) as ex:
+                list(ex.map(work, range(k), share, delays))
+            e2e_s = time.perf_counter() - t0
+            nd = nds[0]
+            del runners
         e2e = {"value": samples * args.steps / e2e_s, "unit": UNIT,
                "h2d_bytes_per_step": int(h_raw.numel() * 2),
                "d2h_bytes_per_step": int(nd * 48 + niso * 4),
-               "cells_per_s": n_cells * args.steps / e2e_s, "inflight": k}
-        del runners
+               "cells_per_s": n_cells * args.steps / e2e_s, "inflight": k, "mode": args.e2e_mode}
     cpu = None
     if not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
@@ -370,7 +377,9 @@ def main():
                     help="anisotropic configs: sample the raw grid in physical coordinates, no resampling (G28)")
     ap.add_argument("--cull-every", type=int, default=0,
                     help="periodic culling every k iterations (P:326, G25); 0 = the paper's end-of-run cull")
-    ap.add_argument("--e2e-priorities", type=int, default=1, help="distinct stream priorities per in-flight step")
+    ap.add_argument("--e2e-mode", default="batch", choices=["batch", "threads"],
+                    help="end to end through snk_run_batch (copies overlapped inside the call) or snk_run threads")
+    ap.add_argument("--e2e-priorities", type=int, default=1, help="threads mode: distinct stream priorities")
     ap.add_argument("--e2e-inflight", type=int, default=2, help="steps in flight in the end-to-end run")
     args = ap.parse_args()
     if args.warmup < 3:

@@ -278,6 +278,24 @@ int32_t snk_run(int32_t dim, const int64_t n_raw[3], const double spacing[3],
                 int64_t* n_dets, int32_t* h_labels, int64_t max_cells, void* d_ws,
                 size_t ws_bytes, void* stream);
 
+/* snk_run over nvol volumes of the same shape (the end-to-end call for a
+ * stream of volumes): volume i is read from h_raw[i], its detections written to
+ * h_dets[i] (capacity det_cap each, count n_dets[i]) and, if h_labels is
+ * non-null and h_labels[i] non-null, its label map to h_labels[i].  The upload
+ * of volume i+1 and the download of volume i-1's results run on two internal
+ * streams while volume i's kernels run on `stream` (double-buffered device
+ * volume, detections and labels in the caller's workspace of
+ * snk_run_batch_workspace_bytes() bytes), so host<->device copies overlap the
+ * kernels.  Pinned host buffers are needed for the overlap.  Results are those
+ * of nvol snk_run calls.  Synchronises. */
+int32_t snk_run_batch_workspace_bytes(int32_t dim, const int64_t n_raw[3], const double spacing[3],
+                                      const snk_params* p, int64_t max_cells, size_t* bytes);
+int32_t snk_run_batch(int32_t dim, const int64_t n_raw[3], const double spacing[3],
+                      const snk_params* p, int64_t nvol, const uint16_t* const* h_raw,
+                      snk_cell* const* h_dets, int64_t det_cap, int64_t* n_dets,
+                      int32_t* const* h_labels, int64_t max_cells, void* d_ws, size_t ws_bytes,
+                      void* stream);
+
 /* Diagnostics: number of kernel launches issued by this thread since load. */
 int64_t snk_launch_count(void);
 

@@ -25,6 +25,28 @@ int32_t cuda_fail(cudaError_t e, const char* where) {
 }
 void count_launch(int64_t k) { g_launches += k; }
 
+namespace {
+__global__ void read_back_kernel(const unsigned char* src, unsigned char* dst, int n) {
+  for (int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
+}
+}  // namespace
+
+int32_t read_back(const void* d_src, void* h_dst, size_t bytes, cudaStream_t st) {
+  constexpr size_t kCap = 256;
+  static thread_local unsigned char* host = nullptr;   // mapped pinned host memory (per thread)
+  static thread_local unsigned char* dev = nullptr;
+  if (bytes > kCap) return fail(SNK_INTERNAL, "read_back: more than 256 bytes");
+  if (!host) {
+    SNK_CUDA_CHECK(cudaHostAlloc(reinterpret_cast<void**>(&host), kCap, cudaHostAllocMapped));
+    SNK_CUDA_CHECK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&dev), host, 0));
+  }
+  read_back_kernel<<<1, 32, 0, st>>>(static_cast<const unsigned char*>(d_src), dev, (int)bytes);
+  SNK_LAUNCH_CHECK("read_back_kernel");
+  SNK_CUDA_CHECK(cudaStreamSynchronize(st));
+  std::memcpy(h_dst, host, bytes);
+  return SNK_OK;
+}
+
 static bool is_pow2(int64_t v) { return v > 0 && (v & (v - 1)) == 0; }
 
 static int32_t validate_grid(const snk_grid* g) {
@@ -327,35 +349,25 @@ int32_t snk_run_workspace_bytes(int32_t dim, const int64_t n_raw[3], const doubl
   return SNK_OK;
 }
 
-int32_t snk_run(int32_t dim, const int64_t n_raw[3], const double spacing[3],
-                const snk_params* p, const uint16_t* h_raw, snk_cell* h_dets, int64_t det_cap,
-                int64_t* n_dets, int32_t* h_labels, int64_t max_cells, void* d_ws,
-                size_t ws_bytes, void* stream) {
-  clear_error();
-  if (!h_raw || !n_dets || det_cap < 0 || (det_cap > 0 && !h_dets) || max_cells < 1)
-    return fail(SNK_CONFIG, "bad args");
-  RunLayout L;
-  SNK_TRY(run_layout(dim, n_raw, spacing, p, max_cells, &L));
-  SNK_TRY(check_ws(L.total, d_ws, ws_bytes));
-  cudaStream_t st = as_stream(stream);
-  char* base = static_cast<char*>(d_ws);
-  uint16_t* d_raw = reinterpret_cast<uint16_t*>(base + L.off_raw);
-  uint16_t* d_iso = L.resample ? reinterpret_cast<uint16_t*>(base + L.off_iso) : d_raw;
+// The device part of one end-to-end step: raw volume (device) -> detections
+// (d_dets) and, if d_labels, the label map.  raw_free (nullable) is recorded on
+// st once the raw buffer has been consumed (after a1/a2), so a batch can
+// upload the next volume into it.
+static int32_t run_compute(const RunLayout& L, int32_t dim, const int64_t n_raw[3], const double spacing[3],
+                           const snk_params* p, const uint16_t* d_raw, snk_cell* d_dets, int32_t* d_labels,
+                           int64_t max_cells, char* base, cudaStream_t st, cudaEvent_t raw_free,
+                           int64_t* nd_out) {
+  uint16_t* d_iso = L.resample ? reinterpret_cast<uint16_t*>(base + L.off_iso) : const_cast<uint16_t*>(d_raw);
   uint16_t* d_smooth = reinterpret_cast<uint16_t*>(base + L.off_smooth);
   uint16_t* d_grad = p->image_term == SNK_IMAGE_GRADMAG ? reinterpret_cast<uint16_t*>(base + L.off_grad) : nullptr;
   float* d_seeds = reinterpret_cast<float*>(base + L.off_seeds);
   snk_cell* d_cells = reinterpret_cast<snk_cell*>(base + L.off_cells);
-  snk_cell* d_dets = reinterpret_cast<snk_cell*>(base + L.off_dets);
-  int32_t* d_labels = reinterpret_cast<int32_t*>(base + L.off_labels);
   void* scratch = base + L.off_scratch;
   const size_t sb = L.scratch_bytes;
-  const size_t nraw = (size_t)n_raw[0] * n_raw[1] * n_raw[2];
-  const size_t niso = (size_t)L.g.n[0] * L.g.n[1] * L.g.n[2];
-
-  SNK_CUDA_CHECK(cudaMemcpyAsync(d_raw, h_raw, nraw * sizeof(uint16_t), cudaMemcpyHostToDevice, st));
   if (L.resample)
     SNK_TRY(resample_impl(dim, n_raw, spacing, 0, n_raw[2], d_raw, 0, L.g.n[2], d_iso, scratch, sb, st));
   SNK_TRY(preprocess_impl(&L.g, p, d_iso, d_smooth, d_grad, scratch, sb, st));
+  if (raw_free) SNK_CUDA_CHECK(cudaEventRecord(raw_free, st));
   int64_t ns = 0, first = 0;
   SNK_TRY(seeds_impl(&L.g, p, d_smooth, d_seeds, max_cells, &ns, &first, scratch, sb, st));
   const uint16_t* d_img = d_grad ? d_grad : d_smooth;
@@ -384,8 +396,33 @@ int32_t snk_run(int32_t dim, const int64_t n_raw[3], const double spacing[3],
       SNK_TRY(evolve_impl(&L.g, p, d_img, d_seeds, nullptr, first, ns, d_cells, scratch, sb, st));
     SNK_TRY(cull_impl(&L.g, p, d_cells, ns, d_dets, max_cells, &nd, scratch, sb, st));
   }
+  if (d_labels) SNK_TRY(label_impl(&L.g, p, d_dets, nd, d_labels, scratch, sb, st));
+  *nd_out = nd;
+  return SNK_OK;
+}
+
+int32_t snk_run(int32_t dim, const int64_t n_raw[3], const double spacing[3],
+                const snk_params* p, const uint16_t* h_raw, snk_cell* h_dets, int64_t det_cap,
+                int64_t* n_dets, int32_t* h_labels, int64_t max_cells, void* d_ws,
+                size_t ws_bytes, void* stream) {
+  clear_error();
+  if (!h_raw || !n_dets || det_cap < 0 || (det_cap > 0 && !h_dets) || max_cells < 1)
+    return fail(SNK_CONFIG, "bad args");
+  RunLayout L;
+  SNK_TRY(run_layout(dim, n_raw, spacing, p, max_cells, &L));
+  SNK_TRY(check_ws(L.total, d_ws, ws_bytes));
+  cudaStream_t st = as_stream(stream);
+  char* base = static_cast<char*>(d_ws);
+  uint16_t* d_raw = reinterpret_cast<uint16_t*>(base + L.off_raw);
+  snk_cell* d_dets = reinterpret_cast<snk_cell*>(base + L.off_dets);
+  int32_t* d_labels = reinterpret_cast<int32_t*>(base + L.off_labels);
+  const size_t nraw = (size_t)n_raw[0] * n_raw[1] * n_raw[2];
+  const size_t niso = (size_t)L.g.n[0] * L.g.n[1] * L.g.n[2];
+  SNK_CUDA_CHECK(cudaMemcpyAsync(d_raw, h_raw, nraw * sizeof(uint16_t), cudaMemcpyHostToDevice, st));
+  int64_t nd = 0;
+  SNK_TRY(run_compute(L, dim, n_raw, spacing, p, d_raw, d_dets, h_labels ? d_labels : nullptr, max_cells, base,
+                      st, nullptr, &nd));
   *n_dets = nd;
-  if (h_labels) SNK_TRY(label_impl(&L.g, p, d_dets, nd, d_labels, scratch, sb, st));
   const int64_t ncopy = std::min(nd, det_cap);
   if (ncopy > 0)
     SNK_CUDA_CHECK(cudaMemcpyAsync(h_dets, d_dets, ncopy * sizeof(snk_cell), cudaMemcpyDeviceToHost, st));
@@ -394,6 +431,107 @@ int32_t snk_run(int32_t dim, const int64_t n_raw[3], const double spacing[3],
   SNK_CUDA_CHECK(cudaStreamSynchronize(st));
   if (nd > det_cap) return fail(SNK_CAPACITY, "detection buffer too small");
   return SNK_OK;
+}
+
+// snk_run over a sequence of volumes: the next volume's upload and the previous
+// results' download run on two internal streams while the current volume's
+// kernels run on `stream` (double-buffered raw volume, detections and label map).
+static size_t batch_extra(const RunLayout& L, const int64_t n_raw[3], int64_t max_cells) {
+  const size_t nraw = (size_t)n_raw[0] * n_raw[1] * n_raw[2];
+  const size_t niso = (size_t)L.g.n[0] * L.g.n[1] * L.g.n[2];
+  auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
+  return al(nraw * sizeof(uint16_t)) + al(niso * sizeof(int32_t)) + al((size_t)max_cells * sizeof(snk_cell));
+}
+
+int32_t snk_run_batch_workspace_bytes(int32_t dim, const int64_t n_raw[3], const double spacing[3],
+                                      const snk_params* p, int64_t max_cells, size_t* bytes) {
+  clear_error();
+  if (!bytes || !n_raw || !spacing || max_cells < 1) return fail(SNK_CONFIG, "bad args");
+  RunLayout L;
+  SNK_TRY(run_layout(dim, n_raw, spacing, p, max_cells, &L));
+  *bytes = ((L.total + 255) & ~size_t(255)) + batch_extra(L, n_raw, max_cells);
+  return SNK_OK;
+}
+
+int32_t snk_run_batch(int32_t dim, const int64_t n_raw[3], const double spacing[3],
+                      const snk_params* p, int64_t nvol, const uint16_t* const* h_raw,
+                      snk_cell* const* h_dets, int64_t det_cap, int64_t* n_dets,
+                      int32_t* const* h_labels, int64_t max_cells, void* d_ws, size_t ws_bytes,
+                      void* stream) {
+  clear_error();
+  if (nvol < 0 || (nvol > 0 && (!h_raw || !n_dets || !h_dets)) || det_cap < 0 || max_cells < 1)
+    return fail(SNK_CONFIG, "bad args");
+  RunLayout L;
+  SNK_TRY(run_layout(dim, n_raw, spacing, p, max_cells, &L));
+  const size_t off2 = (L.total + 255) & ~size_t(255);
+  SNK_TRY(check_ws(off2 + batch_extra(L, n_raw, max_cells), d_ws, ws_bytes));
+  for (int64_t i = 0; i < nvol; ++i)
+    if (!h_raw[i] || (det_cap > 0 && !h_dets[i])) return fail(SNK_CONFIG, "null host buffer");
+  if (nvol == 0) return SNK_OK;
+  cudaStream_t st = as_stream(stream);
+  char* base = static_cast<char*>(d_ws);
+  const size_t nraw = (size_t)n_raw[0] * n_raw[1] * n_raw[2];
+  const size_t niso = (size_t)L.g.n[0] * L.g.n[1] * L.g.n[2];
+  auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
+  uint16_t* raw[2] = {reinterpret_cast<uint16_t*>(base + L.off_raw), reinterpret_cast<uint16_t*>(base + off2)};
+  int32_t* lab[2] = {reinterpret_cast<int32_t*>(base + L.off_labels),
+                     reinterpret_cast<int32_t*>(base + off2 + al(nraw * 2))};
+  snk_cell* dets[2] = {reinterpret_cast<snk_cell*>(base + L.off_dets),
+                       reinterpret_cast<snk_cell*>(base + off2 + al(nraw * 2) + al(niso * 4))};
+  const bool want_labels = h_labels != nullptr;
+  cudaStream_t su = nullptr, sd = nullptr;
+  cudaEvent_t up[2] = {}, raw_free[2] = {}, done[2] = {}, out_free[2] = {};
+  int32_t status = SNK_OK;
+  auto ck = [&](cudaError_t e, const char* w) {
+    if (e != cudaSuccess && status == SNK_OK) status = cuda_fail(e, w);
+    return status == SNK_OK;
+  };
+  bool ok = ck(cudaStreamCreateWithFlags(&su, cudaStreamNonBlocking), "cudaStreamCreate") &&
+            ck(cudaStreamCreateWithFlags(&sd, cudaStreamNonBlocking), "cudaStreamCreate");
+  for (int k = 0; k < 2 && ok; ++k)
+    ok = ck(cudaEventCreateWithFlags(&up[k], cudaEventDisableTiming), "cudaEventCreate") &&
+         ck(cudaEventCreateWithFlags(&raw_free[k], cudaEventDisableTiming), "cudaEventCreate") &&
+         ck(cudaEventCreateWithFlags(&done[k], cudaEventDisableTiming), "cudaEventCreate") &&
+         ck(cudaEventCreateWithFlags(&out_free[k], cudaEventDisableTiming), "cudaEventCreate");
+  if (ok) ok = ck(cudaMemcpyAsync(raw[0], h_raw[0], nraw * 2, cudaMemcpyHostToDevice, su), "upload") &&
+               ck(cudaEventRecord(up[0], su), "cudaEventRecord");
+  for (int64_t i = 0; i < nvol && ok; ++i) {
+    const int s = (int)(i & 1), s1 = 1 - s;
+    if (i + 1 < nvol) {   // upload the next volume once its buffer has been consumed
+      if (i >= 1) ok = ck(cudaStreamWaitEvent(su, raw_free[s1], 0), "wait");
+      ok = ok && ck(cudaMemcpyAsync(raw[s1], h_raw[i + 1], nraw * 2, cudaMemcpyHostToDevice, su), "upload") &&
+           ck(cudaEventRecord(up[s1], su), "cudaEventRecord");
+    }
+    ok = ok && ck(cudaStreamWaitEvent(st, up[s], 0), "wait");
+    if (i >= 2) ok = ok && ck(cudaStreamWaitEvent(st, out_free[s], 0), "wait");   // results i-2 downloaded
+    if (!ok) break;
+    int64_t nd = 0;
+    const int32_t rs = run_compute(L, dim, n_raw, spacing, p, raw[s], dets[s], want_labels ? lab[s] : nullptr,
+                                   max_cells, base, st, raw_free[s], &nd);
+    if (rs != SNK_OK) { status = rs; break; }
+    n_dets[i] = nd;
+    ok = ck(cudaEventRecord(done[s], st), "cudaEventRecord") && ck(cudaStreamWaitEvent(sd, done[s], 0), "wait");
+    const int64_t ncopy = std::min(nd, det_cap);
+    if (ok && ncopy > 0)
+      ok = ck(cudaMemcpyAsync(h_dets[i], dets[s], ncopy * sizeof(snk_cell), cudaMemcpyDeviceToHost, sd), "download");
+    if (ok && want_labels && h_labels[i])
+      ok = ck(cudaMemcpyAsync(h_labels[i], lab[s], niso * sizeof(int32_t), cudaMemcpyDeviceToHost, sd), "download");
+    ok = ok && ck(cudaEventRecord(out_free[s], sd), "cudaEventRecord");
+    if (nd > det_cap && status == SNK_OK) status = fail(SNK_CAPACITY, "detection buffer too small");
+  }
+  // drain and release (also on failure)
+  if (su) { cudaStreamSynchronize(su); }
+  if (sd) { cudaStreamSynchronize(sd); }
+  cudaStreamSynchronize(st);
+  for (int k = 0; k < 2; ++k) {
+    if (up[k]) cudaEventDestroy(up[k]);
+    if (raw_free[k]) cudaEventDestroy(raw_free[k]);
+    if (done[k]) cudaEventDestroy(done[k]);
+    if (out_free[k]) cudaEventDestroy(out_free[k]);
+  }
+  if (su) cudaStreamDestroy(su);
+  if (sd) cudaStreamDestroy(sd);
+  return status;
 }
 
 }  // extern "C"

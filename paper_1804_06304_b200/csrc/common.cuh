@@ -117,6 +117,12 @@ int32_t cull_impl(const snk_grid* g, const snk_params* p, const snk_cell* d_cell
 int32_t label_impl(const snk_grid* g, const snk_params* p, const snk_cell* d_dets, int64_t n,
                    int32_t* d_labels, void* d_ws, size_t ws_bytes, cudaStream_t st);
 
+// Small device -> host readback (counts; <= 256 bytes), then synchronises st.
+// A one-thread kernel stores into mapped pinned host memory, so the readback
+// never queues behind a bulk copy on the copy engines (snk_run_batch downloads
+// a label map while the next volume's kernels need their counts).
+int32_t read_back(const void* d_src, void* h_dst, size_t bytes, cudaStream_t st);
+
 int evolve_warps_per_cell(const snk_params* p, int64_t n_cells);
 int32_t evolve_stats(int64_t out[4], bool reset);
 

@@ -288,8 +288,7 @@ int32_t compact(int64_t n, Pred pred, Emit emit, int64_t cap, int* counts, int64
   SNK_LAUNCH_CHECK("scan_kernel");
   flag_write_kernel<<<(unsigned)nb, 1024, 0, st>>>(n, pred, emit, offsets, cap);
   SNK_LAUNCH_CHECK("flag_write_kernel");
-  SNK_CUDA_CHECK(cudaMemcpyAsync(n_out, offsets + nb, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-  SNK_CUDA_CHECK(cudaStreamSynchronize(st));
+  SNK_TRY(read_back(offsets + nb, n_out, sizeof(int64_t), st));
   return SNK_OK;
 }
 
@@ -480,15 +479,13 @@ int32_t cull_impl(const snk_grid* g, const snk_params* p, const snk_cell* d_cell
     SNK_LAUNCH_CHECK("bitonic_shared_kernel");
   }
   Scalars h{};
-  SNK_CUDA_CHECK(cudaMemcpyAsync(&h, sc, sizeof(Scalars), cudaMemcpyDeviceToHost, st));
-  SNK_CUDA_CHECK(cudaStreamSynchronize(st));
+  SNK_TRY(read_back(sc, &h, sizeof(Scalars), st));
   if (h.bad_id) return fail(SNK_SHAPE, "cull needs cell ids in [0, 2^32)");
   const int64_t nc = (int64_t)h.ncand;
   if (nc == 0) return SNK_OK;
   gather_sorted_kernel<<<(unsigned)ceil_div(nc, 256), 256, 0, st>>>(d_cells, vals, nc, S, &sc->rmax_bits);
   SNK_LAUNCH_CHECK("gather_sorted_kernel");
-  SNK_CUDA_CHECK(cudaMemcpyAsync(&h, sc, sizeof(Scalars), cudaMemcpyDeviceToHost, st));
-  SNK_CUDA_CHECK(cudaStreamSynchronize(st));
+  SNK_TRY(read_back(sc, &h, sizeof(Scalars), st));
   const double rho = rho_of(g->dim);
   float rmax = 0.0f;
   std::memcpy(&rmax, &h.rmax_bits, sizeof rmax);
@@ -525,8 +522,7 @@ int32_t cull_impl(const snk_grid* g, const snk_params* p, const snk_cell* d_cell
                                                                   &sc->undecided);
     SNK_LAUNCH_CHECK("mis_round_kernel");
     unsigned long long und = 0;
-    SNK_CUDA_CHECK(cudaMemcpyAsync(&und, &sc->undecided, sizeof und, cudaMemcpyDeviceToHost, st));
-    SNK_CUDA_CHECK(cudaStreamSynchronize(st));
+    SNK_TRY(read_back(&sc->undecided, &und, sizeof und, st));
     if (und == 0) break;
     if (round > nc + 2) return fail(SNK_INTERNAL, "overlap competition did not converge");
   }

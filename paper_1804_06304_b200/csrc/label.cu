@@ -215,8 +215,7 @@ int32_t label_impl(const snk_grid* g, const snk_params* p, const snk_cell* d_det
   }
   SNK_TRY(scan_counts(counts, ntiles, offsets, st, stmp));
   int64_t total = 0;
-  SNK_CUDA_CHECK(cudaMemcpyAsync(&total, offsets + ntiles, sizeof total, cudaMemcpyDeviceToHost, st));
-  SNK_CUDA_CHECK(cudaStreamSynchronize(st));
+  SNK_TRY(read_back(offsets + ntiles, &total, sizeof total, st));
   if ((size_t)total > ent_cap) return fail(SNK_CAPACITY, "detection radii exceed r_max: tile lists overflow");
   if (n > 0) {
     tile_fill_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(d_dets, n, G, offsets, cursor, entries);

@@ -648,8 +648,7 @@ int32_t seeds_impl(const snk_grid* g, const snk_params* p, const uint16_t* d_smo
                                                       grid_scale(g, 0), grid_scale(g, 1), grid_scale(g, 2));
     SNK_LAUNCH_CHECK("bits_write_kernel");
     int64_t total = 0;
-    SNK_CUDA_CHECK(cudaMemcpyAsync(&total, woff + nbw, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-    SNK_CUDA_CHECK(cudaStreamSynchronize(st));
+    SNK_TRY(read_back(woff + nbw, &total, sizeof(int64_t), st));
     *n_out = total;
     if (total > cap) return fail(SNK_CAPACITY, "seed buffer too small");
     return SNK_OK;
@@ -713,8 +712,7 @@ int32_t seeds_impl(const snk_grid* g, const snk_params* p, const uint16_t* d_smo
     bits_write_kernel<<<(unsigned)nbw, 1024, 0, st>>>(bits, nw, F.wpr, nx, ny, F.own_z0, woff, d_seeds, cap, 0);
     SNK_LAUNCH_CHECK("bits_write_kernel");
     int64_t total = 0;
-    SNK_CUDA_CHECK(cudaMemcpyAsync(&total, woff + nbw, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-    SNK_CUDA_CHECK(cudaStreamSynchronize(st));
+    SNK_TRY(read_back(woff + nbw, &total, sizeof(int64_t), st));
     *n_out = total;
     if (total > cap) return fail(SNK_CAPACITY, "seed buffer too small");
     return SNK_OK;
@@ -763,8 +761,7 @@ int32_t seeds_impl(const snk_grid* g, const snk_params* p, const uint16_t* d_smo
   maxima_write_kernel<<<(unsigned)nb, kCompactThreads, 0, st>>>(A, offsets, d_seeds, cap);
   SNK_LAUNCH_CHECK("maxima_write_kernel");
   int64_t total = 0;
-  SNK_CUDA_CHECK(cudaMemcpyAsync(&total, offsets + nb, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-  SNK_CUDA_CHECK(cudaStreamSynchronize(st));
+  SNK_TRY(read_back(offsets + nb, &total, sizeof(int64_t), st));
   *n_out = total;
   if (total > cap) return fail(SNK_CAPACITY, "seed buffer too small");
   return SNK_OK;

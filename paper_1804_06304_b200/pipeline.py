@@ -211,6 +211,38 @@ class HostRunner:
         return self.h_dets[: n * 48].numpy().view(snk.CELL_DTYPE).copy()
 
 
+class BatchRunner:
+    """The end-to-end call for a stream of volumes (snk_run_batch): host raw
+    volumes in, host detections and label maps out; the next volume's upload
+    and the previous results' download overlap the current volume's kernels."""
+
+    def __init__(self, dim, n_raw, params, spacing=(1.0, 1.0, 1.0), max_cells=None, labels=True,
+                 device="cuda"):
+        self.dim, self.n_raw, self.spacing, self.params = dim, tuple(n_raw), tuple(spacing), params
+        n_iso = snk.snk_resample_dims(dim, self.n_raw, self.spacing)
+        nvox = n_iso[0] * n_iso[1] * n_iso[2]
+        if max_cells is None:
+            max_cells = max(1024, nvox // max(1, (2 * max(params.seed_window, 1) + 1) ** dim) + 1024)
+        self.max_cells = int(max_cells)
+        ws = snk.snk_run_batch_workspace_bytes(dim, self.n_raw, self.spacing, params, self.max_cells)
+        self.ws = torch.empty(ws, dtype=torch.uint8, device=device)
+        # two result slots are in flight at a time; volumes alternate between them
+        self.h_dets = [torch.empty(self.max_cells * 48, dtype=torch.uint8, pin_memory=True) for _ in range(2)]
+        self.h_labels = ([torch.empty((n_iso[2], n_iso[1], n_iso[0]), dtype=torch.int32, pin_memory=True)
+                          for _ in range(2)] if labels else None)
+        self.n_iso = n_iso
+
+    def run(self, h_raws, stream=None) -> list:
+        k = len(h_raws)
+        dets = [self.h_dets[i % 2] for i in range(k)]
+        labs = [self.h_labels[i % 2] for i in range(k)] if self.h_labels is not None else None
+        return snk.snk_run_batch(self.dim, self.n_raw, self.spacing, self.params, list(h_raws), dets,
+                                 self.max_cells, labs, self.max_cells, self.ws, stream)
+
+    def dets_np(self, slot, n) -> np.ndarray:
+        return self.h_dets[slot][: n * 48].numpy().view(snk.CELL_DTYPE).copy()
+
+
 def wall(fn, *a, **k):
     t = time.perf_counter()
     r = fn(*a, **k)

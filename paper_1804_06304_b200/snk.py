@@ -91,6 +91,9 @@ _SIGS = {
     "snk_run_workspace_bytes": (_i32, [_i32, _vp, _vp, _P(snk_params), _i64, _P(_sz)]),
     "snk_run": (_i32, [_i32, _vp, _vp, _P(snk_params), _vp, _vp, _i64, _P(_i64), _vp, _i64, _vp, _sz,
                        _vp]),
+    "snk_run_batch_workspace_bytes": (_i32, [_i32, _vp, _vp, _P(snk_params), _i64, _P(_sz)]),
+    "snk_run_batch": (_i32, [_i32, _vp, _vp, _P(snk_params), _i64, _vp, _vp, _i64, _vp, _vp, _i64, _vp, _sz,
+                             _vp]),
     "snk_launch_count": (_i64, []),
     "snk_evolve_stats": (_i32, [_vp, _i32]),
 }
@@ -277,6 +280,30 @@ def snk_run(dim, n_raw, spacing, p, h_raw, h_dets, det_cap, h_labels, max_cells,
                         det_cap, C.byref(nd), _ptr(h_labels), max_cells, _ptr(d_ws), _nbytes(d_ws),
                         _stream(stream)), "snk_run")
     return nd.value
+
+
+def snk_run_batch_workspace_bytes(dim, n_raw, spacing, p, max_cells) -> int:
+    n = (C.c_int64 * 3)(*[int(a) for a in n_raw])
+    sp = (C.c_double * 3)(*[float(a) for a in spacing])
+    out = C.c_size_t()
+    _check(_lib.snk_run_batch_workspace_bytes(dim, n, sp, C.byref(p), max_cells, C.byref(out)),
+           "snk_run_batch_workspace_bytes")
+    return out.value
+
+
+def snk_run_batch(dim, n_raw, spacing, p, h_raws, h_dets, det_cap, h_labels, max_cells, d_ws, stream=None):
+    """h_raws / h_dets / h_labels: sequences of host buffers (one per volume; the
+    same buffer may repeat); returns the detection counts."""
+    k = len(h_raws)
+    n = (C.c_int64 * 3)(*[int(a) for a in n_raw])
+    sp = (C.c_double * 3)(*[float(a) for a in spacing])
+    raws = (C.c_void_p * k)(*[_ptr(b) for b in h_raws])
+    dets = (C.c_void_p * k)(*[_ptr(b) for b in h_dets])
+    labs = (C.c_void_p * k)(*[_ptr(b) for b in h_labels]) if h_labels is not None else None
+    nd = (C.c_int64 * max(k, 1))()
+    _check(_lib.snk_run_batch(dim, n, sp, C.byref(p), k, raws, dets, det_cap, nd, labs, max_cells, _ptr(d_ws),
+                              _nbytes(d_ws), _stream(stream)), "snk_run_batch")
+    return [int(nd[i]) for i in range(k)]
 
 
 # ---------------------------------------------------------------- struct helpers

@@ -788,3 +788,25 @@ def test_brick_fast_path_bit_identical_to_warp_kernel(gpu, N, W):
     P.evolve()
     torch.cuda.synchronize()
     assert P.cells_np().tobytes() == a.tobytes()
+
+
+def test_run_batch_equals_run(gpu):
+    """snk_run_batch (uploads / downloads overlapped with the kernels on internal
+    streams, double-buffered) gives, volume by volume, the bytes of snk_run."""
+    torch, snk, pipeline = gpu
+    cfg = synth.CONFIGS["C1"].with_(max_iters=80)
+    p = pipeline.params_for(cfg)
+    raws = [torch.from_numpy(synth.generate(cfg.with_(gen_seed=cfg.gen_seed + i))).pin_memory() for i in range(3)]
+    hr = pipeline.HostRunner(3, cfg.n, p)
+    exp = []
+    for r in raws:
+        nd = hr.run(r)
+        exp.append((hr.dets_np(nd).tobytes(), hr.h_labels.numpy().copy()))
+    br = pipeline.BatchRunner(3, cfg.n, p, max_cells=hr.max_cells)
+    seq = [raws[0], raws[1], raws[2], raws[1]]
+    nds = br.run(seq)
+    assert len(nds) == 4
+    # slots alternate: volume 2 -> slot 0, volume 3 (= raws[1]) -> slot 1
+    assert br.dets_np(0, nds[2]).tobytes() == exp[2][0] and np.array_equal(br.h_labels[0].numpy(), exp[2][1])
+    assert br.dets_np(1, nds[3]).tobytes() == exp[1][0] and np.array_equal(br.h_labels[1].numpy(), exp[1][1])
+    assert nds[0] == len(exp[0][0]) // 48 and nds[1] == len(exp[1][0]) // 48
