@@ -111,8 +111,8 @@ def exchange_halo(plan: SlabPlan, own_raw: torch.Tensor, group=None) -> torch.Te
 
 
 def _wire(t: torch.Tensor) -> torch.Tensor:
-    """u16 planes travel as int16 (same bytes; NCCL/gloo have no uint16)."""
-    return t.view(torch.int16) if t.dtype == torch.uint16 else t
+    """u16 planes travel as bytes (NCCL has no 16-bit integer type; gloo no uint16)."""
+    return t.view(torch.uint8) if t.dtype == torch.uint16 else t
 
 
 def plan_like(plan: SlabPlan, rank: int) -> SlabPlan:
@@ -287,6 +287,7 @@ def bench_rank(args, cfg):
         tdist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     else:
         tdist.init_process_group(backend)
+    tdist.barrier()   # a collective over all ranks before the first point-to-point batch (NCCL)
     assert tuple(cfg.iso_n) == tuple(cfg.n), "the slab driver takes isotropic volumes"
     p = pipeline.params_for(cfg, image_term=snk.IMAGE_INTENSITY, cull_every=getattr(args, "cull_every", 0))
     plan = plan_slabs(cfg.n, world, rank, p)
