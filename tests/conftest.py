@@ -28,3 +28,23 @@ def gpu():
         pytest.skip("no CUDA device")
     from paper_1804_06304_b200 import pipeline, snk
     return torch, snk, pipeline
+
+
+GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+
+def golden_rows(name):
+    """Whitespace-separated rows of tests/golden/<name> (comments '#' stripped)."""
+    rows = []
+    for line in open(os.path.join(GOLDEN, name)):
+        line = line.split("#", 1)[0].strip()
+        if line:
+            rows.append(line.split())
+    return rows
+
+
+def golden_value(key):
+    for row in golden_rows("worked_examples.txt"):
+        if row[0] == key:
+            return float(row[1])
+    raise KeyError(key)

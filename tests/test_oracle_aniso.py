@@ -20,6 +20,8 @@ import numpy as np
 import pytest
 from scipy import ndimage, special
 
+from conftest import golden_value
+
 SC = (1.0, 1.0, 2.0)
 
 
@@ -118,5 +120,5 @@ def test_equilibrium_radius_on_anisotropic_grid(ora):
     p = ora.Params(r0=10.0, n_samples=1024, dim=3, scale=SC)
     seeds = np.array([[25.0, 22.5, 24.0]] * 8, np.float32)
     cells = ora.evolve(vol, p, seeds, ids=np.arange(8) * 7 + 3)
-    assert abs(cells["R"].mean() - 12.8493) < 0.15
+    assert abs(cells["R"].mean() - golden_value("equilibrium_radius_3d")) < 0.15
     assert np.all(np.abs(cells["c"] - [24.0, 23.5, 23.0]).max(axis=1) < 0.3)

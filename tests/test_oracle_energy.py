@@ -14,6 +14,8 @@ import numpy as np
 import pytest
 from scipy import integrate
 
+from conftest import golden_rows
+
 import synth
 
 warnings.filterwarnings("ignore", category=integrate.IntegrationWarning)
@@ -29,8 +31,11 @@ def blob_energy_quad(ora, R, r0, dim, dR=1e-4):
     return 2.0 * area * val
 
 
-@pytest.mark.parametrize("R,expect", [(8.0, 0.0), (9.0, 0.0), (12.0, -6098.8785),
-                                      (13.0, -8377.5804), (16.0, -8377.5804)])
+# Eq. 3 values (tests/golden/eq3_closed_form.txt)
+EQ3 = {d: [(float(r[1]), float(r[2])) for r in golden_rows("eq3_closed_form.txt") if int(r[0]) == d] for d in (2, 3)}
+
+
+@pytest.mark.parametrize("R,expect", EQ3[3])
 def test_eq3_closed_form_3d(ora, R, expect):
     # Eq. 3: 0 | -(8/3) pi (R^3 - r0^3) | -(8/3) pi r0^3, r0 = 10
     closed = (0.0 if R < 10 else (-(8 / 3) * math.pi * (R ** 3 - 1000) if R / 2 ** (1 / 3) < 10
@@ -39,8 +44,7 @@ def test_eq3_closed_form_3d(ora, R, expect):
     assert blob_energy_quad(ora, R, 10.0, 3) == pytest.approx(expect, rel=1e-3, abs=0.05)
 
 
-@pytest.mark.parametrize("R,expect", [(8.0, 0.0), (12.0, -276.4602), (14.2, -628.3185),
-                                      (20.0, -628.3185)])
+@pytest.mark.parametrize("R,expect", EQ3[2])
 def test_eq3_analogue_2d(ora, R, expect):
     # 2D analogue with rho = 1/sqrt(2): -2 pi (R^2/2 - ... ) etc.
     assert blob_energy_quad(ora, R, 10.0, 2) == pytest.approx(expect, rel=1e-3, abs=0.05)

@@ -14,6 +14,7 @@ import pytest
 from scipy import integrate, optimize, special
 
 import synth
+from conftest import golden_value
 
 
 def blurred_ball(r, r0, sigma, A):
@@ -57,7 +58,7 @@ def test_equilibrium_radius_3d(ora, mode):
     evolution of centred snakes converges to within 0.1 of it — plain MC (0),
     with the control variate (2) and with the stratified ray march (3)."""
     rstar = radial_argmin(ora, lambda r: blurred_ball(r, 10.0, 1.0, 100.0), 3, lo=11, hi=14)
-    assert rstar == pytest.approx(12.8493, abs=2e-3)
+    assert rstar == pytest.approx(golden_value("equilibrium_radius_3d"), abs=2e-3)
     vol = _ball_volume(48, (24.0, 24.0, 24.0), 10.0, ora=ora)
     p = ora.Params(r0=10.0, n_samples=1024, dim=3, mode=mode)
     seeds = np.array([[25.0, 23.0, 24.5]] * 8, np.float32)
@@ -71,7 +72,7 @@ def test_equilibrium_radius_2d(ora):
     """2D mode: blurred disk r0 = 15, A = 100, sigma = 1: R* = 21.3630
     (hard-edge theory sqrt(2) r0 = 21.2132)."""
     rstar = radial_argmin(ora, lambda r: blurred_disk(r, 15.0, 1.0, 100.0), 2, lo=19, hi=23)
-    assert rstar == pytest.approx(21.3630, abs=2e-3)
+    assert rstar == pytest.approx(golden_value("equilibrium_radius_2d"), abs=2e-3)
     v = synth.sphere_volume((72, 72, 1), (36.0, 36.0, 0.0), 15.0, amp=100.0, supersample=6)
     vol = ora.blur(v, 2, 1.0)
     p = ora.Params(r0=25.0, n_samples=1024, dim=2)

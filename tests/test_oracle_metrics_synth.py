@@ -5,14 +5,16 @@ import pytest
 import synth
 from oracle import metrics
 
+from conftest import golden_value
+
 
 def test_table1_arithmetic():
     # Table I row "3D snakuscules": P = 0.97, R = 0.84 -> F = 0.90;
     # G23: SPEC AC10's 0.8953 is wrong, F(0.97, 0.84) = 0.9003.
-    assert metrics.f_measure(0.97, 0.84) == pytest.approx(0.9003, abs=5e-5)
+    assert metrics.f_measure(0.97, 0.84) == pytest.approx(golden_value("f_measure_spec_ac10"), abs=5e-5)
     assert round(metrics.f_measure(0.97, 0.84), 2) == 0.90
     # G22: the CellSegm row is internally inconsistent (0.7615, printed 0.82)
-    assert metrics.f_measure(0.66, 0.90) == pytest.approx(0.7615, abs=5e-5)
+    assert metrics.f_measure(0.66, 0.90) == pytest.approx(golden_value("f_measure_cellsegm"), abs=5e-5)
     assert metrics.prf(0, 0, 0) == (0.0, 0.0, 0.0)
 
 

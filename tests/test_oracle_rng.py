@@ -9,13 +9,12 @@ import pytest
 from scipy import stats
 
 
-# Random123 philox4x32_10 KAT vectors (kat_vectors, "philox4x32 10").
-KAT = [
-    ([0, 0, 0, 0], [0, 0], [0x6627e8d5, 0xe169c58d, 0xbc57ac4c, 0x9b00dbd8]),
-    ([0xffffffff] * 4, [0xffffffff] * 2, [0x408f276d, 0x41c83b0e, 0xa20bc7c6, 0x6d5451fd]),
-    ([0x243f6a88, 0x85a308d3, 0x13198a2e, 0x03707344], [0xa4093822, 0x299f31d0],
-     [0xd16cfe09, 0x94fdcceb, 0x5001e420, 0x24126ea1]),
-]
+from conftest import golden_rows
+
+# Random123 philox4x32_10 KAT vectors (tests/golden/philox4x32_10_kat.txt, with its citation)
+KAT = [([int(x, 16) for x in r[0:4]], [int(x, 16) for x in r[5:7]], [int(x, 16) for x in r[8:12]])
+       for r in golden_rows("philox4x32_10_kat.txt")]
+assert len(KAT) == 3
 
 
 @pytest.mark.parametrize("ctr,key,expect", KAT)
