@@ -810,3 +810,27 @@ def test_run_batch_equals_run(gpu):
     assert br.dets_np(0, nds[2]).tobytes() == exp[2][0] and np.array_equal(br.h_labels[0].numpy(), exp[2][1])
     assert br.dets_np(1, nds[3]).tobytes() == exp[1][0] and np.array_equal(br.h_labels[1].numpy(), exp[1][1])
     assert nds[0] == len(exp[0][0]) // 48 and nds[1] == len(exp[1][0]) // 48
+
+
+def test_run_batch_resampled_and_periodic(gpu):
+    """snk_run_batch with an anisotropic (resampled) volume and periodic culling:
+    the raw buffer is recycled only after a1/a2 consumed it; results equal snk_run."""
+    torch, snk, pipeline = gpu
+    c3 = synth.CONFIGS["C3"]
+    base = synth.generate(c3)
+    raws = [torch.from_numpy(np.ascontiguousarray(base[8 * i:8 * i + 24, 100:164, 64:128])).pin_memory()
+            for i in range(3)]
+    n = (64, 64, 24)
+    cfg = c3.with_(n=n, max_iters=60)
+    p = pipeline.params_for(cfg, cull_every=20)
+    hr = pipeline.HostRunner(3, n, p, spacing=c3.spacing)
+    exp = []
+    for r in raws:
+        nd = hr.run(r)
+        exp.append((hr.dets_np(nd).tobytes(), hr.h_labels.numpy().copy()))
+    br = pipeline.BatchRunner(3, n, p, spacing=c3.spacing, max_cells=hr.max_cells)
+    nds = br.run(raws)
+    # the last two volumes are still in the two result slots
+    assert br.dets_np(0, nds[2]).tobytes() == exp[2][0] and np.array_equal(br.h_labels[0].numpy(), exp[2][1])
+    assert br.dets_np(1, nds[1]).tobytes() == exp[1][0] and np.array_equal(br.h_labels[1].numpy(), exp[1][1])
+    assert nds[0] * 48 == len(exp[0][0])
