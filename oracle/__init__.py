@@ -126,6 +126,7 @@ def _declare(L):
         "ora_energy_mc": (None, [vp, vp, vp, vp, vp, vp, d, u32, i64, vp]),
         "ora_evolve_range": (None, [vp, vp, vp, vp, vp, vp, i64, i32, i32]),
         "ora_energy_grid": (None, [vp, vp, vp, vp, vp, vp, d, vp]),
+        "ora_interp": (None, [vp, vp, vp, vp, vp, vp, i64, vp, vp]),
         "ora_energy_ss": (d, [vp, vp, vp, vp, d, i32]),
         "ora_evolve": (None, [vp, vp, vp, vp, vp, vp, vp, i64, vp]),
         "ora_cull": (i32, [vp, vp, vp, vp, vp, i64, i32, d, vp, vp]),
@@ -282,6 +283,20 @@ def energy_mc(vol, params: Params, c, R, it, cell_id, org=None, n_global=None):
     pc = params.c()
     lib().ora_energy_mc(_p(v), _p(n), _p(o), _p(nb), C.byref(pc), _p(cc), R, it, cell_id, _p(out))
     return out
+
+
+def interp(vol, pts_xyz, dim=3, iscale=1.0, scale=(1.0, 1.0, 1.0), org=None, n_global=None):
+    """O5 step 4 (G17): d-linear lookup of the u16 volume at physical points
+    (x, y, z) — clamp to [0, n-1], i0 = min(floor(k), n-2), x then y then z —
+    times iscale.  Returns (values, halo flags)."""
+    v = _u16(vol)
+    n, o, nb = _box(v, org, n_global)
+    pc = Params(dim=dim, iscale=iscale, scale=tuple(scale)).c()
+    k = np.ascontiguousarray(pts_xyz, np.float64).reshape(-1, 3)
+    out = np.zeros(len(k))
+    halo = np.zeros(len(k), np.int32)
+    lib().ora_interp(_p(v), _p(n), _p(o), _p(nb), C.byref(pc), _p(k), len(k), _p(out), _p(halo))
+    return out, halo.astype(bool)
 
 
 def energy_grid(vol, params: Params, c, R):

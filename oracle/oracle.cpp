@@ -691,6 +691,18 @@ void ora_energy_mc(const uint16_t* v, const int64_t n[3], const int64_t org[3], 
   out6[5] = o.halo ? 1.0 : 0.0;
 }
 
+// The d-linear lookup itself (§8(c) O5 step 4, G17), exposed so that tests pin
+// it directly: out[i] = iscale * I(k_i) at the physical points k_i (xyz).
+void ora_interp(const uint16_t* v, const int64_t n[3], const int64_t org[3], const int64_t nb[3],
+                const ora_params* p, const double* k_xyz, int64_t npts, double* out, int32_t* halo_out) {
+  const Image img = make_image(v, n, org, nb, p);
+  for (int64_t i = 0; i < npts; ++i) {
+    bool halo = false;
+    out[i] = img.interp(&k_xyz[3 * i], &halo);
+    if (halo_out) halo_out[i] = halo ? 1 : 0;
+  }
+}
+
 void ora_energy_grid(const uint16_t* v, const int64_t n[3], const int64_t org[3], const int64_t nb[3],
                      const ora_params* p, const double c[3], double R, double* out6) {
   const Image img = make_image(v, n, org, nb, p);
