@@ -866,18 +866,29 @@ int ora_cull(const float* c_xyz, const float* R, const float* E, const uint32_t*
     if (E[a] != E[b]) return E[a] < E[b];
     return ids[a] < ids[b];
   });
+  // the kept cells' values (exact fp32 -> fp64 conversions) in kept order
   std::vector<int64_t> kept;
+  std::vector<double> kx, ky, kz, kR;
   for (int64_t i : cand) {
-    bool ok = true;
-    for (int64_t a : kept) {
-      const double dx = (double)c_xyz[3 * i] - (double)c_xyz[3 * a];
-      const double dy = (double)c_xyz[3 * i + 1] - (double)c_xyz[3 * a + 1];
-      const double dz = (double)c_xyz[3 * i + 2] - (double)c_xyz[3 * a + 2];
+    const double cx = (double)c_xyz[3 * i], cy = (double)c_xyz[3 * i + 1], cz = (double)c_xyz[3 * i + 2];
+    const double Ri = (double)R[i];
+    // "for every kept a: d2 >= t^2" — an AND over the kept set (order-free;
+    // OpenMP splits the set when it is large)
+    const int64_t nk = (int64_t)kept.size();
+    int ok = 1;
+#pragma omp parallel for reduction(&& : ok) schedule(static) if (nk > 8192)
+    for (int64_t a = 0; a < nk; ++a) {
+      const double dx = cx - kx[a];
+      const double dy = cy - ky[a];
+      const double dz = cz - kz[a];
       const double d2 = dx * dx + dy * dy + dz * dz;
-      const double t = rho * (double)std::max(R[i], R[a]);
-      if (!(d2 >= t * t)) { ok = false; break; }
+      const double t = rho * std::max(Ri, kR[a]);
+      ok = ok && (d2 >= t * t);
     }
-    if (ok) kept.push_back(i);
+    if (ok) {
+      kept.push_back(i);
+      kx.push_back(cx); ky.push_back(cy); kz.push_back(cz); kR.push_back(Ri);
+    }
   }
   *n_keep = (int64_t)kept.size();
   for (size_t k = 0; k < kept.size(); ++k) keep_idx[k] = kept[k];
