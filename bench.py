@@ -303,7 +303,7 @@ def run_ours(args):
             del runners
         e2e = {"value": samples * args.steps / e2e_s, "unit": UNIT,
                "h2d_bytes_per_step": int(h_raw.numel() * 2),
-               "d2h_bytes_per_step": int(nd * 48 + niso * 4),
+               "d2h_bytes_per_step": int(nd * 64 + niso * 4),
                "cells_per_s": n_cells * args.steps / e2e_s, "inflight": k, "mode": args.e2e_mode}
     cpu = None
     if not args.no_cpu_baseline:

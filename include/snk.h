@@ -35,7 +35,7 @@
 extern "C" {
 #endif
 
-#define SNK_ABI_VERSION 3
+#define SNK_ABI_VERSION 4
 
 /* Status codes — mirror SPEC's exit scheme plus CUDA / capacity. */
 typedef enum {
@@ -134,8 +134,14 @@ typedef struct snk_params {
   uint64_t seed;
 } snk_params;
 
-/* One contour (48 bytes): the per-cell "radius field" (a sphere: r(omega) = R),
- * centre, seed, final energy E_final (G13), flags, iterations run, global id. */
+/* One contour (64 bytes): the per-cell "radius field" (a sphere: r(omega) = R),
+ * centre, seed, final energy E_final (G13), flags, iterations run, global id.
+ * disp = c - seed is the evolved state itself: the kernels step the
+ * displacement from the seed (fp32 resolution ~2e-6 voxel at |disp| < 32)
+ * rather than the absolute centre (resolution 1.2e-4 voxel at x ~ 2000, which
+ * let the fp32 trajectory drift ~1e-3 voxel from the fp64 oracle's on C4);
+ * c = seed + disp rounded to fp32.  snk_evolve_range resumes from disp, so a
+ * segmented run is bit-identical to an uninterrupted one. */
 typedef struct snk_cell {
   float c[3];
   float R;
@@ -144,6 +150,8 @@ typedef struct snk_cell {
   uint32_t flags;
   int32_t iters;
   int64_t id;
+  float disp[3];
+  uint32_t reserved; /* 0 */
 } snk_cell;
 
 int32_t snk_abi_version(void);

@@ -538,4 +538,4 @@ int32_t snk_run_batch(int32_t dim, const int64_t n_raw[3], const double spacing[
 
 static_assert(sizeof(snk_grid) == 88, "snk_grid layout is part of the ABI");
 static_assert(sizeof(snk_params) == 136, "snk_params layout is part of the ABI");
-static_assert(sizeof(snk_cell) == 48, "snk_cell layout is part of the ABI");
+static_assert(sizeof(snk_cell) == 64, "snk_cell layout is part of the ABI");

@@ -720,11 +720,16 @@ __device__ __forceinline__ Acc warp_tree(const Acc* v) {
 
 __device__ __forceinline__ float clampf(float v, float lo, float hi) { return fminf(fmaxf(v, lo), hi); }
 
-// The per-cell state and the iteration update, shared by both kernels.
+// The per-cell state and the iteration update, shared by both kernels.  The
+// state is the displacement u = c - seed (snk_cell.disp): |u| <= leash, so fp32
+// resolves it to ~2e-6 voxel, where the absolute centre of a C4 cell (x up to
+// 2047) only has 1.2e-4 — stepping c itself let fp32 trajectories drift ~1e-3
+// from the fp64 oracle's (profiles/r2_state_precision.md).  The centre used by
+// an iteration is c = seed + u, rounded to fp32.
 struct CellState {
   float sx, sy, sz;     // seed
-  float cx, cy, cz, R, E;
-  float llo[3], lhi[3]; // leash box: seed -+ leash
+  float ux, uy, uz;     // displacement c - seed
+  float R, E;
   uint32_t flags;
   int64_t id;
   uint32_t q0, q1, q3;  // Philox round-1 words of the constant counter words (id), keyed
@@ -751,20 +756,14 @@ __device__ __forceinline__ void cell_begin(const EvoParams& P, int64_t cell, int
   s.q0 = (uint32_t)(p1 >> 32) ^ P.rk0[0];
   s.q1 = (uint32_t)p1;
   s.q3 = id_hi ^ P.rk1[0];
-  const float sd[3] = {s.sx, s.sy, s.sz};
-#pragma unroll
-  for (int a = 0; a < 3; ++a) {
-    s.llo[a] = __fsub_rn(sd[a], P.leash);
-    s.lhi[a] = __fadd_rn(sd[a], P.leash);
-  }
   if (P.state) {
     const snk_cell& r = P.state[cell];
-    s.cx = r.c[0]; s.cy = r.c[1]; s.cz = r.c[2];
+    s.ux = r.disp[0]; s.uy = r.disp[1]; s.uz = r.disp[2];
     s.R = r.R;
     s.E = r.energy;
     s.flags = r.flags;
   } else {
-    s.cx = s.sx; s.cy = s.sy; s.cz = s.sz;
+    s.ux = 0.0f; s.uy = 0.0f; s.uz = 0.0f;
     s.R = P.r0;
     s.E = 0.0f;
     s.flags = 0;
@@ -773,7 +772,9 @@ __device__ __forceinline__ void cell_begin(const EvoParams& P, int64_t cell, int
 
 __device__ __forceinline__ CellIt cell_iter(const EvoParams& P, const CellState& s, int it) {
   CellIt C;
-  C.cx = s.cx; C.cy = s.cy; C.cz = s.cz;
+  C.cx = __fadd_rn(s.sx, s.ux);
+  C.cy = __fadd_rn(s.sy, s.uy);
+  C.cz = __fadd_rn(s.sz, s.uz);
   C.rho_s = __fadd_rn(s.R, P.half_dR);
   C.a = __fmul_rn(-__fsub_rn(s.R, P.half_dR), P.inv_dR);
   C.p0 = s.q0 ^ (uint32_t)it;
@@ -814,38 +815,47 @@ __device__ __forceinline__ bool cell_update(const EvoParams& P, CellState& s, co
   const float dcy = clampf(-__fmul_rn(h, gcy), -P.max_step, P.max_step);
   const float dcz = D == 3 ? clampf(-__fmul_rn(h, gcz), -P.max_step, P.max_step) : 0.0f;
   const float dR = clampf(-__fmul_rn(h, gR), -P.max_step, P.max_step);
-  const float ox = s.cx, oy = s.cy, oz = s.cz, oR = s.R;
-  const float cx = __fadd_rn(s.cx, dcx), cy = __fadd_rn(s.cy, dcy), cz = __fadd_rn(s.cz, dcz);
+  const float ox = s.ux, oy = s.uy, oz = s.uz, oR = s.R;
+  const float cx = __fadd_rn(s.ux, dcx), cy = __fadd_rn(s.uy, dcy), cz = __fadd_rn(s.uz, dcz);
   const float R = clampf(__fadd_rn(s.R, dR), P.r_min, P.r_max);
-  // leash
-  const float lx = clampf(cx, s.llo[0], s.lhi[0]);
-  const float ly = clampf(cy, s.llo[1], s.lhi[1]);
-  const float lz = D == 3 ? clampf(cz, s.llo[2], s.lhi[2]) : cz;
-  // domain: c_a in [m, n_a - 1 - m], m = R + dR/2, or the axis centre when
-  // n_a - 1 < 2m (P.dom_small: possible for some axis at all)
+  // leash: |c_a - s_a| = |u_a| <= leash
+  const float lx = clampf(cx, -P.leash, P.leash);
+  const float ly = clampf(cy, -P.leash, P.leash);
+  const float lz = D == 3 ? clampf(cz, -P.leash, P.leash) : cz;
+  // domain: c_a = s_a + u_a in [m, L_a - m] (L_a = n_a - 1), m = R + dR/2, i.e.
+  // u_a in [m - s_a, (L_a - m) - s_a]; or c_a = L_a / 2 when L_a < 2m (P.dom_small:
+  // possible for some axis at all)
   const float m = __fadd_rn(R, P.half_dR);
   float dx, dy, dz = lz;
   if (NB) {
     const float m2 = __fmul_rn(2.0f, m);
     const bool small = P.dom_small != 0;
-    dx = (small && P.dom1[0] < m2) ? __fmul_rn(0.5f, P.dom1[0]) : clampf(lx, m, __fsub_rn(P.dom1[0], m));
-    dy = (small && P.dom1[1] < m2) ? __fmul_rn(0.5f, P.dom1[1]) : clampf(ly, m, __fsub_rn(P.dom1[1], m));
-    if (D == 3) dz = (small && P.dom1[2] < m2) ? __fmul_rn(0.5f, P.dom1[2]) : clampf(lz, m, __fsub_rn(P.dom1[2], m));
+    dx = (small && P.dom1[0] < m2) ? __fsub_rn(__fmul_rn(0.5f, P.dom1[0]), s.sx)
+                                   : clampf(lx, __fsub_rn(m, s.sx), __fsub_rn(__fsub_rn(P.dom1[0], m), s.sx));
+    dy = (small && P.dom1[1] < m2) ? __fsub_rn(__fmul_rn(0.5f, P.dom1[1]), s.sy)
+                                   : clampf(ly, __fsub_rn(m, s.sy), __fsub_rn(__fsub_rn(P.dom1[1], m), s.sy));
+    if (D == 3)
+      dz = (small && P.dom1[2] < m2) ? __fsub_rn(__fmul_rn(0.5f, P.dom1[2]), s.sz)
+                                     : clampf(lz, __fsub_rn(m, s.sz), __fsub_rn(__fsub_rn(P.dom1[2], m), s.sz));
   } else if (P.dom_small) {
     const float m2 = __fmul_rn(2.0f, m);
-    dx = P.dom1[0] < m2 ? __fmul_rn(0.5f, P.dom1[0]) : clampf(lx, m, __fsub_rn(P.dom1[0], m));
-    dy = P.dom1[1] < m2 ? __fmul_rn(0.5f, P.dom1[1]) : clampf(ly, m, __fsub_rn(P.dom1[1], m));
-    if (D == 3) dz = P.dom1[2] < m2 ? __fmul_rn(0.5f, P.dom1[2]) : clampf(lz, m, __fsub_rn(P.dom1[2], m));
+    dx = P.dom1[0] < m2 ? __fsub_rn(__fmul_rn(0.5f, P.dom1[0]), s.sx)
+                        : clampf(lx, __fsub_rn(m, s.sx), __fsub_rn(__fsub_rn(P.dom1[0], m), s.sx));
+    dy = P.dom1[1] < m2 ? __fsub_rn(__fmul_rn(0.5f, P.dom1[1]), s.sy)
+                        : clampf(ly, __fsub_rn(m, s.sy), __fsub_rn(__fsub_rn(P.dom1[1], m), s.sy));
+    if (D == 3)
+      dz = P.dom1[2] < m2 ? __fsub_rn(__fmul_rn(0.5f, P.dom1[2]), s.sz)
+                          : clampf(lz, __fsub_rn(m, s.sz), __fsub_rn(__fsub_rn(P.dom1[2], m), s.sz));
   } else {
-    dx = clampf(lx, m, __fsub_rn(P.dom1[0], m));
-    dy = clampf(ly, m, __fsub_rn(P.dom1[1], m));
-    if (D == 3) dz = clampf(lz, m, __fsub_rn(P.dom1[2], m));
+    dx = clampf(lx, __fsub_rn(m, s.sx), __fsub_rn(__fsub_rn(P.dom1[0], m), s.sx));
+    dy = clampf(ly, __fsub_rn(m, s.sy), __fsub_rn(__fsub_rn(P.dom1[1], m), s.sy));
+    if (D == 3) dz = clampf(lz, __fsub_rn(m, s.sz), __fsub_rn(__fsub_rn(P.dom1[2], m), s.sz));
   }
   if (NB) {
     const bool fin = it == P.T + 1;   // E_final only: no update
-    s.cx = fin ? ox : dx;
-    s.cy = fin ? oy : dy;
-    s.cz = fin ? oz : dz;
+    s.ux = fin ? ox : dx;
+    s.uy = fin ? oy : dy;
+    s.uz = fin ? oz : dz;
     s.R = fin ? oR : R;
     if (it == P.T) {   // the flags of the last step (a uniform branch after the update)
       float mv = fabsf(__fsub_rn(R, oR));
@@ -858,13 +868,13 @@ __device__ __forceinline__ bool cell_update(const EvoParams& P, CellState& s, co
     }
     return fin;
   }
-  s.cx = dx; s.cy = dy; s.cz = dz;
+  s.ux = dx; s.uy = dy; s.uz = dz;
   s.R = R;
   if (it == P.T) {
     float mv = fabsf(__fsub_rn(R, oR));
-    mv = fmaxf(mv, fabsf(__fsub_rn(s.cx, ox)));
-    mv = fmaxf(mv, fabsf(__fsub_rn(s.cy, oy)));
-    mv = fmaxf(mv, fabsf(__fsub_rn(s.cz, oz)));
+    mv = fmaxf(mv, fabsf(__fsub_rn(s.ux, ox)));
+    mv = fmaxf(mv, fabsf(__fsub_rn(s.uy, oy)));
+    mv = fmaxf(mv, fabsf(__fsub_rn(s.uz, oz)));
     if (mv < P.conv_tol) s.flags |= SNK_F_CONVERGED;
     if ((lx != cx) || (ly != cy) || (lz != cz)) s.flags |= SNK_F_LEASHED;
     if ((dx != lx) || (dy != ly) || (dz != lz)) s.flags |= SNK_F_DOMAIN;
@@ -878,7 +888,11 @@ __device__ __forceinline__ void cell_finish(const EvoParams& P, CellState& s, in
   if (s.R <= P.r_min) s.flags |= SNK_F_COLLAPSED;
   if (s.R >= P.r_max) s.flags |= SNK_F_RMAX;
   snk_cell o;
-  o.c[0] = s.cx; o.c[1] = s.cy; o.c[2] = s.cz;
+  o.c[0] = __fadd_rn(s.sx, s.ux);
+  o.c[1] = __fadd_rn(s.sy, s.uy);
+  o.c[2] = __fadd_rn(s.sz, s.uz);
+  o.disp[0] = s.ux; o.disp[1] = s.uy; o.disp[2] = s.uz;
+  o.reserved = 0;
   o.R = s.R;
   o.seed[0] = s.sx; o.seed[1] = s.sy; o.seed[2] = s.sz;
   o.energy = s.E;
@@ -1078,7 +1092,7 @@ __global__ void __launch_bounds__(32 * W, W == 4 ? SNK_BRICK_MINB4 : (W <= 2 ? 5
   static_assert(EST == 0 || (PIPE && CH == 8), "CV / RAY estimators: 8 samples per thread, pipelined draws");
   extern __shared__ __align__(16) uint16_t brick[];
   __shared__ __align__(16) float xch[2][5][W];      // [parity][component][warp]
-  __shared__ float bc[4];                           // PIPE: (cx, cy, cz, R) after warp 0's update
+  __shared__ float bc[4];                           // PIPE: (ux, uy, uz, R) after warp 0's update
   const int lane = threadIdx.x & 31, wsub = threadIdx.x >> 5;
   const int64_t cell = blockIdx.x;
   CellState s;
@@ -1094,7 +1108,7 @@ __global__ void __launch_bounds__(32 * W, W == 4 ? SNK_BRICK_MINB4 : (W <= 2 ? 5
   }
   for (int it = P.it0; it <= P.it1; ++it) {
     CellIt C = cell_iter(P, s, it);
-    const float c[3] = {s.cx, s.cy, s.cz};
+    const float c[3] = {C.cx, C.cy, C.cz};
     const int mode = bk.template prepare<est_aniso(EST)>(brick, P, c, C.rho_s);
     Acc part;
     C.boff = bk.boff;
@@ -1173,7 +1187,7 @@ __global__ void __launch_bounds__(32 * W, W == 4 ? SNK_BRICK_MINB4 : (W <= 2 ? 5
         sum.cz = comp_tree<W>(xo + 3 * W);
         sum.aR = comp_tree<W>(xo + 4 * W);
         cell_update<D, false, EST>(P, s, C, sum, it);
-        if (lane == 0) { bc[0] = s.cx; bc[1] = s.cy; bc[2] = s.cz; bc[3] = s.R; }
+        if (lane == 0) { bc[0] = s.ux; bc[1] = s.uy; bc[2] = s.uz; bc[3] = s.R; }
       }
       if (done) break;
       CellIt Cn;   // the next iteration's Philox key words
@@ -1183,7 +1197,7 @@ __global__ void __launch_bounds__(32 * W, W == 4 ? SNK_BRICK_MINB4 : (W <= 2 ? 5
       if constexpr (est_kind(EST) == SNK_EST_RAY) draw_dirs_ray<D>(P, Cn, j0 / 8u, dir);
       else draw_dirs<D, CH>(P, Cn, j0, dir);
       __syncthreads();
-      if (wsub != 0) { s.cx = bc[0]; s.cy = bc[1]; s.cz = bc[2]; s.R = bc[3]; }
+      if (wsub != 0) { s.ux = bc[0]; s.uy = bc[1]; s.uz = bc[2]; s.R = bc[3]; }
     } else {
       Acc sum;
       sum.a0 = comp_tree<W>(xo + 0 * W);
@@ -1226,7 +1240,7 @@ __global__ void __launch_bounds__(32 * W, 3) evolve_grid_kernel(const __grid_con
   const float fn1[3] = {P.fnx1, P.fny1, P.fnz1};
   for (int it = P.it0; it <= P.it1; ++it) {
     const CellIt C = cell_iter(P, s, it);
-    const float c[3] = {s.cx, s.cy, s.cz};
+    const float c[3] = {C.cx, C.cy, C.cz};
     const int mode = bk.prepare(brick, P, c, C.rho_s);
     const float rs = C.rho_s, rs2 = __fmul_rn(rs, rs);
     // the voxel box (a superset of the ball: membership is decided by r^2 < rs^2)
@@ -1398,7 +1412,11 @@ __global__ void cells_init_kernel(const float* seeds, const int64_t* ids, int64_
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   snk_cell o;
-  for (int a = 0; a < 3; ++a) o.c[a] = o.seed[a] = seeds[3 * i + a];
+  for (int a = 0; a < 3; ++a) {
+    o.c[a] = o.seed[a] = seeds[3 * i + a];
+    o.disp[a] = 0.0f;
+  }
+  o.reserved = 0;
   o.R = r0;
   o.energy = 0.0f;
   o.flags = 0;

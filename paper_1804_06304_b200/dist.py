@@ -12,7 +12,7 @@ Exchange steps (the only ones the method has):
   N1  raw halo planes from the ranks that own them (P2P, once per step);
   N2  all_gather of per-rank seed counts -> global ids = exclusive prefix
       (slabs are contiguous in linear-index order, so ids equal one GPU's);
-  N3  all_gather of the E0 candidates (48-byte snk_cell records); every rank
+  N3  all_gather of the E0 candidates (64-byte snk_cell records); every rank
       then runs the identical deterministic cull (the overlap competition
       crosses slab boundaries);
   labels stay distributed (each rank labels its own planes).
@@ -30,6 +30,8 @@ from dataclasses import dataclass
 
 import torch
 import torch.distributed as tdist
+
+CELL_BYTES = 64   # sizeof(snk_cell) (include/snk.h); kept here so the driver imports without libsnk
 
 
 @dataclass
@@ -132,7 +134,7 @@ def allgather_counts(count: int, device, group=None) -> list:
     return [int(o.item()) for o in outs]
 
 
-def allgather_records(rec: torch.Tensor, count: int, device, group=None, rec_bytes: int = 48):
+def allgather_records(rec: torch.Tensor, count: int, device, group=None, rec_bytes: int = CELL_BYTES):
     """N3: concatenate every rank's `count` records (uint8, rec_bytes each) in rank order."""
     if _staged(group) and torch.device(device).type == "cuda":
         allrec, tot, counts = allgather_records(rec[:count * rec_bytes].cpu(), count, "cpu", group, rec_bytes)
@@ -217,10 +219,10 @@ class CudaBackend:
         self.grad = torch.empty(shape, dtype=torch.uint16, device=dev) if gradmag else None
         self.max_cells = max_cells
         self.seeds_t = torch.empty((max_cells, 3), dtype=torch.float32, device=dev)
-        self.cells = torch.empty(max_cells * 48, dtype=torch.uint8, device=dev)
-        self.cand = torch.empty(max_cells * 48, dtype=torch.uint8, device=dev)
+        self.cells = torch.empty(max_cells * CELL_BYTES, dtype=torch.uint8, device=dev)
+        self.cand = torch.empty(max_cells * CELL_BYTES, dtype=torch.uint8, device=dev)
         self.total_cap = max_cells * plan.world
-        self.dets = torch.empty(self.total_cap * 48, dtype=torch.uint8, device=dev)
+        self.dets = torch.empty(self.total_cap * CELL_BYTES, dtype=torch.uint8, device=dev)
         self.labels = torch.empty((plan.own[1] - plan.own[0], n[1], n[0]), dtype=torch.int32, device=dev)
         ws = max(snk.snk_workspace_bytes(self.grid, params, self.total_cap), 1)
         self.ws = torch.empty(ws, dtype=torch.uint8, device=dev)
@@ -345,7 +347,7 @@ def bench_rank(args, cfg):
         own.copy_(h_raw, non_blocking=True)
         r = run.step(own)
         h_labels.copy_(r["labels"], non_blocking=True)
-        h_dets[:r["n_dets"] * 48].copy_(r["dets"][:r["n_dets"] * 48], non_blocking=True)
+        h_dets[:r["n_dets"] * CELL_BYTES].copy_(r["dets"][:r["n_dets"] * CELL_BYTES], non_blocking=True)
         torch.cuda.synchronize()
     wall = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=red_dev)
     tdist.all_reduce(wall, op=tdist.ReduceOp.MAX)
@@ -371,7 +373,7 @@ def bench_rank(args, cfg):
                "cpu_baseline": None,
                "e2e": {"value": samples * args.steps / e2e_s, "unit": "ray-samples/s",
                        "h2d_bytes_per_step": int(nown * 2 * world),
-                       "d2h_bytes_per_step": int(cfg.n[0] * cfg.n[1] * cfg.n[2] * 4 + r["n_dets"] * 48 * world)}}
+                       "d2h_bytes_per_step": int(cfg.n[0] * cfg.n[1] * cfg.n[2] * 4 + r["n_dets"] * CELL_BYTES * world)}}
     tdist.barrier()
     tdist.destroy_process_group()
     return out

@@ -3,6 +3,7 @@ of C-ABI calls.  PyTorch is used only for memory and streams; every step runs
 in libsnk's kernels."""
 from __future__ import annotations
 
+import contextlib
 import time
 from dataclasses import dataclass
 
@@ -25,7 +26,7 @@ def params_for(cfg, **over) -> snk.snk_params:
 
 def as_cells(t: torch.Tensor, n: int) -> np.ndarray:
     """Device byte buffer of snk_cell records -> numpy record array (copies n records)."""
-    return t[: n * 48].cpu().numpy().view(snk.CELL_DTYPE).copy()
+    return t[: n * snk.CELL_BYTES].cpu().numpy().view(snk.CELL_DTYPE).copy()
 
 
 @dataclass
@@ -72,8 +73,8 @@ class Pipeline:
         self.smooth = torch.empty(shape_iso, dtype=torch.uint16, device=dev)
         self.grad = torch.empty(shape_iso, dtype=torch.uint16, device=dev) if self.gradmag else None
         self.seeds = torch.empty((self.max_cells, 3), dtype=torch.float32, device=dev)
-        self.cells = torch.empty(self.max_cells * 48, dtype=torch.uint8, device=dev)
-        self.dets = torch.empty(self.max_cells * 48, dtype=torch.uint8, device=dev)
+        self.cells = torch.empty(self.max_cells * snk.CELL_BYTES, dtype=torch.uint8, device=dev)
+        self.dets = torch.empty(self.max_cells * snk.CELL_BYTES, dtype=torch.uint8, device=dev)
         self.labels = torch.empty(shape_iso, dtype=torch.int32, device=dev) if labels else None
         ws = snk.snk_workspace_bytes(self.grid, params, self.max_cells)
         if self.resample:
@@ -131,7 +132,9 @@ class Pipeline:
                 live = snk.snk_cull(self.grid, self.params, cur, live, nxt, self.max_cells, self.ws, stream)
                 cur, nxt = nxt, cur
         if cur is not self.cells and live:
-            self.cells[: live * 48].copy_(cur[: live * 48])
+            # on the stream the last segment ran on (the copy must follow it)
+            with torch.cuda.stream(stream) if stream is not None else contextlib.nullcontext():
+                self.cells[: live * snk.CELL_BYTES].copy_(cur[: live * snk.CELL_BYTES])
         self.n_live = live
 
     def cull(self, stream=None) -> int:
@@ -198,7 +201,7 @@ class HostRunner:
         self.max_cells = int(max_cells)
         ws = snk.snk_run_workspace_bytes(dim, self.n_raw, self.spacing, params, self.max_cells)
         self.ws = torch.empty(ws, dtype=torch.uint8, device=device)
-        self.h_dets = torch.empty(self.max_cells * 48, dtype=torch.uint8, pin_memory=True)
+        self.h_dets = torch.empty(self.max_cells * snk.CELL_BYTES, dtype=torch.uint8, pin_memory=True)
         self.h_labels = (torch.empty((n_iso[2], n_iso[1], n_iso[0]), dtype=torch.int32, pin_memory=True)
                          if labels else None)
         self.n_iso = n_iso
@@ -208,7 +211,7 @@ class HostRunner:
                            self.max_cells, self.h_labels, self.max_cells, self.ws, stream)
 
     def dets_np(self, n) -> np.ndarray:
-        return self.h_dets[: n * 48].numpy().view(snk.CELL_DTYPE).copy()
+        return self.h_dets[: n * snk.CELL_BYTES].numpy().view(snk.CELL_DTYPE).copy()
 
 
 class BatchRunner:
@@ -227,7 +230,7 @@ class BatchRunner:
         ws = snk.snk_run_batch_workspace_bytes(dim, self.n_raw, self.spacing, params, self.max_cells)
         self.ws = torch.empty(ws, dtype=torch.uint8, device=device)
         # two result slots are in flight at a time; volumes alternate between them
-        self.h_dets = [torch.empty(self.max_cells * 48, dtype=torch.uint8, pin_memory=True) for _ in range(2)]
+        self.h_dets = [torch.empty(self.max_cells * snk.CELL_BYTES, dtype=torch.uint8, pin_memory=True) for _ in range(2)]
         self.h_labels = ([torch.empty((n_iso[2], n_iso[1], n_iso[0]), dtype=torch.int32, pin_memory=True)
                           for _ in range(2)] if labels else None)
         self.n_iso = n_iso
@@ -240,7 +243,7 @@ class BatchRunner:
                                  self.max_cells, labs, self.max_cells, self.ws, stream)
 
     def dets_np(self, slot, n) -> np.ndarray:
-        return self.h_dets[slot][: n * 48].numpy().view(snk.CELL_DTYPE).copy()
+        return self.h_dets[slot][: n * snk.CELL_BYTES].numpy().view(snk.CELL_DTYPE).copy()
 
 
 def wall(fn, *a, **k):

@@ -60,12 +60,14 @@ class snk_params(C.Structure):
 class snk_cell(C.Structure):
     _fields_ = [("c", C.c_float * 3), ("R", C.c_float), ("seed", C.c_float * 3),
                 ("energy", C.c_float), ("flags", C.c_uint32), ("iters", C.c_int32),
-                ("id", C.c_int64)]
+                ("id", C.c_int64), ("disp", C.c_float * 3), ("reserved", C.c_uint32)]
 
 
 CELL_DTYPE = np.dtype([("c", "<f4", 3), ("R", "<f4"), ("seed", "<f4", 3), ("energy", "<f4"),
-                       ("flags", "<u4"), ("iters", "<i4"), ("id", "<i8")])
-assert CELL_DTYPE.itemsize == C.sizeof(snk_cell) == 48
+                       ("flags", "<u4"), ("iters", "<i4"), ("id", "<i8"), ("disp", "<f4", 3),
+                       ("reserved", "<u4")])
+CELL_BYTES = 64   # sizeof(snk_cell), include/snk.h
+assert CELL_DTYPE.itemsize == C.sizeof(snk_cell) == CELL_BYTES
 
 _vp, _i32, _i64, _sz = C.c_void_p, C.c_int32, C.c_int64, C.c_size_t
 _P = C.POINTER

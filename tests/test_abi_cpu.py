@@ -39,10 +39,10 @@ def test_library_is_sm100a_only(snk):
 
 
 def test_struct_layouts(snk):
-    assert C.sizeof(snk.snk_cell) == 48
+    assert C.sizeof(snk.snk_cell) == 64
     assert C.sizeof(snk.snk_grid) == 88                 # static_assert-ed in abi.cu too
     assert C.sizeof(snk.snk_params) == 136
-    assert snk.snk_abi_version() == 3
+    assert snk.snk_abi_version() == 4
     assert snk.status_string(0) == "ok" and snk.status_string(6) == "capacity exceeded"
 
 

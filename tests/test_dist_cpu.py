@@ -17,7 +17,7 @@ import synth
 from paper_1804_06304_b200 import dist as D
 
 REC = np.dtype([("c", "<f4", 3), ("R", "<f4"), ("seed", "<f4", 3), ("energy", "<f4"),
-                ("flags", "<u4"), ("iters", "<i4"), ("id", "<i8")])
+                ("flags", "<u4"), ("iters", "<i4"), ("id", "<i8"), ("disp", "<f4", 3), ("reserved", "<u4")])
 CFG = synth.Config(name="slab", dim=3, n=(48, 40, 150), count=(2, 2, 6), pitch=(24.0, 20.0, 25.0),
                    jitter=2.0, rbar=(5.0, 6.5), bg_wavelength=64.0, r0=7.0, n_samples=64,
                    max_iters=40, seed_window=3, gen_seed=77, philox_seed=991)
@@ -31,6 +31,7 @@ def _to_rec(cells):
     r = np.zeros(len(cells), REC)
     r["c"], r["R"], r["seed"] = cells["c"], cells["R"], cells["seed"]
     r["energy"], r["flags"], r["iters"], r["id"] = cells["E"], cells["flags"], cells["iters"], cells["id"]
+    r["disp"] = (cells["c"] - cells["seed"]).astype(np.float32)
     return r
 
 
@@ -100,8 +101,8 @@ def _worker(rank, world, port, q, k=0):
         # the halo exchange reproduced exactly the planes of the full volume
         local = D.exchange_halo(plan, own)
         assert np.array_equal(local.numpy(), raw[plan.buf[0]:plan.buf[1]])
-        q.put((rank, out["seeds"], out["cells"].numpy()[: out["n_live"] * 48].copy(),
-               out["dets"].numpy()[: out["n_dets"] * 48].copy(), out["labels"], out["id_base"]))
+        q.put((rank, out["seeds"], out["cells"].numpy()[: out["n_live"] * 64].copy(),
+               out["dets"].numpy()[: out["n_dets"] * 64].copy(), out["labels"], out["id_base"]))
     finally:
         tdist.destroy_process_group()
 

@@ -42,8 +42,8 @@ def _worker(rank, world, port, q, k=0):
         r = D.SlabRun(plan, be, torch.device("cuda", 0), cull_every=k, max_iters=CFG.max_iters).step(own)
         torch.cuda.synchronize()
         ns, nd, nl = r["n_seeds"], r["n_dets"], r["n_live"]
-        q.put((rank, {"seeds": r["seeds"][:ns].cpu().numpy(), "cells": r["cells"][:nl * 48].cpu().numpy(),
-                      "dets": r["dets"][:nd * 48].cpu().numpy(), "labels": r["labels"].cpu().numpy(),
+        q.put((rank, {"seeds": r["seeds"][:ns].cpu().numpy(), "cells": r["cells"][:nl * 64].cpu().numpy(),
+                      "dets": r["dets"][:nd * 64].cpu().numpy(), "labels": r["labels"].cpu().numpy(),
                       "id_base": r["id_base"], "n_total": r["n_total"]}))
     except Exception as e:  # surface the failure in the parent
         q.put((rank, repr(e)))
@@ -60,8 +60,8 @@ def single(gpu):
     P.upload(synth.generate(CFG))
     res = P.step()
     torch.cuda.synchronize()
-    return {"seeds": P.seeds[:res.n_seeds].cpu().numpy(), "cells": P.cells[:res.n_seeds * 48].cpu().numpy(),
-            "dets": P.dets[:res.n_dets * 48].cpu().numpy(), "labels": P.labels.cpu().numpy()}
+    return {"seeds": P.seeds[:res.n_seeds].cpu().numpy(), "cells": P.cells[:res.n_seeds * 64].cpu().numpy(),
+            "dets": P.dets[:res.n_dets * 64].cpu().numpy(), "labels": P.labels.cpu().numpy()}
 
 
 @pytest.mark.parametrize("world", [2, 3])
@@ -94,7 +94,7 @@ def single_periodic(gpu):
     P.upload(synth.generate(CFG))
     res = P.step()
     torch.cuda.synchronize()
-    return {"cells": P.cells_np(), "dets": P.dets[:res.n_dets * 48].cpu().numpy(),
+    return {"cells": P.cells_np(), "dets": P.dets[:res.n_dets * 64].cpu().numpy(),
             "labels": P.labels.cpu().numpy(), "n_seeds": res.n_seeds}
 
 

@@ -229,7 +229,7 @@ def test_full_size_sampled_parity(gpu, name):
     ids = rng.permutation(1 << 20)[:len(seeds)].astype(np.int64) + 12345
     # GPU: the bench's kernel configuration (auto: brick kernel), explicit seeds and ids
     p1 = pipeline.params_for(cfg)
-    cells = torch.empty(len(seeds) * 48, dtype=torch.uint8, device="cuda")
+    cells = torch.empty(len(seeds) * snk.CELL_BYTES, dtype=torch.uint8, device="cuda")
     snk.snk_evolve(P.grid, p1, P.smooth, _t(torch, seeds), _t(torch, ids), 0, len(seeds), cells, None)
     torch.cuda.synchronize()
     g = pipeline.as_cells(cells, len(seeds))
@@ -364,7 +364,7 @@ def test_evolve_slab_buffer_bit_identical(gpu):
     sel = np.nonzero(P.seeds_np()[:, 2] < 20)[0]
     z1 = 20 + int(np.ceil(2 * cfg.r0 + 2 * cfg.r0 + 2 + 2))
     g = snk.make_grid(3, (64, 64, 64), z_lo=0, nz_buf=z1, own=(0, 20))
-    cells = torch.empty(len(sel) * 48, dtype=torch.uint8, device="cuda")
+    cells = torch.empty(len(sel) * snk.CELL_BYTES, dtype=torch.uint8, device="cuda")
     snk.snk_evolve(g, p, P.smooth[:z1].contiguous(), P.seeds[sel].contiguous(),
                    _t(torch, sel.astype(np.int64)), 0, len(sel), cells, None)
     torch.cuda.synchronize()
@@ -430,7 +430,7 @@ def test_evolve_grid_2d_and_slab(gpu):
     sel = np.nonzero(P.seeds_np()[:, 2] < 20)[0]
     z1 = 20 + int(np.ceil(2 * cfg.r0 + 2 * cfg.r0 + 2 + 2))
     g = snk.make_grid(3, (64, 64, 64), z_lo=0, nz_buf=z1, own=(0, 20))
-    cells = torch.empty(len(sel) * 48, dtype=torch.uint8, device="cuda")
+    cells = torch.empty(len(sel) * snk.CELL_BYTES, dtype=torch.uint8, device="cuda")
     snk.snk_evolve(g, p, P.smooth[:z1].contiguous(), P.seeds[sel].contiguous(),
                    _t(torch, sel.astype(np.int64)), 0, len(sel), cells, None)
     torch.cuda.synchronize()
@@ -459,7 +459,7 @@ def test_evolve_estimator_variants(gpu, est, mode, W, N):
     sel = np.nonzero(P.seeds_np()[:, 2] < 20)[0]
     z1 = 20 + int(np.ceil(2 * cfg.r0 + 2 * cfg.r0 + 2 + 2))
     gs = snk.make_grid(3, (64, 64, 64), z_lo=0, nz_buf=z1, own=(0, 20))
-    cells = torch.empty(len(sel) * 48, dtype=torch.uint8, device="cuda")
+    cells = torch.empty(len(sel) * snk.CELL_BYTES, dtype=torch.uint8, device="cuda")
     snk.snk_evolve(gs, p, P.smooth[:z1].contiguous(), P.seeds[sel].contiguous(),
                    _t(torch, sel.astype(np.int64)), 0, len(sel), cells, None)
     torch.cuda.synchronize()
@@ -506,7 +506,7 @@ def test_evolve_range_resumes_bit_exactly(gpu):
         P.evolve()
         torch.cuda.synchronize()
         one = P.cells_np()
-        cells = torch.empty(n * 48, dtype=torch.uint8, device="cuda")
+        cells = torch.empty(n * snk.CELL_BYTES, dtype=torch.uint8, device="cuda")
         snk.snk_cells_init(p, P.seeds, None, 0, n, cells)
         for a, b in [(1, 1), (2, 40), (41, 90), (91, 91)]:
             snk.snk_evolve_range(P.grid, p, P.smooth, cells, n, a, b, None)
@@ -527,8 +527,8 @@ def test_periodic_culling_c1_vs_oracle(gpu):
     seeds = P.seeds_np()
     # stage by stage: GPU segments, oracle cull of the GPU records == GPU cull
     n = P.n_seeds
-    cur = torch.empty(n * 48, dtype=torch.uint8, device="cuda")
-    nxt = torch.empty(n * 48, dtype=torch.uint8, device="cuda")
+    cur = torch.empty(n * snk.CELL_BYTES, dtype=torch.uint8, device="cuda")
+    nxt = torch.empty(n * snk.CELL_BYTES, dtype=torch.uint8, device="cuda")
     snk.snk_cells_init(p, P.seeds, None, 0, n, cur)
     ocells = oracle.init_cells(op, seeds)
     live = n
@@ -671,9 +671,9 @@ def test_edge_cases(gpu):
     B = oracle.blur(d.cpu().numpy(), 3, 1.0)
     assert np.array_equal(sm.cpu().numpy(), B)
     assert np.array_equal(seeds[:n].cpu().numpy(), oracle.seeds_maxima(B, 3, 1, 0))
-    snk.snk_evolve(g, pp, sm, seeds, None, 0, 0, torch.empty(48, dtype=torch.uint8, device="cuda"), None)
-    assert snk.snk_cull(g, pp, torch.empty(48, dtype=torch.uint8, device="cuda"), 0,
-                        torch.empty(48, dtype=torch.uint8, device="cuda"), 1, ws) == 0
+    snk.snk_evolve(g, pp, sm, seeds, None, 0, 0, torch.empty(snk.CELL_BYTES, dtype=torch.uint8, device="cuda"), None)
+    assert snk.snk_cull(g, pp, torch.empty(snk.CELL_BYTES, dtype=torch.uint8, device="cuda"), 0,
+                        torch.empty(snk.CELL_BYTES, dtype=torch.uint8, device="cuda"), 1, ws) == 0
 
 
 # ---------------------------------------------------------------- anisotropic grids without resampling (§8(f) 4, G28)
@@ -727,7 +727,7 @@ def test_anisotropic_physical_pipeline_c3_crop(gpu):
     # z-slab buffer, physical z planes [0, 20) owned
     sel = np.nonzero(P.seeds_np()[:, 2] < 20.0)[0][:16]
     g = snk.make_grid(3, n, z_lo=0, nz_buf=40, own=(0, 20), scale=sc)
-    out = torch.empty(len(sel) * 48, dtype=torch.uint8, device="cuda")
+    out = torch.empty(len(sel) * snk.CELL_BYTES, dtype=torch.uint8, device="cuda")
     snk.snk_evolve(g, p, P.smooth[:40].contiguous(), P.seeds[sel].contiguous(),
                    _t(torch, sel.astype(np.int64)), 0, len(sel), out, None)
     torch.cuda.synchronize()
@@ -746,7 +746,7 @@ def test_anisotropic_lattice_and_config_errors(gpu):
     st, exp = oracle.seeds_lattice(n, 3, 10.0, scale=(1.0, 1.0, 2.0))
     assert cnt == len(exp) > 1 and np.array_equal(seeds[:cnt].cpu().numpy(), exp)
     vol = torch.zeros((32, 60, 64), dtype=torch.uint16, device="cuda")
-    cells = torch.empty(48 * 4, dtype=torch.uint8, device="cuda")
+    cells = torch.empty(snk.CELL_BYTES * 4, dtype=torch.uint8, device="cuda")
     with pytest.raises(snk.SNKError):   # grid estimator is isotropic only
         snk.snk_evolve(g, snk.make_params(10.0, estimator=snk.EST_GRID), vol, seeds, None, 0, 2, cells, None)
     with pytest.raises(snk.SNKError):   # N must be 1024 (4 warps x 8 samples)
@@ -809,7 +809,7 @@ def test_run_batch_equals_run(gpu):
     # slots alternate: volume 2 -> slot 0, volume 3 (= raws[1]) -> slot 1
     assert br.dets_np(0, nds[2]).tobytes() == exp[2][0] and np.array_equal(br.h_labels[0].numpy(), exp[2][1])
     assert br.dets_np(1, nds[3]).tobytes() == exp[1][0] and np.array_equal(br.h_labels[1].numpy(), exp[1][1])
-    assert nds[0] == len(exp[0][0]) // 48 and nds[1] == len(exp[1][0]) // 48
+    assert nds[0] == len(exp[0][0]) // snk.CELL_BYTES and nds[1] == len(exp[1][0]) // snk.CELL_BYTES
 
 
 def test_run_batch_resampled_and_periodic(gpu):
@@ -833,4 +833,4 @@ def test_run_batch_resampled_and_periodic(gpu):
     # the last two volumes are still in the two result slots
     assert br.dets_np(0, nds[2]).tobytes() == exp[2][0] and np.array_equal(br.h_labels[0].numpy(), exp[2][1])
     assert br.dets_np(1, nds[1]).tobytes() == exp[1][0] and np.array_equal(br.h_labels[1].numpy(), exp[1][1])
-    assert nds[0] * 48 == len(exp[0][0])
+    assert nds[0] * snk.CELL_BYTES == len(exp[0][0])
