@@ -114,9 +114,8 @@ def test_slabs_periodic_culling_match_single_gpu(single_periodic):
         pr.join(timeout=120)
     for r in range(world):
         assert not isinstance(out[r], str), out[r]
-    rec = np.dtype([("c", "<f4", 3), ("R", "<f4"), ("seed", "<f4", 3), ("energy", "<f4"),
-                    ("flags", "<u4"), ("iters", "<i4"), ("id", "<i8")])
-    got = np.concatenate([out[r]["cells"] for r in range(world)]).view(rec)
+    from paper_1804_06304_b200 import snk
+    got = np.concatenate([out[r]["cells"] for r in range(world)]).view(snk.CELL_DTYPE)
     exp = single_periodic["cells"]
     assert len(exp) < single_periodic["n_seeds"]
     assert got[np.argsort(got["id"])].tobytes() == exp[np.argsort(exp["id"])].tobytes()
