@@ -168,6 +168,30 @@ def oracle_crop_run(cfg, raw_full, target_cells: int, threads: int):
     return samples, dt, desc, len(seeds)
 
 
+CPU_CELLS_PER_CORE = 100   # the oracle sample: a centred crop with ~100 cells per host core
+
+
+def cpu_sample(cfg, threads: int, part=None):
+    """The oracle's bounded sample (both arms time exactly this): the centred crop
+    of the workload holding ~CPU_CELLS_PER_CORE cells per core, a2 -> a4 -> a5/a6
+    -> a7 on it.  Only the crop's planes are generated (outside the timing)."""
+    target = CPU_CELLS_PER_CORE * threads
+    lo, hi, _, _ = crop_geometry(cfg, target)
+    if part is None:
+        part = synth.generate(cfg, lo[2], hi[2] + 1)
+
+    def raw(lo_, hi_):
+        return part[lo_[2] - lo[2]:hi_[2] - lo[2] + 1, lo_[1]:hi_[1] + 1, lo_[0]:hi_[0] + 1]
+    return oracle_crop_run(cfg, raw, target_cells=target, threads=threads), part
+
+
+def cpu_baseline_entry(cfg):
+    threads = os.cpu_count() or 1
+    (s, dt, desc, nc), _ = cpu_sample(cfg, threads)
+    return {"value": s / dt, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": desc,
+            "seconds": round(dt, 2), "cells_per_s": nc / dt}
+
+
 # ---------------------------------------------------------------- our arm
 def run_ours(args):
     import torch
@@ -175,7 +199,10 @@ def run_ours(args):
     cfg = synth.CONFIGS[args.config]
     if args.n_samples:   # sweeps (e.g. the C5 N-sweep); the headline uses the config's N
         cfg = cfg.with_(n_samples=args.n_samples)
-    if world > 1:
+    if world > 1 or args.dist:
+        if "WORLD_SIZE" not in os.environ:   # --dist at N = 1 without a launcher
+            os.environ.update(RANK="0", LOCAL_RANK="0", WORLD_SIZE="1", MASTER_ADDR="127.0.0.1",
+                              MASTER_PORT=str(_free_port()))
         from paper_1804_06304_b200 import dist as D
         return D.bench_rank(args, cfg)
     torch.cuda.set_device(local_rank)
@@ -183,8 +210,8 @@ def run_ours(args):
     p = pipeline.params_for(cfg, image_term=snk.IMAGE_INTENSITY, cta_warps=args.cta_warps,
                             kernel_variant=args.kernel_variant, cull_every=args.cull_every,
                             estimator={"mc": snk.EST_MC, "cv": snk.EST_MC_CV, "ray": snk.EST_RAY}[args.estimator])
-    P = pipeline.Pipeline(cfg.dim, cfg.n, p, spacing=cfg.spacing, gradmag=not args.physical,
-                          physical=args.physical)
+    # the gradient magnitude (a3) only when the image term uses it
+    P = pipeline.Pipeline(cfg.dim, cfg.n, p, spacing=cfg.spacing, gradmag=False, physical=args.physical)
     h_raw = torch.empty((cfg.n[2], cfg.n[1], cfg.n[0]), dtype=torch.uint16, pin_memory=True)
     t = time.perf_counter()
     synth.generate_into_ptr(cfg, h_raw.data_ptr())
@@ -306,12 +333,8 @@ def run_ours(args):
                "d2h_bytes_per_step": int(nd * 64 + niso * 4),
                "cells_per_s": n_cells * args.steps / e2e_s, "inflight": k, "mode": args.e2e_mode}
     cpu = None
-    if not args.no_cpu_baseline:
-        threads = os.cpu_count() or 1
-        raw_np = h_raw.numpy()
-        s, dt, desc, nc = oracle_crop_run(cfg, raw_np, target_cells=250 * threads, threads=threads)
-        cpu = {"value": s / dt, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": desc,
-               "seconds": round(dt, 2), "cells_per_s": nc / dt}
+    if not args.no_cpu_baseline and cfg.dim == 3 and tuple(cfg.iso_n) == tuple(cfg.n):
+        cpu = cpu_baseline_entry(cfg)
     out = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
@@ -336,27 +359,52 @@ def run_reference(args):
         return None
     cfg = synth.CONFIGS[args.config]
     threads = os.cpu_count() or 1
-    # the bounded sample: a crop of the same workload (only its planes generated, outside the timing)
-    target = 60 * threads
-    lo, hi, _, _ = crop_geometry(cfg, target)
-    part = synth.generate(cfg, lo[2], hi[2] + 1)
-
-    def raw(lo_, hi_):
-        return part[lo_[2] - lo[2]:hi_[2] - lo[2] + 1, lo_[1]:hi_[1] + 1, lo_[0]:hi_[0] + 1]
+    # the bounded sample, identical to our arm's cpu_baseline (cpu_sample)
     samples = secs = 0.0
     desc = ""
+    part = None
     for k in range(args.warmup + args.steps):
-        s, dt, desc, _ = oracle_crop_run(cfg, raw, target_cells=target, threads=threads)
+        (s, dt, desc, _), part = cpu_sample(cfg, threads, part)
         if k >= args.warmup:
             samples += s
             secs += dt
     v = samples / secs
-    return {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world,
+    return {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": max(world, args.gpus),
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": secs / args.steps * 1e3,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "config": {"workload": workload_name(cfg)},
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": desc},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def _free_port() -> int:
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+def launch_ranks(n: int) -> int:
+    """`bench.py --gpus N` without a launcher: start N ranks (one process per
+    GPU) through torch.distributed.run on 127.0.0.1 and return their exit code;
+    rank 0 prints the JSON line."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+def launch_check(args):
+    """--launch-check: the rank plumbing alone (no kernels): every rank joins the
+    process group (gloo), the ranks are all-gathered; rank 0 reports the world."""
+    import torch
+    import torch.distributed as tdist
+    rank, _, world = dist_env()
+    tdist.init_process_group("gloo")
+    got = [None] * world
+    tdist.all_gather_object(got, rank)
+    tdist.destroy_process_group()
+    assert world == args.gpus and got == list(range(world)), (world, got)
+    return {"launch_check": True, "n_gpus": world, "ranks": got}
 
 
 def main():
@@ -381,10 +429,18 @@ def main():
                     help="end to end through snk_run_batch (copies overlapped inside the call) or snk_run threads")
     ap.add_argument("--e2e-priorities", type=int, default=1, help="threads mode: distinct stream priorities")
     ap.add_argument("--e2e-inflight", type=int, default=2, help="steps in flight in the end-to-end run")
+    ap.add_argument("--dist", action="store_true",
+                    help="run through the z-slab driver (dist.py) even at N = 1 (NCCL world of one)")
+    ap.add_argument("--launch-check", action="store_true", help="check the rank launch only (no kernels)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3   # contract: at least 3 warm-up steps
-    out = run_reference(args) if args.impl == "reference" else run_ours(args)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl == "ours":
+        sys.exit(launch_ranks(args.gpus))
+    if args.launch_check:
+        out = launch_check(args)
+    else:
+        out = run_reference(args) if args.impl == "reference" else run_ours(args)
     rank, _, _ = dist_env()
     if out is not None and rank == 0:
         print(json.dumps(out), flush=True)

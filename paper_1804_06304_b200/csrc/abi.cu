@@ -373,20 +373,22 @@ static int32_t run_compute(const RunLayout& L, int32_t dim, const int64_t n_raw[
   const uint16_t* d_img = d_grad ? d_grad : d_smooth;
   int64_t nd = 0;
   if (p->cull_every > 0 && p->cull_every < p->max_iters) {
-    // periodic culling (G25): segments, the a7 cull after each but the last
-    static thread_local int seg[1 << 12][2];
-    const int nseg = checkpoint_segments(p->max_iters, p->cull_every, seg, 1 << 12);
+    // periodic culling (G25): segments [1, k], [k+1, 2k], ... (checkpoints
+    // after iterations k, 2k, ... < T), the last one ending at T + 1; the a7
+    // cull after each but the last.  Bounds computed on the fly (any T, k).
     snk_cell* cur = d_cells;
     snk_cell* nxt = d_dets;
     int64_t live = ns;
     SNK_TRY(cells_init_impl(p, d_seeds, nullptr, first, ns, cur, st));
-    for (int k = 0; k < nseg; ++k) {
-      SNK_TRY(evolve_impl(&L.g, p, d_img, nullptr, nullptr, 0, live, cur, scratch, sb, st, seg[k][0],
-                          seg[k][1], true));
-      if (k + 1 < nseg) {
+    const int T = p->max_iters, kc = p->cull_every;
+    for (int a = 1; a <= T + 1;) {
+      const int e = (a + kc - 1 < T) ? a + kc - 1 : T + 1;
+      SNK_TRY(evolve_impl(&L.g, p, d_img, nullptr, nullptr, 0, live, cur, scratch, sb, st, a, e, true));
+      if (e <= T) {
         SNK_TRY(cull_impl(&L.g, p, cur, live, nxt, max_cells, &live, scratch, sb, st));
         std::swap(cur, nxt);
       }
+      a = e + 1;
     }
     SNK_TRY(cull_impl(&L.g, p, cur, live, nxt, max_cells, &nd, scratch, sb, st));
     if (nxt != d_dets)

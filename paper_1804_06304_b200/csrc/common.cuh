@@ -105,7 +105,6 @@ int32_t evolve_impl(const snk_grid* g, const snk_params* p, const uint16_t* d_im
 int32_t cells_init_impl(const snk_params* p, const float* d_seeds, const int64_t* d_ids,
                         int64_t id_base, int64_t n, snk_cell* d_cells, cudaStream_t st);
 // the periodic-culling segments of G25: ends k, 2k, ... (< T), then T + 1
-int checkpoint_segments(int T, int k, int (*seg)[2], int cap);
 int32_t compact_impl(const snk_params* p, const snk_cell* d_cells, int64_t n, snk_cell* d_out,
                      int64_t cap, int64_t* n_out, void* d_ws, size_t ws_bytes, cudaStream_t st);
 int32_t select_ids_impl(const snk_cell* d_cells, int64_t n, int64_t id_lo, int64_t id_hi,

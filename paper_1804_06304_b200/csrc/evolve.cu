@@ -1436,15 +1436,6 @@ int32_t cells_init_impl(const snk_params* p, const float* d_seeds, const int64_t
   return SNK_OK;
 }
 
-int checkpoint_segments(int T, int k, int (*seg)[2], int cap) {
-  int m = 0, a = 1;
-  if (k > 0 && k < T)
-    for (int e = k; e < T && m < cap - 1; e += k) { seg[m][0] = a; seg[m][1] = e; ++m; a = e + 1; }
-  seg[m][0] = a;
-  seg[m][1] = T + 1;
-  return m + 1;
-}
-
 int32_t evolve_stats(int64_t out[4], bool reset) {
   unsigned long long h[4];
   SNK_CUDA_CHECK(cudaMemcpyFromSymbol(h, g_evolve_stats, sizeof h));

@@ -182,11 +182,14 @@ class SlabRun:
         if ev is not None:
             ev[0].record()
         live = ns
+        cell_iters = ns * (self.T + 1)   # cell-iterations evolved by this rank (each N samples)
         if self.cull_every > 0:
             cells = self.be.init_cells(pl, seeds, ns, id_base)
             segs = checkpoints(self.T, self.cull_every)
+            cell_iters = 0
             for i, (a, b) in enumerate(segs):
                 cells = self.be.evolve_range(pl, smooth, cells, live, a, b)    # a5 segment
+                cell_iters += live * (b - a + 1)
                 if i + 1 < len(segs):                                           # checkpoint
                     cand, nc = self.be.compact(cells, live)
                     allc, ntot, _ = allgather_records(cand, nc, self.device, self.group)   # N6
@@ -201,6 +204,7 @@ class SlabRun:
         dets, nd = self.be.cull(pl, allc, ntot)                         # a7: overlap
         labels = self.be.label(pl, dets, nd)                            # a8
         return {"n_seeds": ns, "n_live": live, "id_base": id_base, "n_total": sum(counts), "cells": cells,
+                "cell_iters": cell_iters,
                 "seeds": seeds, "dets": dets, "n_dets": nd, "labels": labels, "smooth": smooth}
 
 
@@ -285,7 +289,12 @@ def bench_rank(args, cfg):
     torch.cuda.set_device(local_rank)
     # SNK_DIST_BACKEND=gloo: several ranks on one GPU (host-staged exchanges; tests only)
     backend = os.environ.get("SNK_DIST_BACKEND", "nccl")
+    want = int(getattr(args, "gpus", world) or world)
+    assert world == want, f"launched with WORLD_SIZE={world} but --gpus {want}"
     if backend == "nccl":
+        # keep NCCL's communicator set-up lines (rank, device, transport) in the log
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         tdist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     else:
         tdist.init_process_group(backend)
@@ -296,7 +305,7 @@ def bench_rank(args, cfg):
     z0, z1 = plan.own
     nown = (z1 - z0) * cfg.n[0] * cfg.n[1]
     max_cells = max(4096, (plan.nz_buf * cfg.n[0] * cfg.n[1]) // (2 * cfg.window + 1) ** 3 + 4096)
-    be = CudaBackend(plan, p, max_cells)
+    be = CudaBackend(plan, p, max_cells, gradmag=p.image_term == snk.IMAGE_GRADMAG)
     h_raw = torch.empty((z1 - z0, cfg.n[1], cfg.n[0]), dtype=torch.uint16, pin_memory=True)
     synth.generate_into_ptr(cfg, h_raw.data_ptr(), z0, z1)
     own = torch.empty(h_raw.shape, dtype=torch.uint16, device="cuda")
@@ -327,9 +336,12 @@ def bench_rank(args, cfg):
     total_ms, evolve_ms_max = float(ms[0].item()), float(ms[1].item())
     launches = snk.snk_launch_count() - l0
     n_total = r["n_total"]
-    samples = n_total * (cfg.max_iters + 1) * cfg.n_samples
+    # ray-samples evaluated (with periodic culling only the live cells' iterations), all ranks
+    ci = torch.tensor([r["cell_iters"]], dtype=torch.int64, device=red_dev)
+    tdist.all_reduce(ci, op=tdist.ReduceOp.SUM)
+    samples = int(ci.item()) * cfg.n_samples
     # this rank's evolve kernel against the per-GPU ALU peak; reported as the mean over ranks
-    my_samples = r["n_seeds"] * (cfg.max_iters + 1) * cfg.n_samples
+    my_samples = r["cell_iters"] * cfg.n_samples
     clocks = clk.summary()
     f_clk = (clocks["sm_max_mhz"] or 1965.0) * 1e6
     peak = SMS * LANES_PER_SM * f_clk / 1e9
@@ -352,6 +364,11 @@ def bench_rank(args, cfg):
     wall = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=red_dev)
     tdist.all_reduce(wall, op=tdist.ReduceOp.MAX)
     e2e_s = float(wall.item())
+    # the oracle's bounded sample on rank 0's host cores (after the timed regions)
+    cpu = None
+    if rank == 0 and not getattr(args, "no_cpu_baseline", False):
+        from bench import cpu_baseline_entry  # noqa: E402
+        cpu = cpu_baseline_entry(cfg)
     out = None
     if rank == 0:
         out = {"metric": "contour ray-samples/sec and cells segmented/sec at 1/2/4/8 B200; HBM/L2 GB/s",
@@ -362,6 +379,7 @@ def bench_rank(args, cfg):
                "config": {"workload": f"{cfg.name} z-slabs", "volume_iso": list(cfg.n), "cells": n_total,
                           "detections": r["n_dets"], "n_samples": cfg.n_samples, "iters": cfg.max_iters,
                           "parallelism": f"z-slab x{world}", "halo_planes": plan.halo,
+                          "cull_every": p.cull_every,
                           "l2": "inputs larger than L2", "backend": backend},
                "cells_per_s": n_total * args.steps / (total_ms / 1e3), "gpu_launches": int(launches),
                "phase_ms": {"evolve_max_over_ranks": evolve_ms_max},
@@ -370,7 +388,7 @@ def bench_rank(args, cfg):
                             "unit": "Glane-op/s", "frac": round(achieved / peak, 4), "traffic": None,
                             "kernel": "evolve_brick_kernel (slab)", "ops_per_sample": OPS_PER_SAMPLE,
                             "per": "GPU, mean over ranks"},
-               "cpu_baseline": None,
+               "cpu_baseline": cpu,
                "e2e": {"value": samples * args.steps / e2e_s, "unit": "ray-samples/s",
                        "h2d_bytes_per_step": int(nown * 2 * world),
                        "d2h_bytes_per_step": int(cfg.n[0] * cfg.n[1] * cfg.n[2] * 4 + r["n_dets"] * CELL_BYTES * world)}}

@@ -81,8 +81,18 @@ def test_validation_of_round_one_features(snk):
     assert snk.snk_validate(snk.make_grid(3, (60, 64, 32), scale=(0.0, 0.0, 0.0)), snk.make_params(10.0)) == snk.OK
     # the periodic-culling segments: the binding's list equals the driver's
     from paper_1804_06304_b200 import dist
-    for T, k in ((400, 50), (400, 0), (400, 400), (40, 15), (7, 3), (1, 1)):
-        assert snk.checkpoints(T, k) == dist.checkpoints(T, k)
+    def c_loop(T, k):   # transcription of snk_run's segment loop (abi.cu), computed on the fly
+        if not (0 < k < T):
+            return [(1, T + 1)]
+        out, a = [], 1
+        while a <= T + 1:
+            e = a + k - 1 if a + k - 1 < T else T + 1
+            out.append((a, e))
+            a = e + 1
+        return out
+
+    for T, k in ((400, 50), (400, 0), (400, 400), (40, 15), (7, 3), (1, 1), (5000, 1), (9000, 2)):
+        assert snk.checkpoints(T, k) == dist.checkpoints(T, k) == c_loop(T, k)
         segs = snk.checkpoints(T, k)
         assert segs[0][0] == 1 and segs[-1][1] == T + 1
         assert all(b + 1 == a for (_, b), (a, _) in zip(segs, segs[1:]))

@@ -122,3 +122,76 @@ def test_slabs_periodic_culling_match_single_gpu(single_periodic):
     for r in range(world):
         assert np.array_equal(out[r]["dets"], single_periodic["dets"])
     assert np.array_equal(np.concatenate([out[r]["labels"] for r in range(world)]), single_periodic["labels"])
+
+
+def _nccl_world1(q):
+    import torch
+    import torch.distributed as tdist
+    from paper_1804_06304_b200 import dist as D, pipeline, snk
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(_free_port()), NCCL_DEBUG="INFO",
+                      NCCL_DEBUG_SUBSYS="INIT")
+    torch.cuda.set_device(0)
+    tdist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        p = pipeline.params_for(CFG, image_term=snk.IMAGE_INTENSITY)
+        plan = D.plan_slabs(CFG.n, 1, 0, p)
+        own = torch.from_numpy(synth.generate(CFG)).cuda()
+        be = D.CudaBackend(plan, p, max_cells=4096, gradmag=False)
+        r = D.SlabRun(plan, be, torch.device("cuda", 0), max_iters=CFG.max_iters).step(own)
+        torch.cuda.synchronize()
+        ns, nd = r["n_seeds"], r["n_dets"]
+        q.put({"backend": tdist.get_backend(), "seeds": r["seeds"][:ns].cpu().numpy(),
+               "cells": r["cells"][:ns * 64].cpu().numpy(), "dets": r["dets"][:nd * 64].cpu().numpy(),
+               "labels": r["labels"].cpu().numpy()})
+    except Exception as e:
+        q.put(repr(e))
+        raise
+    finally:
+        tdist.destroy_process_group()
+
+
+def test_nccl_world_of_one_matches_single_gpu(single):
+    """The driver's NCCL branch (the N2 / N3 all_gathers through NCCL on device
+    buffers) on the one GPU of this box: bit-identical to the pipeline."""
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    pr = ctx.Process(target=_nccl_world1, args=(q,))
+    pr.start()
+    out = q.get(timeout=600)
+    pr.join(timeout=120)
+    assert not isinstance(out, str), out
+    assert out["backend"] == "nccl"
+    for k in ("seeds", "cells", "dets", "labels"):
+        assert np.array_equal(out[k], single[k]), k
+
+
+def _bench(args, env=None):
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    e = dict(os.environ)
+    e.update(env or {})
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), *args], capture_output=True, text=True,
+                       env=e, timeout=900, cwd=root)
+    assert r.returncode == 0, r.stderr[-3000:]
+    line = [ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1]
+    return json.loads(line), r.stdout + r.stderr
+
+
+def test_bench_launches_ranks_itself(gpu):
+    """`bench.py --gpus 2` without a launcher starts two ranks (torch.distributed.run);
+    here they share the box's one GPU (gloo, host-staged exchanges) and find the
+    same cells and detections as one GPU; `--dist` runs the driver's NCCL branch
+    at N = 1."""
+    common = ["--config", "C1", "--steps", "1", "--warmup", "3", "--no-cpu-baseline"]
+    one, _ = _bench(common + ["--no-e2e"])
+    two, _ = _bench(["--gpus", "2"] + common, {"SNK_DIST_BACKEND": "gloo"})
+    assert two["n_gpus"] == 2 and one["n_gpus"] == 1
+    assert two["config"]["cells"] == one["config"]["cells"]
+    assert two["config"]["detections"] == one["config"]["detections"]
+    nc, err = _bench(["--dist"] + common)
+    assert nc["n_gpus"] == 1 and nc["config"]["backend"] == "nccl"
+    assert nc["config"]["detections"] == one["config"]["detections"]
+    assert "NCCL INFO" in err
