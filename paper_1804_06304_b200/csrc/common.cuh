@@ -132,6 +132,12 @@ bool vec8_ok(const snk_grid* g, const void* a, const void* b, const void* c);
 int32_t sep_pass(int axis, int op, int h, const uint16_t* in, uint16_t* out, int nx, int ny, int nz,
                  int lo, int hi, cudaStream_t st);
 
+// a2 as one TMA-staged pass (stencil.cu): isotropic grids, radius 1..8, x extent
+// % 8 == 0, 16-byte aligned buffers; taps = the 2h + 1 Q14 taps
+bool blur_tma_ok(const snk_grid* g, int h, const void* in, const void* out);
+int32_t blur_tma(const snk_grid* g, int h, const int32_t* taps, const uint16_t* in, uint16_t* out,
+                 cudaStream_t st);
+
 // exclusive scan of n int counts into n + 1 int64 offsets (offsets[n] = total);
 // tmp: scan_ws(n) bytes of scratch (nullptr: single-block scan)
 size_t scan_ws(int64_t n);

@@ -11,6 +11,12 @@
 
 #include "common.cuh"
 
+// 1: the fused TMA-staged blur (stencil.cu) where it applies; 0: the three
+// streaming separable passes below (kept for comparison and the fallbacks)
+#ifndef SNK_BLUR_TMA
+#define SNK_BLUR_TMA 1
+#endif
+
 namespace snk {
 
 namespace {
@@ -656,6 +662,9 @@ int32_t preprocess_impl(const snk_grid* g, const snk_params* p, const uint16_t* 
     }
   } else if (h == 0) {
     SNK_CUDA_CHECK(cudaMemcpyAsync(d_smooth, d_in, nvox * sizeof(uint16_t), cudaMemcpyDeviceToDevice, st));
+  } else if (SNK_BLUR_TMA && blur_tma_ok(g, h, d_in, d_smooth)) {
+    // x, y and z in one TMA-staged pass (stencil.cu): 2 B read + 2 B written per voxel
+    SNK_TRY(blur_tma(g, h, taps.data(), d_in, d_smooth, st));
   } else if (h <= 8 && vec8_ok(g, d_in, d_smooth, tmp)) {
     // three (2D: two) streaming separable passes, 8 voxels per thread
     if (g->dim == 3) {

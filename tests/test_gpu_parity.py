@@ -53,7 +53,10 @@ def _assert_cells_close(g, o, ctx=""):
                                              (3, (7, 9, 8), 1.0), (3, (33, 17, 48), 0.5),
                                              (2, (1, 100, 256), 1.0), (2, (1, 31, 8), 2.0),
                                              # nz > 32: the column-streamed z pass, ragged last chunk
-                                             (3, (70, 9, 16), 1.0), (3, (41, 6, 24), 2.0), (3, (33, 7, 8), 0.5)])
+                                             (3, (70, 9, 16), 1.0), (3, (41, 6, 24), 2.0), (3, (33, 7, 8), 0.5),
+                                             # the TMA blur: several x / y tiles, z chunks of 64 + ragged
+                                             (3, (130, 70, 136), 1.0), (3, (67, 33, 64), 2.0),
+                                             (3, (3, 100, 200), 1.0), (2, (1, 97, 520), 1.0)])
 def test_blur_gradmag_bitexact(gpu, dim, shape, sigma):
     torch, snk, _ = gpu
     rng = np.random.default_rng(hash(shape) % 2 ** 32)
