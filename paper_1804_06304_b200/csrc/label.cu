@@ -2,8 +2,9 @@
 // reading G19).  Voxel x gets 1 + the index of the detection whose inner ball
 // (radius rho R, the nucleus at the Eq. 3 optimum) contains it with
 // the smallest normalised key d2/thr, ties to the smaller index; 0 if none.
-// Arithmetic is IEEE fp64 with explicit _rn intrinsics (no contraction), so the
-// map is bit-identical to the definition.
+// The decisions are those of IEEE fp64 with explicit _rn intrinsics (no
+// contraction): an fp32 filter with a proven margin settles membership, fp64
+// the rest, so the map is bit-identical to the definition.
 //
 // Mapping: detections are binned onto 32x8x8-voxel tiles (2D: 32x32) by the
 // bounding box of their inner ball; one CTA (256 threads) per tile stages the
@@ -29,6 +30,8 @@ struct TileGrid {
   double rho2;         // rho^2 (G19)
   double rho;          // bbox radius factor
   double sc[3];        // physical voxel size per axis (G28; 1 isotropic)
+  float scf[3];        // the same in fp32 (the fp32 filter)
+  double band;         // relative half-width of the fp32 filter's uncertain band
 };
 
 __device__ __forceinline__ bool tile_range(const snk_cell& d, const TileGrid& G, int lo[3], int hi[3]) {
@@ -74,89 +77,203 @@ __global__ void tile_fill_kernel(const snk_cell* __restrict__ dets, int64_t n, T
       }
 }
 
-// D = 3: tile 32x8x8, thread (x, y) walks 8 planes.  D = 2: tile 32x32x1, thread
-// handles 4 rows (y, y+8, y+16, y+24).
+// The exact O7 quantities of voxel (px, py, pz) against detection i (fp64, no
+// contraction, the oracle's order): d2 = (dx^2 + dy^2) + dz^2 and key = d2 / thr.
+__device__ __forceinline__ double exact_d2(double px, double py, double pz, const snk_cell& d) {
+  const double dx = __dsub_rn(px, (double)d.c[0]), dy = __dsub_rn(py, (double)d.c[1]);
+  const double dz = __dsub_rn(pz, (double)d.c[2]);
+  return __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
+}
+__device__ __forceinline__ double exact_thr(const snk_cell& d, double rho2) {
+  return __dmul_rn(__dmul_rn((double)d.R, (double)d.R), rho2);
+}
+
+// One tile's staged detection data (shared memory), filled from registers.
+struct Stage {
+  float c[3][kStage];
+  float lo[kStage], hi[kStage];
+  int idx[kStage];
+};
+
+// Registers of thread k's share of a tile list (k < count): loaded one tile
+// ahead, so the dependent loads (entries -> records) overlap the current tile.
+struct Prefetch {
+  int cnt;
+  int i;
+  float c[3], lo, hi;
+};
+
+__device__ __forceinline__ void prefetch_tile(Prefetch& f, const snk_cell* __restrict__ dets, const TileGrid& G,
+                                              const int64_t* __restrict__ offsets, const int* __restrict__ entries,
+                                              int64_t tile) {
+  const int64_t e0 = offsets[tile], e1 = offsets[tile + 1];
+  f.cnt = (int)(e1 - e0);
+  if ((int)threadIdx.x < min(f.cnt, kStage)) {
+    f.i = entries[e0 + threadIdx.x];
+    const snk_cell d = dets[f.i];
+    f.c[0] = d.c[0];
+    f.c[1] = d.c[1];
+    f.c[2] = d.c[2];
+    const double thr = exact_thr(d, G.rho2);
+    f.lo = (float)__dmul_rn(thr, 1.0 - G.band);
+    f.hi = (float)__dmul_rn(thr, 1.0 + G.band);
+  }
+}
+
+// D = 3: tile 32x8x8, thread (x, y) walks 8 planes; a CTA takes kZT tiles
+// along z (the next tile's list is prefetched into registers while the current
+// one is evaluated).  D = 2: tile 32x32x1, thread handles 4 rows (y, y+8,
+// y+16, y+24).
+//
+// Membership d2 <= thr is decided in fp32 outside a relative band of 1e-5
+// (anisotropic grids: 1e-3) around thr: d2f (fp32, FFMA) is within 1e-6
+// (relative) of the exact d2 and thr_lo / thr_hi bracket thr by the band, so
+// d2f > thr_hi implies d2 > thr and d2f < thr_lo implies d2 < thr; only pairs
+// inside the band take the exact fp64 test.  The key d2 / thr (fp64 division) is evaluated only when a
+// voxel lies inside two or more inner balls — a lone candidate wins whatever
+// its key — so the map equals the all-fp64 definition bit for bit.  The common
+// case (every candidate plane certain and first) is a branch-free select.
+constexpr int kZT = 4;
+
 template <int D>
 __global__ void __launch_bounds__(kThreads) label_kernel(const snk_cell* __restrict__ dets, TileGrid G,
                                                          const int64_t* __restrict__ offsets,
                                                          const int* __restrict__ entries,
                                                          int32_t* __restrict__ labels) {
   constexpr int NV = D == 3 ? kTZ3 : kTY2 / kTY;   // voxels per thread
-  __shared__ double s_c[3][kStage];
-  __shared__ double s_thr[kStage];
-  __shared__ int s_idx[kStage];
-  const int64_t tile = blockIdx.x;
-  const int tx = (int)(tile % G.nt[0]), ty = (int)((tile / G.nt[0]) % G.nt[1]),
-            tz = (int)(tile / ((int64_t)G.nt[0] * G.nt[1]));
+  __shared__ Stage S[2];
+  const int ntz = D == 3 ? G.nt[2] : 1;
+  const int zgroups = D == 3 ? (ntz + kZT - 1) / kZT : 1;
+  const int64_t col = blockIdx.x / zgroups;        // (tx, ty)
+  const int tz0 = D == 3 ? (int)(blockIdx.x % zgroups) * kZT : 0;
+  const int tz1 = D == 3 ? min(tz0 + kZT, ntz) : 1;
+  const int tx = (int)(col % G.nt[0]), ty = (int)(col / G.nt[0]);
   const int lx = threadIdx.x % kTX, ly = threadIdx.x / kTX;
   const int x = tx * G.tx + lx;
-  int yv[NV], zv[NV];
-#pragma unroll
-  for (int k = 0; k < NV; ++k) {
-    yv[k] = D == 3 ? ty * G.ty + ly : ty * G.ty + ly + k * kTY;
-    zv[k] = D == 3 ? G.z0 + tz * G.tz + k : G.z0;
-  }
-  int best[NV];
-  double best_key[NV];
-#pragma unroll
-  for (int k = 0; k < NV; ++k) { best[k] = -1; best_key[k] = 0.0; }
   const double px = __dmul_rn((double)x, G.sc[0]);   // physical voxel position (G28; exact for scale 1)
-  const int64_t e0 = offsets[tile], e1 = offsets[tile + 1];
-  for (int64_t s = e0; s < e1; s += kStage) {
-    const int cnt = (int)(e1 - s < kStage ? e1 - s : kStage);
-    __syncthreads();
-    for (int k = threadIdx.x; k < cnt; k += blockDim.x) {
-      const int i = entries[s + k];
-      const snk_cell d = dets[i];
-      s_c[0][k] = (double)d.c[0];
-      s_c[1][k] = (double)d.c[1];
-      s_c[2][k] = (double)d.c[2];
-      s_thr[k] = __dmul_rn(__dmul_rn((double)d.R, (double)d.R), G.rho2);
-      s_idx[k] = i;
+  const float pxf = __fmul_rn((float)x, G.scf[0]);
+  auto tile_id = [&](int tz) { return ((int64_t)tz * G.nt[1] + ty) * G.nt[0] + tx; };
+  Prefetch f;
+  prefetch_tile(f, dets, G, offsets, entries, tile_id(tz0));
+  for (int tz = tz0; tz < tz1; ++tz) {
+    Stage& st = S[tz & 1];
+    const int cnt = f.cnt;
+    if ((int)threadIdx.x < min(cnt, kStage)) {
+      st.c[0][threadIdx.x] = f.c[0];
+      st.c[1][threadIdx.x] = f.c[1];
+      st.c[2][threadIdx.x] = f.c[2];
+      st.lo[threadIdx.x] = f.lo;
+      st.hi[threadIdx.x] = f.hi;
+      st.idx[threadIdx.x] = f.i;
     }
-    __syncthreads();
-    for (int k = 0; k < cnt; ++k) {
-      const double thr = s_thr[k];
-      const int i = s_idx[k];
-      const double dx = __dsub_rn(px, s_c[0][k]);
-      const double dx2 = __dmul_rn(dx, dx);
-      if (D == 3) {
-        const double dy = __dsub_rn(__dmul_rn((double)yv[0], G.sc[1]), s_c[1][k]);
-        const double dxy = __dadd_rn(dx2, __dmul_rn(dy, dy));   // d2 = (dx^2 + dy^2) + dz^2
-        if (!(dxy <= thr)) continue;                             // dz^2 >= 0: no plane can qualify
+    __syncthreads();   // stage complete (the other stage was last read before this barrier's predecessor)
+    if (tz + 1 < tz1) prefetch_tile(f, dets, G, offsets, entries, tile_id(tz + 1));
+    int yv[NV], zv[NV];
+    float pyf[NV], pzf[NV];   // the filter's positions (fp32; its margin covers their rounding)
 #pragma unroll
-        for (int v = 0; v < NV; ++v) {
-          const double dz = __dsub_rn(__dmul_rn((double)zv[v], G.sc[2]), s_c[2][k]);
-          const double d2 = __dadd_rn(dxy, __dmul_rn(dz, dz));
-          if (d2 <= thr) {
-            const double key = __ddiv_rn(d2, thr);
-            if (best[v] < 0 || key < best_key[v] || (key == best_key[v] && i < best[v])) {
-              best[v] = i;
-              best_key[v] = key;
-            }
+    for (int k = 0; k < NV; ++k) {
+      yv[k] = D == 3 ? ty * G.ty + ly : ty * G.ty + ly + k * kTY;
+      zv[k] = D == 3 ? G.z0 + tz * G.tz + k : G.z0;
+      pyf[k] = __fmul_rn((float)yv[k], G.scf[1]);
+      pzf[k] = __fmul_rn((float)zv[k], G.scf[2]);
+    }
+    int best[NV];
+    double best_key[NV];   // valid once a second candidate made it necessary (best_kv)
+    bool best_kv[NV];
+#pragma unroll
+    for (int k = 0; k < NV; ++k) { best[k] = -1; best_key[k] = 0.0; best_kv[k] = false; }
+    auto slow = [&](int v, int i, float d2f, float lo) {
+      // the exact O7 rules for plane v (rare: near a boundary, or a second ball)
+      const double py = __dmul_rn((double)yv[v], G.sc[1]);
+      const double pz = D == 3 ? __dmul_rn((double)zv[v], G.sc[2]) : 0.0;
+      if (!(d2f < lo)) {
+        const snk_cell d = dets[i];
+        if (!(exact_d2(px, py, pz, d) <= exact_thr(d, G.rho2))) return;
+      }
+      if (best[v] < 0) {
+        best[v] = i;
+        return;
+      }
+      if (!best_kv[v]) {
+        const snk_cell b = dets[best[v]];
+        best_key[v] = __ddiv_rn(exact_d2(px, py, pz, b), exact_thr(b, G.rho2));
+        best_kv[v] = true;
+      }
+      const snk_cell d = dets[i];
+      const double key = __ddiv_rn(exact_d2(px, py, pz, d), exact_thr(d, G.rho2));
+      if (key < best_key[v] || (key == best_key[v] && i < best[v])) {
+        best[v] = i;
+        best_key[v] = key;
+      }
+    };
+    for (int s0 = 0; s0 < cnt; s0 += kStage) {
+      // lists longer than one stage (never on the throughput configs): re-stage synchronously
+      const Stage* sp = &st;
+      if (s0 > 0) {
+        __syncthreads();
+        const int64_t e0 = offsets[tile_id(tz)] + s0;
+        const int m = cnt - s0 < kStage ? cnt - s0 : kStage;
+        Stage& o = S[(tz + 1) & 1];   // free: its next use is the next tile (after a barrier)
+        if ((int)threadIdx.x < m) {
+          const int i = entries[e0 + threadIdx.x];
+          const snk_cell d = dets[i];
+          const double thr = exact_thr(d, G.rho2);
+          o.c[0][threadIdx.x] = d.c[0];
+          o.c[1][threadIdx.x] = d.c[1];
+          o.c[2][threadIdx.x] = d.c[2];
+          o.lo[threadIdx.x] = (float)__dmul_rn(thr, 1.0 - G.band);
+          o.hi[threadIdx.x] = (float)__dmul_rn(thr, 1.0 + G.band);
+          o.idx[threadIdx.x] = i;
+        }
+        __syncthreads();
+        sp = &o;
+      }
+      const int m = cnt - s0 < kStage ? cnt - s0 : kStage;
+      for (int k = 0; k < m; ++k) {
+        const float hi = sp->hi[k], lo = sp->lo[k];
+        const float dxf = __fsub_rn(pxf, sp->c[0][k]);
+        float d2f[NV];
+        if (D == 3) {
+          const float dyf = __fsub_rn(pyf[0], sp->c[1][k]);
+          const float dxy = __fmaf_rn(dxf, dxf, __fmul_rn(dyf, dyf));
+          if (dxy > hi) continue;   // dz^2 >= 0: no plane of this column can qualify
+#pragma unroll
+          for (int v = 0; v < NV; ++v) {
+            const float dzf = __fsub_rn(pzf[v], sp->c[2][k]);
+            d2f[v] = __fmaf_rn(dzf, dzf, dxy);
+          }
+        } else {
+#pragma unroll
+          for (int v = 0; v < NV; ++v) {
+            const float dyf = __fsub_rn(pyf[v], sp->c[1][k]);
+            d2f[v] = __fmaf_rn(dxf, dxf, __fmul_rn(dyf, dyf));
           }
         }
-      } else {
+        const int i = sp->idx[k];
+        // bitwise (not short-circuit) so the test compiles to predicates, not branches
+        unsigned need = 0u;
 #pragma unroll
-        for (int v = 0; v < NV; ++v) {
-          const double dy = __dsub_rn(__dmul_rn((double)yv[v], G.sc[1]), s_c[1][k]);
-          const double d2 = __dadd_rn(dx2, __dmul_rn(dy, dy));
-          if (d2 <= thr) {
-            const double key = __ddiv_rn(d2, thr);
-            if (best[v] < 0 || key < best_key[v] || (key == best_key[v] && i < best[v])) {
-              best[v] = i;
-              best_key[v] = key;
-            }
-          }
+        for (int v = 0; v < NV; ++v)
+          need |= (unsigned)(d2f[v] <= hi) & ((unsigned)(best[v] >= 0) | (unsigned)(d2f[v] >= lo));
+        if (!need) {
+#pragma unroll
+          for (int v = 0; v < NV; ++v) best[v] = d2f[v] < lo ? i : best[v];   // certain and first
+        } else {
+#pragma unroll
+          for (int v = 0; v < NV; ++v)
+            if (d2f[v] <= hi) slow(v, i, d2f[v], lo);
         }
       }
     }
-  }
-  if (x >= G.nx) return;
+    if (cnt > kStage) __syncthreads();   // the re-staged buffer is the next tile's stage
+    if (x < G.nx) {
+      int32_t* dst = labels + ((int64_t)(zv[0] - G.z0) * G.ny + yv[0]) * G.nx + x;
+      const int64_t step = D == 3 ? (int64_t)G.ny * G.nx : (int64_t)kTY * G.nx;
 #pragma unroll
-  for (int v = 0; v < NV; ++v)
-    if (yv[v] < G.ny && zv[v] < G.z1)
-      labels[((int64_t)(zv[v] - G.z0) * G.ny + yv[v]) * G.nx + x] = best[v] + 1;
+      for (int v = 0; v < NV; ++v)
+        if (yv[v] < G.ny && zv[v] < G.z1) dst[v * step] = best[v] + 1;
+    }
+  }
 }
 
 TileGrid make_grid(const snk_grid* g) {
@@ -172,7 +289,13 @@ TileGrid make_grid(const snk_grid* g) {
   G.nt[2] = (int)ceil_div(std::max(G.z1 - G.z0, 0), G.tz);
   G.rho2 = g->dim == 3 ? kRhoSq3 : kRhoSq2;
   G.rho = rho_of(g->dim);
-  for (int a = 0; a < 3; ++a) G.sc[a] = grid_scale(g, a);
+  for (int a = 0; a < 3; ++a) {
+    G.sc[a] = grid_scale(g, a);
+    G.scf[a] = (float)G.sc[a];
+  }
+  // isotropic: fp32 positions are exact integers and d2f is within 1e-6 of d2;
+  // physical positions x * scale round in fp32 (1e-4 voxel at x ~ 1000)
+  G.band = grid_aniso(g) ? 1e-3 : 1e-5;
   return G;
 }
 
@@ -221,8 +344,10 @@ int32_t label_impl(const snk_grid* g, const snk_params* p, const snk_cell* d_det
     tile_fill_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(d_dets, n, G, offsets, cursor, entries);
     SNK_LAUNCH_CHECK("tile_fill_kernel");
   }
-  if (g->dim == 3) label_kernel<3><<<(unsigned)ntiles, kThreads, 0, st>>>(d_dets, G, offsets, entries, d_labels);
-  else label_kernel<2><<<(unsigned)ntiles, kThreads, 0, st>>>(d_dets, G, offsets, entries, d_labels);
+  // 3D: one CTA per column of kZT tiles along z
+  const int64_t nblk = g->dim == 3 ? (int64_t)G.nt[0] * G.nt[1] * ceil_div(G.nt[2], kZT) : ntiles;
+  if (g->dim == 3) label_kernel<3><<<(unsigned)nblk, kThreads, 0, st>>>(d_dets, G, offsets, entries, d_labels);
+  else label_kernel<2><<<(unsigned)nblk, kThreads, 0, st>>>(d_dets, G, offsets, entries, d_labels);
   SNK_LAUNCH_CHECK("label_kernel");
   return SNK_OK;
 }
