@@ -293,8 +293,10 @@ def bench_rank(args, cfg):
     assert world == want, f"launched with WORLD_SIZE={world} but --gpus {want}"
     if backend == "nccl":
         # keep NCCL's communicator set-up lines (rank, device, transport) in the log
-        os.environ.setdefault("NCCL_DEBUG", "INFO")
-        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        # (images may preset NCCL_DEBUG=VERSION / WARN, which hides them)
+        if os.environ.get("NCCL_DEBUG", "").upper() in ("", "VERSION", "WARN"):
+            os.environ["NCCL_DEBUG"] = "INFO"
+            os.environ["NCCL_DEBUG_SUBSYS"] = "INIT"
         tdist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     else:
         tdist.init_process_group(backend)
