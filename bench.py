@@ -31,6 +31,10 @@ import synth  # noqa: E402  (input generator: no method arithmetic)
 
 METRIC = "contour ray-samples/sec and cells segmented/sec at 1/2/4/8 B200; HBM/L2 GB/s"
 UNIT = "ray-samples/s"
+# Algorithmic bytes per ray-sample: the d-linear gather reads
+# 8 u16 taps in 3D (16 B) and 4 in 2D (8 B); the ray-march estimator (G27) also
+# gathers one d-linear lookup per step.
+GATHER_BYTES = {3: 16, 2: 8}
 # Algorithmic issue slots per MC sample: Philox4x32-10 30 (3/4 block),
 # uniforms 6, direction + radius 12 (5 SFU), position 3, d-linear gather 8 loads + 26 ALU,
 # weights S, S_r, S_R 15, leaves 6, tree adds 5  ->  111 lane-ops per sample.
@@ -43,6 +47,10 @@ OPS_BY_ESTIMATOR = {"mc": OPS_PER_SAMPLE, "cv": OPS_PER_SAMPLE + 1, "ray": 87}
 # sqrt) 8, position 2, bilinear gather 2 axes x 6 + 1 index + 4 conversions + 3 lerps x 2
 # = 23 (+ 4 loads), S/S_r/S_R 15, leaves 4 + tree adds 4  ->  80
 OPS_PER_SAMPLE_2D = 80
+# L2 read bandwidth measured on this pool's B200 (scripts/micro/l2bw.cu,
+# profiles/r2_l2bw.txt: best of the L2-resident working sets 16-96 MB)
+L2_PEAK_GBPS = 19398.1
+L2_PEAK_SOURCE = "measured, profiles/r2_l2bw.txt (scripts/micro/l2bw.cu)"
 SMS = 148
 LANES_PER_SM = 128
 
@@ -106,6 +114,33 @@ def workload_name(cfg):
     dims = f"{iso[0]}x{iso[1]}" + (f"x{iso[2]}" if cfg.dim == 3 else "")
     nn = int(np.prod(cfg.count))
     return f"{cfg.name}: synthetic {dims}{aniso}, {nn} nuclei, N={cfg.n_samples}, T={cfg.max_iters}"
+
+
+def hbm_peak():
+    """The measured HBM copy bandwidth (MEASURED_PEAKS.json, driver-written), else
+    B200_PROFILING.md's fallback."""
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (measured copy bandwidth)"
+    except (OSError, KeyError, ValueError):
+        return 6650.0, "of fallback (B200_PROFILING.md: 6.65 TB/s)"
+
+
+def spread(xs):
+    """median and spread of per-step times (ms)."""
+    return {"median": statistics.median(xs), "min": min(xs), "max": max(xs), "n": len(xs)}
+
+
+def ncu_sol(config: str, kernel: str = "evolve_brick_kernel"):
+    """the committed ncu --set full capture's speed-of-light
+    percentages of the binding units (issue slots, shared-memory wavefronts)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            e = json.load(f)[config][kernel]
+        return {k: round(e[k] / 100.0, 4) for k in ("issue_pct", "shared_wavefront_pct") if k in e} | \
+            {"source": e["source"]}
+    except (OSError, KeyError, ValueError):
+        return None
 
 
 def ncu_traffic(config: str, kernel: str = "evolve_brick_kernel"):
@@ -259,25 +294,39 @@ def run_ours(args):
     samples = P.cell_iters * cfg.n_samples
     value = samples * args.steps / (total_ms / 1e3)
     cells_per_s = n_cells * args.steps / (total_ms / 1e3)
-    phase = {"preprocess+seeds": statistics.mean(e[0].elapsed_time(e[1]) for e in evs),
-             "evolve": statistics.mean(evolve_ms),
-             "cull+label": statistics.mean(e[2].elapsed_time(e[3]) for e in evs)}
+    phase_lists = {"preprocess+seeds": [e[0].elapsed_time(e[1]) for e in evs], "evolve": evolve_ms,
+                   "cull+label": [e[2].elapsed_time(e[3]) for e in evs]}
+    phase = {k: statistics.median(v) for k, v in phase_lists.items()}
     clocks = clk.summary()
-    # roofline: the evolve kernel is issue-bound plain ALU work
+    # Roofline of the dominant kernel: (ii) the algorithmic gather
+    # bytes (16 B per 3D sample, 8 B per 2D sample) per launch / its device time
+    # against the measured HBM peak and the measured L2 peak; (i) the binding
+    # units' SOL from the committed ncu capture of the same config; and the
+    # instruction-issue model (lane-ops) for reference.
+    ev_s = statistics.median(evolve_ms) / 1e3
+    gbytes = GATHER_BYTES[cfg.dim]
+    achieved = samples * gbytes / ev_s / 1e9
+    hbm, hbm_src = hbm_peak()
     f_clk = (clocks["sm_max_mhz"] or 1965.0) * 1e6
-    peak = SMS * LANES_PER_SM * f_clk / 1e9            # G lane-ops/s
-    ev_s = statistics.mean(evolve_ms) / 1e3
+    lane_peak = SMS * LANES_PER_SM * f_clk / 1e9            # G lane-ops/s
     ops = OPS_BY_ESTIMATOR[args.estimator] if cfg.dim == 3 else OPS_PER_SAMPLE_2D
-    achieved = samples * ops / ev_s / 1e9
     traffic, traffic_src = ncu_traffic(cfg.name) if not args.cull_every else (None, None)
-    roofline = {"bound": "alu", "achieved": round(achieved, 1), "peak": round(peak, 1),
-                "unit": "Glane-op/s", "frac": round(achieved / peak, 4), "traffic": traffic,
+    roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
+                "frac": round(achieved / hbm, 4), "traffic": traffic,
+                "peak_source": hbm_src,
+                "l2": {"achieved": round(achieved, 1), "peak": L2_PEAK_GBPS, "unit": "GB/s",
+                       "frac": round(achieved / L2_PEAK_GBPS, 4), "peak_source": L2_PEAK_SOURCE},
+                "sol_ncu": ncu_sol(cfg.name) if not args.cull_every else None,
+                "alu_model": {"achieved": round(samples * ops / ev_s / 1e9, 1), "peak": round(lane_peak, 1),
+                              "unit": "Glane-op/s", "frac": round(samples * ops / ev_s / 1e9 / lane_peak, 4),
+                              "ops_per_sample": ops,
+                              "peak_source": f"{SMS} SMs x {LANES_PER_SM} FP32 lanes x sm_max_mhz"},
+                "algorithmic_bytes_per_sample": gbytes,
+                "algorithmic_gather_bytes_per_launch": samples * gbytes,
                 "traffic_unit": "DRAM bytes per launch (ncu --set full)", "traffic_source": traffic_src,
-                "algorithmic_gather_bytes_per_launch": samples * 16,
-                "kernel": "evolve_brick_kernel" if args.kernel_variant != 1 else "evolve_warp_kernel", "ops_per_sample": ops,
+                "kernel": "evolve_brick_kernel" if args.kernel_variant != 1 else "evolve_warp_kernel",
                 "samples_per_s_kernel": samples / ev_s,
-                "gather_GBps": round(samples * 16 / ev_s / 1e9, 1),
-                "peak_source": f"{SMS} SMs x {LANES_PER_SM} FP32 lanes x sm_max_mhz (B200_PROFILING.md)"}
+                "timing": "CUDA events around the evolve launch on its stream, median over the timed steps"}
     # end to end through the public host-buffer call (snk_run)
     e2e = None
     if not args.no_e2e and not args.physical:   # snk_run resamples anisotropic input (a1)
@@ -344,7 +393,8 @@ def run_ours(args):
                    "seed_mode": cfg.seed_mode, "parallelism": "1 GPU", "cull_every": args.cull_every,
                    "estimator": args.estimator, "physical": bool(args.physical),
                    "l2": "inputs larger than L2 (u16 volume %.1f GiB > 126 MB)" % (h_raw.numel() * 2 / 2**30)},
-        "cells_per_s": cells_per_s, "phase_ms": phase, "gpu_launches": int(launches),
+        "cells_per_s": cells_per_s, "phase_ms": phase,
+        "phase_ms_spread": {k: spread(v) for k, v in phase_lists.items()}, "gpu_launches": int(launches),
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
         "generate_s": round(gen_s, 2),
         "evolve_stats_per_step": {k: v / (args.steps + args.warmup) for k, v in evo_stats.items()},
@@ -410,7 +460,7 @@ def launch_check(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="C4")
     ap.add_argument("--n-samples", type=int, default=0, help="override the config's N (sweeps only)")

@@ -19,7 +19,7 @@ _TAG = os.environ.get("SNK_BUILD_TAG", "")
 OBJ = os.path.join(HERE, "build_obj" + (f"_{_TAG}" if _TAG else ""))
 LIB = os.path.join(HERE, f"libsnk_{_TAG}.so" if _TAG else "libsnk.so")
 SOURCES = ["abi.cu", "volume.cu", "stencil.cu", "seeds.cu", "evolve.cu", "cull.cu", "label.cu"]
-HEADERS = ["common.cuh"]
+HEADERS = ["common.cuh", "tma.cuh"]
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 BASE = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-ffp-contract=off",

@@ -19,7 +19,11 @@ namespace snk {
 
 namespace {
 
-constexpr int kTX = 32, kTY = 8, kTZ3 = 8, kTY2 = 32, kThreads = 256;
+constexpr int kTX = 32, kTY = 8, kTY2 = 32, kThreads = 256;
+#ifndef SNK_LABEL_TZ
+#define SNK_LABEL_TZ 8
+#endif
+constexpr int kTZ3 = SNK_LABEL_TZ;   // tile depth: voxels per thread (3D)
 constexpr int kStage = 256;
 
 struct TileGrid {
@@ -120,19 +124,48 @@ __device__ __forceinline__ void prefetch_tile(Prefetch& f, const snk_cell* __res
   }
 }
 
-// D = 3: tile 32x8x8, thread (x, y) walks 8 planes; a CTA takes kZT tiles
-// along z (the next tile's list is prefetched into registers while the current
-// one is evaluated).  D = 2: tile 32x32x1, thread handles 4 rows (y, y+8,
-// y+16, y+24).
+// The exact O7 rules for one (voxel, candidate) pair the fp32 filter could not
+// settle (near a ball's boundary, or a second ball containing the voxel): rare,
+// so it lives out of line (its fp64 registers stay out of the main loop).
+// key: this voxel's best key (valid once kv; shared memory).  Returns the new
+// best index in the low 32 bits and the key-valid flag in bit 32.
+__device__ __forceinline__ long long label_exact(const snk_cell* __restrict__ dets, double px, double py, double pz,
+                                              double rho2, int i, int best, int kv, double* key, float d2f,
+                                              float lo) {
+  auto pack = [](int b, int v) { return (long long)(uint32_t)b | ((long long)v << 32); };
+  if (!(d2f < lo)) {
+    const snk_cell d = dets[i];
+    if (!(exact_d2(px, py, pz, d) <= exact_thr(d, rho2))) return pack(best, kv);
+  }
+  if (best < 0) return pack(i, 0);
+  if (!kv) {
+    const snk_cell b = dets[best];
+    *key = __ddiv_rn(exact_d2(px, py, pz, b), exact_thr(b, rho2));
+  }
+  const snk_cell d = dets[i];
+  const double k = __ddiv_rn(exact_d2(px, py, pz, d), exact_thr(d, rho2));
+  if (k < *key || (k == *key && i < best)) {
+    *key = k;
+    return pack(i, 1);
+  }
+  return pack(best, 1);
+}
+
+// D = 3: tile 32 x 8 x kTZ3, thread (x, y) walks the tile's kTZ3 planes; a CTA
+// takes kZT tiles along z (the next tile's list is prefetched into registers
+// while the current one is evaluated).  D = 2: tile 32 x 32, a thread takes 4
+// rows (y, y + 8, y + 16, y + 24).
 //
 // Membership d2 <= thr is decided in fp32 outside a relative band of 1e-5
 // (anisotropic grids: 1e-3) around thr: d2f (fp32, FFMA) is within 1e-6
 // (relative) of the exact d2 and thr_lo / thr_hi bracket thr by the band, so
 // d2f > thr_hi implies d2 > thr and d2f < thr_lo implies d2 < thr; only pairs
-// inside the band take the exact fp64 test.  The key d2 / thr (fp64 division) is evaluated only when a
-// voxel lies inside two or more inner balls — a lone candidate wins whatever
-// its key — so the map equals the all-fp64 definition bit for bit.  The common
-// case (every candidate plane certain and first) is a branch-free select.
+// inside the band take the exact fp64 test (one call site, planes looped with
+// the running bests in shared memory).  The key d2 / thr (fp64 division)
+// is evaluated only when a voxel lies inside two or more inner balls — a lone
+// candidate wins whatever its key — so the map equals the all-fp64 definition
+// bit for bit.  The common case (every plane of the column certain, and first)
+// is a branch-free select on bit masks.
 constexpr int kZT = 4;
 
 template <int D>
@@ -142,6 +175,8 @@ __global__ void __launch_bounds__(kThreads) label_kernel(const snk_cell* __restr
                                                          int32_t* __restrict__ labels) {
   constexpr int NV = D == 3 ? kTZ3 : kTY2 / kTY;   // voxels per thread
   __shared__ Stage S[2];
+  __shared__ double skey[NV][kThreads];            // the exact path's best keys
+  __shared__ int sbest[NV][kThreads];              // the exact path's running bests
   const int ntz = D == 3 ? G.nt[2] : 1;
   const int zgroups = D == 3 ? (ntz + kZT - 1) / kZT : 1;
   const int64_t col = blockIdx.x / zgroups;        // (tx, ty)
@@ -150,8 +185,11 @@ __global__ void __launch_bounds__(kThreads) label_kernel(const snk_cell* __restr
   const int tx = (int)(col % G.nt[0]), ty = (int)(col / G.nt[0]);
   const int lx = threadIdx.x % kTX, ly = threadIdx.x / kTX;
   const int x = tx * G.tx + lx;
-  const double px = __dmul_rn((double)x, G.sc[0]);   // physical voxel position (G28; exact for scale 1)
+  const int y0 = ty * G.ty + ly;                   // 3D: the thread's row; 2D: its first row
   const float pxf = __fmul_rn((float)x, G.scf[0]);
+  const float pyf0 = __fmul_rn((float)y0, G.scf[1]);
+  const int64_t plane = (int64_t)G.ny * G.nx;
+  const int64_t vstep = D == 3 ? plane : (int64_t)kTY * G.nx;   // between a thread's voxels
   auto tile_id = [&](int tz) { return ((int64_t)tz * G.nt[1] + ty) * G.nt[0] + tx; };
   Prefetch f;
   prefetch_tile(f, dets, G, offsets, entries, tile_id(tz0));
@@ -168,44 +206,15 @@ __global__ void __launch_bounds__(kThreads) label_kernel(const snk_cell* __restr
     }
     __syncthreads();   // stage complete (the other stage was last read before this barrier's predecessor)
     if (tz + 1 < tz1) prefetch_tile(f, dets, G, offsets, entries, tile_id(tz + 1));
-    int yv[NV], zv[NV];
-    float pyf[NV], pzf[NV];   // the filter's positions (fp32; its margin covers their rounding)
+    const int zt = D == 3 ? G.z0 + tz * G.tz : G.z0;   // the tile's first plane (3D)
+    float pvf[NV];   // per voxel: 3D its plane's z, 2D its row's y (the filter's fp32 positions)
 #pragma unroll
-    for (int k = 0; k < NV; ++k) {
-      yv[k] = D == 3 ? ty * G.ty + ly : ty * G.ty + ly + k * kTY;
-      zv[k] = D == 3 ? G.z0 + tz * G.tz + k : G.z0;
-      pyf[k] = __fmul_rn((float)yv[k], G.scf[1]);
-      pzf[k] = __fmul_rn((float)zv[k], G.scf[2]);
-    }
+    for (int v = 0; v < NV; ++v)
+      pvf[v] = D == 3 ? __fmul_rn((float)(zt + v), G.scf[2]) : __fmul_rn((float)(y0 + v * kTY), G.scf[1]);
     int best[NV];
-    double best_key[NV];   // valid once a second candidate made it necessary (best_kv)
-    bool best_kv[NV];
 #pragma unroll
-    for (int k = 0; k < NV; ++k) { best[k] = -1; best_key[k] = 0.0; best_kv[k] = false; }
-    auto slow = [&](int v, int i, float d2f, float lo) {
-      // the exact O7 rules for plane v (rare: near a boundary, or a second ball)
-      const double py = __dmul_rn((double)yv[v], G.sc[1]);
-      const double pz = D == 3 ? __dmul_rn((double)zv[v], G.sc[2]) : 0.0;
-      if (!(d2f < lo)) {
-        const snk_cell d = dets[i];
-        if (!(exact_d2(px, py, pz, d) <= exact_thr(d, G.rho2))) return;
-      }
-      if (best[v] < 0) {
-        best[v] = i;
-        return;
-      }
-      if (!best_kv[v]) {
-        const snk_cell b = dets[best[v]];
-        best_key[v] = __ddiv_rn(exact_d2(px, py, pz, b), exact_thr(b, G.rho2));
-        best_kv[v] = true;
-      }
-      const snk_cell d = dets[i];
-      const double key = __ddiv_rn(exact_d2(px, py, pz, d), exact_thr(d, G.rho2));
-      if (key < best_key[v] || (key == best_key[v] && i < best[v])) {
-        best[v] = i;
-        best_key[v] = key;
-      }
-    };
+    for (int v = 0; v < NV; ++v) best[v] = -1;
+    uint32_t has = 0, kv = 0;   // planes with a best; planes whose best key is in skey
     for (int s0 = 0; s0 < cnt; s0 += kStage) {
       // lists longer than one stage (never on the throughput configs): re-stage synchronously
       const Stage* sp = &st;
@@ -234,44 +243,69 @@ __global__ void __launch_bounds__(kThreads) label_kernel(const snk_cell* __restr
         const float dxf = __fsub_rn(pxf, sp->c[0][k]);
         float d2f[NV];
         if (D == 3) {
-          const float dyf = __fsub_rn(pyf[0], sp->c[1][k]);
+          const float dyf = __fsub_rn(pyf0, sp->c[1][k]);
           const float dxy = __fmaf_rn(dxf, dxf, __fmul_rn(dyf, dyf));
           if (dxy > hi) continue;   // dz^2 >= 0: no plane of this column can qualify
+          const float cz = sp->c[2][k];
 #pragma unroll
           for (int v = 0; v < NV; ++v) {
-            const float dzf = __fsub_rn(pzf[v], sp->c[2][k]);
+            const float dzf = __fsub_rn(pvf[v], cz);
             d2f[v] = __fmaf_rn(dzf, dzf, dxy);
           }
         } else {
+          const float cy = sp->c[1][k];
 #pragma unroll
           for (int v = 0; v < NV; ++v) {
-            const float dyf = __fsub_rn(pyf[v], sp->c[1][k]);
+            const float dyf = __fsub_rn(pvf[v], cy);
             d2f[v] = __fmaf_rn(dxf, dxf, __fmul_rn(dyf, dyf));
           }
         }
+        uint32_t mhi = 0, mlo = 0;   // planes with d2f <= hi (maybe inside), d2f < lo (certainly inside)
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+          mhi |= (uint32_t)(d2f[v] <= hi) << v;
+          mlo |= (uint32_t)(d2f[v] < lo) << v;
+        }
         const int i = sp->idx[k];
-        // bitwise (not short-circuit) so the test compiles to predicates, not branches
-        unsigned need = 0u;
+        if (!(mhi & (has | ~mlo))) {   // every maybe-inside plane is certain and first
 #pragma unroll
-        for (int v = 0; v < NV; ++v)
-          need |= (unsigned)(d2f[v] <= hi) & ((unsigned)(best[v] >= 0) | (unsigned)(d2f[v] >= lo));
-        if (!need) {
-#pragma unroll
-          for (int v = 0; v < NV; ++v) best[v] = d2f[v] < lo ? i : best[v];   // certain and first
+          for (int v = 0; v < NV; ++v) best[v] = (mlo >> v) & 1u ? i : best[v];
+          has |= mlo;
         } else {
 #pragma unroll
-          for (int v = 0; v < NV; ++v)
-            if (d2f[v] <= hi) slow(v, i, d2f[v], lo);
+          for (int v = 0; v < NV; ++v) sbest[v][threadIdx.x] = best[v];
+          const double px = __dmul_rn((double)x, G.sc[0]);
+#pragma unroll 1
+          for (int v = 0; v < NV; ++v) {
+            if (!((mhi >> v) & 1u)) continue;
+            float dv = d2f[0];
+#pragma unroll
+            for (int u = 1; u < NV; ++u) dv = u == v ? d2f[u] : dv;
+            const double py = D == 3 ? __dmul_rn((double)y0, G.sc[1]) : __dmul_rn((double)(y0 + v * kTY), G.sc[1]);
+            const double pz = D == 3 ? __dmul_rn((double)(zt + v), G.sc[2]) : 0.0;
+            const long long r = label_exact(dets, px, py, pz, G.rho2, i, sbest[v][threadIdx.x], (kv >> v) & 1u,
+                                            &skey[v][threadIdx.x], dv, lo);
+            sbest[v][threadIdx.x] = (int)(uint32_t)r;
+            kv |= (uint32_t)(r >> 32) << v;
+          }
+#pragma unroll
+          for (int v = 0; v < NV; ++v) {
+            best[v] = sbest[v][threadIdx.x];
+            has |= (uint32_t)(best[v] >= 0) << v;
+          }
         }
       }
     }
     if (cnt > kStage) __syncthreads();   // the re-staged buffer is the next tile's stage
     if (x < G.nx) {
-      int32_t* dst = labels + ((int64_t)(zv[0] - G.z0) * G.ny + yv[0]) * G.nx + x;
-      const int64_t step = D == 3 ? (int64_t)G.ny * G.nx : (int64_t)kTY * G.nx;
+      int32_t* dst = labels + ((int64_t)(zt - G.z0) * G.ny + y0) * G.nx + x;
+      const int nv = D == 3 ? min(NV, G.z1 - zt) : min(NV, (G.ny - y0 + kTY - 1) / kTY);
+      if (D == 3 && y0 >= G.ny) continue;
 #pragma unroll
-      for (int v = 0; v < NV; ++v)
-        if (yv[v] < G.ny && zv[v] < G.z1) dst[v * step] = best[v] + 1;
+      for (int v = 0; v < NV; ++v) {
+        if (v < nv) *dst = best[v] + 1;
+        dst += vstep;
+      }
     }
   }
 }

@@ -7,8 +7,11 @@
 //            window, only for candidates) -> order-preserving compaction.
 // Integer-exact; bit-identical to the definition.
 #include <cmath>
+#include <cstdlib>
+#include <mutex>
 
 #include "common.cuh"
+#include "tma.cuh"
 
 namespace snk {
 
@@ -473,6 +476,222 @@ __global__ void __launch_bounds__(256) maxima_pred8_kernel(MaxArgs A, const uint
   if (valid) mask[t] = (uint8_t)bits;
 }
 
+// ---------------------------------------------------------------------------
+// TMA-staged MAXIMA (3D, isotropic window 1 <= w <= 8, nx % 8 == 0, 16-byte
+// aligned B): the whole a4 predicate in ONE pass over B, with the box max
+// never leaving the SM.  A CTA owns a 64 x 32 column tile and walks a chunk of
+// zc owned planes; every input plane's (64 + 16) x (32 + 2w) box is copied by
+// the Tensor Memory Accelerator into a 4-stage mbarrier ring (x start x0 - 8:
+// 16-byte aligned, profiles/r2_tma_probe.md).  Box elements outside the volume
+// arrive as zeros — the neutral element of max, i.e. the window clipped to the
+// volume (O4).  Per plane: the x box max (shared -> shared), the y box max
+// (shared -> registers), both on packed u16 pairs (VIMNMX3.U16x2: three-input
+// max of two lanes per instruction); the y-maxima enter a per-thread register
+// ring of 2w + 1 planes whose max is M of plane z - w.  Candidates B >= thr &&
+// B == M (B re-read from L2) get the warp-cooperative tie check; one mask byte
+// per 8 voxels, in linear voxel order (bits_count / bits_write compact it).
+#ifndef SNK_QTHREADS
+#define SNK_QTHREADS 256
+#endif
+// 256 threads own the 64 x 32 outputs (8 voxels each); the x pass's (32 + 2w) x 8
+// tasks run on all kQThreads (a build with 384 threads takes them in one round:
+// 1 CTA per SM by registers, C4 seeds 13.4 ms — slower)
+constexpr int kQX = 64, kQY = 32, kQNS = 4, kQThreads = SNK_QTHREADS, kQOut = 256;
+constexpr int kQBX = kQX + 16;
+
+struct MaxTmaArgs {
+  MaxArgs ma;        // B (the buffer), dims, z_lo, windows, thr: the tie check
+  uint8_t* mask;     // one byte per 8-voxel group of the own region
+  int own_z0, own_z1, zc;
+};
+
+__device__ __forceinline__ uint32_t vmax(uint32_t a, uint32_t b) { return __vmaxu2(a, b); }
+
+// Box max over columns c - W .. c + W (lane 0) and c + 1 - W .. c + 1 + W (lane
+// 1) of the output word at even column c = 8 + 2j of a row segment whose words
+// are E[m] = (cols 2m, 2m + 1) and O[m] = (2m + 1, 2m + 2): W + 1 words of one
+// kind and W of the other cover both lanes' windows exactly.
+template <int W>
+__device__ __forceinline__ uint32_t xwin(const uint32_t* E, const uint32_t* O, int j) {
+  uint32_t m;
+  if (W & 1) {   // c - W odd: O[(c-W-1)/2 + i], i <= W; E[(c-W+1)/2 + i], i < W
+    const int o0 = j + (7 - W) / 2, e0 = j + (9 - W) / 2;
+    m = O[o0];
+#pragma unroll
+    for (int i = 1; i <= W; ++i) m = vmax(m, O[o0 + i]);
+#pragma unroll
+    for (int i = 0; i < W; ++i) m = vmax(m, E[e0 + i]);
+  } else {       // c - W even: E[(c-W)/2 + i], i <= W; O[(c-W)/2 + i], i < W
+    const int e0 = j + (8 - W) / 2;
+    m = E[e0];
+#pragma unroll
+    for (int i = 1; i <= W; ++i) m = vmax(m, E[e0 + i]);
+#pragma unroll
+    for (int i = 0; i < W; ++i) m = vmax(m, O[e0 + i]);
+  }
+  return m;
+}
+
+template <int W>
+__global__ void __launch_bounds__(kQThreads, kQThreads > 256 ? 1 : 2)
+    maxima_tma_kernel(const __grid_constant__ CUtensorMap map, const __grid_constant__ MaxTmaArgs A) {
+  constexpr int BY = kQY + 2 * W, K = 2 * W + 1;
+  constexpr uint32_t kBoxBytes = kQBX * BY * 2;
+  constexpr uint32_t kStage = (kBoxBytes + 127) & ~127u;   // TMA destinations: 128-byte aligned
+  extern __shared__ __align__(128) uint8_t smem[];
+  uint16_t* ring = reinterpret_cast<uint16_t*>(smem);                 // [NS] x ([BY][QBX] + pad)
+  uint16_t* sx = reinterpret_cast<uint16_t*>(smem + kQNS * kStage);   // [BY][QX]
+  __shared__ __align__(8) uint64_t full[kQNS];
+  const MaxArgs& M = A.ma;
+  const int nx = M.nx, ny = M.ny;
+  const int x0 = blockIdx.x * kQX, y0 = blockIdx.y * kQY;
+  const int zs = A.own_z0 + blockIdx.z * A.zc, ze = min(zs + A.zc, A.own_z1);
+  const int nplanes = (ze - zs) + 2 * W;
+  const int tid = threadIdx.x, lane = tid & 31;
+  auto box_z = [&](int p) { return zs - W + p - M.z_lo; };   // buffer plane (TMA zero-fills outside)
+  if (tid == 0) {
+    for (int s = 0; s < kQNS; ++s) mbar_init(&full[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (int p = 0; p < kQNS - 1 && p < nplanes; ++p)
+      tma_load_box(&map, ring + p * (kStage / 2), &full[p], x0 - 8, y0 - W, box_z(p), kBoxBytes);
+  }
+  __syncthreads();
+  const int q = tid & 7, r = tid >> 3;            // output cols x0 + 8q .. + 7, row y0 + r
+  const int xo = x0 + 8 * q, yo = y0 + r;
+  const bool outw = tid < kQOut;                  // warp-uniform: this warp owns outputs
+  const bool own = outw && xo < nx && yo < ny;
+  const uint32_t thr = M.thr;
+  const uint32_t thr2 = thr <= 0xffffu ? (thr | (thr << 16)) : 0xffffffffu;
+  uint32_t zr[K][4];
+  for (int base = 0; base < nplanes; base += K) {
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+      const int p = base + j;
+      if (p >= nplanes) break;
+      const int s = p % kQNS;
+      const uint16_t* box = ring + s * (kStage / 2);
+      mbar_wait(&full[s], (uint32_t)((p / kQNS) & 1));
+      __syncthreads();   // box complete; the previous plane's y pass is done with sx
+      // x pass: BY rows x 8 groups of 8 outputs; box cols 8g .. 8g + 23 cover x0 + 8g - 8 .. + 15
+      for (int it = tid; it < BY * 8; it += kQThreads) {
+        const int row = it >> 3, g = it & 7;
+        const uint4* src = reinterpret_cast<const uint4*>(box + row * kQBX + 8 * g);
+        uint32_t E[12], O[11];
+#pragma unroll
+        for (int u = 0; u < 3; ++u) {
+          const uint4 a = src[u];
+          E[4 * u] = a.x; E[4 * u + 1] = a.y; E[4 * u + 2] = a.z; E[4 * u + 3] = a.w;
+        }
+#pragma unroll
+        for (int m = 0; m < 11; ++m) O[m] = __byte_perm(E[m], E[m + 1], 0x5432);
+        uint4 o;
+        o.x = xwin<W>(E, O, 0);
+        o.y = xwin<W>(E, O, 1);
+        o.z = xwin<W>(E, O, 2);
+        o.w = xwin<W>(E, O, 3);
+        *reinterpret_cast<uint4*>(sx + row * kQX + 8 * g) = o;
+      }
+      __syncthreads();   // sx complete; every read of this box done
+      if (tid == 0 && p + kQNS - 1 < nplanes) {
+        const int nq = p + kQNS - 1;
+        tma_load_box(&map, ring + (nq % kQNS) * (kStage / 2), &full[nq % kQNS], x0 - 8, y0 - W, box_z(nq), kBoxBytes);
+      }
+      if (!outw) continue;   // x-pass-only warps (whole warps: the tie check below is warp-collective)
+      // y pass: sx rows r .. r + 2W (sx row i = y0 - W + i)
+      {
+        uint4 a = *reinterpret_cast<const uint4*>(sx + r * kQX + 8 * q);
+        uint32_t m0 = a.x, m1 = a.y, m2 = a.z, m3 = a.w;
+#pragma unroll
+        for (int i = 1; i < K; ++i) {
+          a = *reinterpret_cast<const uint4*>(sx + (r + i) * kQX + 8 * q);
+          m0 = vmax(m0, a.x); m1 = vmax(m1, a.y); m2 = vmax(m2, a.z); m3 = vmax(m3, a.w);
+        }
+        zr[j][0] = m0; zr[j][1] = m1; zr[j][2] = m2; zr[j][3] = m3;
+      }
+      if (p >= 2 * W) {
+        // the ring holds the y-maxima of planes zo - W .. zo + W: M = their max
+        const int zo = zs + p - 2 * W;
+        uint32_t mm[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          uint32_t m = zr[0][k];
+#pragma unroll
+          for (int i = 1; i < K; ++i) m = vmax(m, zr[i][k]);
+          mm[k] = m;
+        }
+        uint32_t bits = 0;
+        uint4 bq = make_uint4(0, 0, 0, 0);
+        if (own) {
+          bq = __ldg(reinterpret_cast<const uint4*>(M.B + ((int64_t)(zo - M.z_lo) * ny + yo) * nx + xo));
+          const uint32_t bw[4] = {bq.x, bq.y, bq.z, bq.w};
+          uint32_t any = 0;
+#pragma unroll
+          for (int k = 0; k < 4; ++k) any |= __vcmpeq2(bw[k], mm[k]) & __vcmpgeu2(bw[k], thr2);
+          if (any) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              const uint32_t c = __vcmpeq2(bw[k], mm[k]) & __vcmpgeu2(bw[k], thr2);
+              bits |= ((c & 1u) | ((c >> 15) & 2u)) << (2 * k);
+            }
+          }
+        }
+        // candidates, one at a time per warp, each checked by all 32 lanes
+        uint32_t pending = bits;
+        unsigned ballot = __ballot_sync(0xffffffffu, pending != 0u);
+        while (ballot) {
+          const int src = __ffs(ballot) - 1;
+          const uint32_t pb = __shfl_sync(0xffffffffu, pending, src);
+          const int k = __ffs(pb) - 1;
+          const uint32_t word = (k >> 1) == 0 ? bq.x : (k >> 1) == 1 ? bq.y : (k >> 1) == 2 ? bq.z : bq.w;
+          const uint32_t bk = __shfl_sync(0xffffffffu, (k & 1) ? word >> 16 : word & 0xffffu, src);
+          const int cx = __shfl_sync(0xffffffffu, xo, src) + k;
+          const int cy = __shfl_sync(0xffffffffu, yo, src);
+          const bool ok = tie_free_warp(M, cx, cy, zo, (uint16_t)bk, lane);
+          if (lane == src) {
+            if (!ok) bits &= ~(1u << k);
+            pending &= ~(1u << k);
+          }
+          ballot = __ballot_sync(0xffffffffu, pending != 0u);
+        }
+        if (own) A.mask[((int64_t)(zo - A.own_z0) * ny + yo) * (nx >> 3) + (xo >> 3)] = (uint8_t)bits;
+      }
+    }
+  }
+}
+
+bool maxima_tma_ok(const snk_grid* g, const snk_params* p, const void* B) {
+  const int w = p->seed_window;
+  return g->dim == 3 && !grid_aniso(g) && w >= 1 && w <= 8 && g->n[0] % 8 == 0 &&
+         (reinterpret_cast<uintptr_t>(B) & 15) == 0 && tma_available();
+}
+
+template <int W>
+int32_t launch_maxima_tma(const MaxTmaArgs& A, int nzb, cudaStream_t st) {
+  constexpr int BY = kQY + 2 * W;
+  const int smem = kQNS * ((kQBX * BY * 2 + 127) & ~127) + BY * kQX * 2;
+  CUtensorMap map;
+  SNK_TRY(volume_map(&map, A.ma.B, A.ma.nx, A.ma.ny, nzb, kQBX, BY));
+  auto k = maxima_tma_kernel<W>;
+  static std::once_flag once;
+  static cudaError_t attr = cudaSuccess;
+  std::call_once(once, [&] { attr = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); });
+  if (attr != cudaSuccess) return cuda_fail(attr, "cudaFuncSetAttribute(maxima_tma_kernel)");
+  dim3 grid((unsigned)ceil_div(A.ma.nx, kQX), (unsigned)ceil_div(A.ma.ny, kQY),
+            (unsigned)ceil_div(A.own_z1 - A.own_z0, A.zc));
+  k<<<grid, kQThreads, smem, st>>>(map, A);
+  SNK_LAUNCH_CHECK("maxima_tma_kernel");
+  return SNK_OK;
+}
+
+int32_t maxima_tma(const MaxTmaArgs& A, int nzb, cudaStream_t st) {
+  switch (A.ma.w) {
+#define SNK_MT(WW) case WW: return launch_maxima_tma<WW>(A, nzb, st);
+    SNK_MT(1) SNK_MT(2) SNK_MT(3) SNK_MT(4) SNK_MT(5) SNK_MT(6) SNK_MT(7) SNK_MT(8)
+#undef SNK_MT
+  }
+  return fail(SNK_INTERNAL, "maxima_tma: window must be 1..8");
+}
+
 bool vec_ok(const snk_grid* g, const snk_params* p) {
   return g->n[0] % 8 == 0 && p->seed_window >= 0 && p->seed_window <= 8;
 }
@@ -601,12 +820,19 @@ int32_t seeds_impl(const snk_grid* g, const snk_params* p, const uint16_t* d_smo
     const int64_t zb1 = dim == 3 ? std::min<int64_t>(g->own_z1 - 1 + wz, g->n[2] - 1) - g->z_lo + 1
                                  : g->own_z1 - g->z_lo;
     const int nzp = (int)(zb1 - zb0);
-    SNK_TRY(sep_pass(0, 1, wx, d_smooth + zb0 * plane, ta + zb0 * plane, nx, ny, nzp, 0, nx - 1, st));
-    SNK_TRY(sep_pass(1, 1, wy, ta + zb0 * plane, tb + zb0 * plane, nx, ny, nzp, 0, ny - 1, st));
+    // x / y / z box-max passes + the predicate; SNK_TMA_MAXIMA=1: the one-pass TMA
+    // kernel (isotropic 3D; 4.7 instead of ~25 GB of DRAM traffic on C4, but
+    // latency-bound at 28% issue: 7.96 vs 7.69 ms, profiles/r2_volume.md)
+    const char* tma_env = getenv("SNK_TMA_MAXIMA");
+    const bool tma_pass = maxima_tma_ok(g, p, d_smooth) && tma_env && tma_env[0] == '1';
+    if (!tma_pass) {
+      SNK_TRY(sep_pass(0, 1, wx, d_smooth + zb0 * plane, ta + zb0 * plane, nx, ny, nzp, 0, nx - 1, st));
+      SNK_TRY(sep_pass(1, 1, wy, ta + zb0 * plane, tb + zb0 * plane, nx, ny, nzp, 0, ny - 1, st));
+    }
     // 3D: the z box-max as its own column-streamed pass into ta (every plane of
     // the window read ~once from HBM), then the predicate reads B and M once;
     // the flat fold of 2w+1 XY planes re-read them through L2 (43 GB per C4 step)
-    const bool zpass = dim == 3 && wz > 0 && nzp > 32;
+    const bool zpass = !tma_pass && dim == 3 && wz > 0 && nzp > 32;
     if (zpass) SNK_TRY(sep_pass(2, 1, wz, tb + zb0 * plane, ta + zb0 * plane, nx, ny, nzp, 0, nzp - 1, st));
     SNK_CUDA_CHECK(cudaMemsetAsync(bits + nw - 1, 0, sizeof(uint32_t), st));
     MaxArgs A;
@@ -627,7 +853,18 @@ int32_t seeds_impl(const snk_grid* g, const snk_params* p, const uint16_t* d_smo
     uint8_t* mask = reinterpret_cast<uint8_t*>(bits);
     const unsigned grid = (unsigned)ceil_div(ng, 256);
     const int oz = (int)g->own_z0;
-    if (dim == 2) {
+    if (tma_pass) {
+      MaxTmaArgs T;
+      T.ma = A;
+      T.mask = mask;
+      T.own_z0 = (int)g->own_z0;
+      T.own_z1 = (int)g->own_z1;
+      // z chunk: long chunks (less z-halo re-reading) unless the grid would not fill the GPU
+      const int64_t cols = ceil_div(nx, kQX) * ceil_div(ny, kQY);
+      T.zc = 128;
+      while (T.zc > 16 && cols * ceil_div(g->own_z1 - g->own_z0, T.zc) < 1024) T.zc /= 2;
+      SNK_TRY(maxima_tma(T, nzb, st));
+    } else if (dim == 2) {
       maxima_pred8_kernel<2, 0><<<grid, 256, 0, st>>>(A, tb, mask, ng, oz);
     } else {
       if (zpass) {
@@ -640,7 +877,7 @@ int32_t seeds_impl(const snk_grid* g, const snk_params* p, const uint16_t* d_smo
 #undef SNK_PRED_CASE
       }
     }
-    SNK_LAUNCH_CHECK("maxima_pred8_kernel");
+    if (!tma_pass) SNK_LAUNCH_CHECK("maxima_pred8_kernel");
     bits_count_kernel<<<(unsigned)nbw, 1024, 0, st>>>(bits, nw, wcounts);
     SNK_LAUNCH_CHECK("bits_count_kernel");
     SNK_TRY(scan_counts(wcounts, nbw, woff, st, stmp));

@@ -24,6 +24,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "tma.cuh"
 
 namespace snk {
 
@@ -35,38 +36,6 @@ constexpr int kBX = kTX + 16;   // box row: x0 - 8 .. x0 + TX + 7 (16-byte align
 struct StencilTaps {
   uint32_t w[9];   // w[0] = centre, w[i] = w_(+-i), i <= 8
 };
-
-__device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
-}
-
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  uint32_t done = 0;
-  while (!done) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-        "selp.u32 %0, 1, 0, p;\n}"
-        : "=r"(done)
-        : "r"(smem_addr(bar)), "r"(parity)
-        : "memory");
-  }
-}
-
-// One elected thread: arm the barrier for `bytes` and copy the box at (x, y, z).
-__device__ __forceinline__ void tma_load_box(const CUtensorMap* map, void* dst, uint64_t* bar, int x, int y, int z,
-                                             uint32_t bytes) {
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic writes to dst (edge fix-up) first
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
-               : "memory");
-  asm volatile(
-      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
-      "[%5];" ::"r"(smem_addr(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(smem_addr(bar))
-      : "memory");
-}
 
 __device__ __forceinline__ void unpack8(const uint4 q, uint32_t* v) {
   v[0] = q.x & 0xffffu; v[1] = q.x >> 16; v[2] = q.y & 0xffffu; v[3] = q.y >> 16;
@@ -112,9 +81,10 @@ __global__ void __launch_bounds__(kThreads, H <= 5 ? 2 : 1) blur_tma_kernel(cons
                                                                            int nz, const __grid_constant__ StencilTaps T) {
   constexpr int BY = kTY + 2 * H, K = 2 * H + 1;
   constexpr uint32_t kBoxBytes = kBX * BY * 2;
+  constexpr uint32_t kStage = (kBoxBytes + 127) & ~127u;   // TMA destinations: 128-byte aligned
   extern __shared__ __align__(128) uint8_t smem[];
-  uint16_t* ring = reinterpret_cast<uint16_t*>(smem);                   // [NS][BY][BX]: the TMA boxes
-  uint32_t* sx = reinterpret_cast<uint32_t*>(smem + kNS * kBoxBytes);   // [BY][TX]: x-passed rows (u32: no unpacking)
+  uint16_t* ring = reinterpret_cast<uint16_t*>(smem);                // [NS] x ([BY][BX] + pad): the TMA boxes
+  uint32_t* sx = reinterpret_cast<uint32_t*>(smem + kNS * kStage);   // [BY][TX]: x-passed rows (u32: no unpacking)
   __shared__ __align__(8) uint64_t full[kNS];
   const int x0 = blockIdx.x * kTX, y0 = blockIdx.y * kTY;
   const int z0 = D == 3 ? blockIdx.z * kZC : 0;
@@ -127,7 +97,7 @@ __global__ void __launch_bounds__(kThreads, H <= 5 ? 2 : 1) blur_tma_kernel(cons
     for (int s = 0; s < kNS; ++s) mbar_init(&full[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     for (int p = 0; p < kNS - 1 && p < nplanes; ++p)
-      tma_load_box(&map, ring + p * kBX * BY, &full[p], x0 - 8, y0 - H, plane_z(p), kBoxBytes);
+      tma_load_box(&map, ring + p * (kStage / 2), &full[p], x0 - 8, y0 - H, plane_z(p), kBoxBytes);
   }
   __syncthreads();
   // this thread's outputs: rows 2 rb, 2 rb + 1 of the tile, x 4 q .. 4 q + 3
@@ -141,7 +111,7 @@ __global__ void __launch_bounds__(kThreads, H <= 5 ? 2 : 1) blur_tma_kernel(cons
       const int p = base + j;
       if (p >= nplanes) break;
       const int s = p % kNS;
-      uint16_t* box = ring + s * kBX * BY;
+      uint16_t* box = ring + s * (kStage / 2);
       mbar_wait(&full[s], (uint32_t)((p / kNS) & 1));
       if (edge) fix_edges<BY>(box, x0, y0, H, nx, ny);
       __syncthreads();   // box complete; the previous plane's y pass is done with sx
@@ -164,7 +134,7 @@ __global__ void __launch_bounds__(kThreads, H <= 5 ? 2 : 1) blur_tma_kernel(cons
       __syncthreads();   // sx complete; every read of this box done
       if (tid == 0 && p + kNS - 1 < nplanes) {
         const int nq = p + kNS - 1;
-        tma_load_box(&map, ring + (nq % kNS) * kBX * BY, &full[nq % kNS], x0 - 8, y0 - H, plane_z(nq), kBoxBytes);
+        tma_load_box(&map, ring + (nq % kNS) * (kStage / 2), &full[nq % kNS], x0 - 8, y0 - H, plane_z(nq), kBoxBytes);
       }
       // y pass, two output rows per thread: sx rows 2 rb .. 2 rb + 2H + 1 (row i + H is output row i)
       uint32_t yv[2][4];
@@ -220,43 +190,11 @@ __global__ void __launch_bounds__(kThreads, H <= 5 ? 2 : 1) blur_tma_kernel(cons
   }
 }
 
-// ------------------------------------------------------------------ host side
-using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
-                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
-                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-
-EncodeTiledFn encode_fn() {
-  static std::once_flag once;
-  static EncodeTiledFn fn = nullptr;
-  std::call_once(once, [] {
-    void* p = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<EncodeTiledFn>(p);
-  });
-  return fn;
-}
-
-// u16 volume (nx, ny, nz) x-fastest as a 3D tensor map, box (bx, by, 1)
-int32_t volume_map(CUtensorMap* map, const uint16_t* base, int nx, int ny, int nz, int bx, int by) {
-  EncodeTiledFn enc = encode_fn();
-  if (!enc) return fail(SNK_CUDA, "cuTensorMapEncodeTiled unavailable");
-  cuuint64_t dims[3] = {(cuuint64_t)nx, (cuuint64_t)ny, (cuuint64_t)nz};
-  cuuint64_t strides[2] = {(cuuint64_t)nx * 2, (cuuint64_t)nx * ny * 2};
-  cuuint32_t box[3] = {(cuuint32_t)bx, (cuuint32_t)by, 1}, es[3] = {1, 1, 1};
-  const CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT16, 3, const_cast<uint16_t*>(base), dims, strides, box, es,
-                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                         CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) return fail(SNK_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
-  return SNK_OK;
-}
-
 template <int D, int H>
 int32_t launch_blur_tma(const uint16_t* in, uint16_t* out, int nx, int ny, int nz, const StencilTaps& T,
                         cudaStream_t st) {
   constexpr int BY = kTY + 2 * H;
-  const int smem = kNS * kBX * BY * 2 + BY * kTX * 4;
+  const int smem = kNS * ((kBX * BY * 2 + 127) & ~127) + BY * kTX * 4;
   CUtensorMap map;
   SNK_TRY(volume_map(&map, in, nx, ny, nz, kBX, BY));
   auto k = blur_tma_kernel<D, H>;
@@ -272,9 +210,42 @@ int32_t launch_blur_tma(const uint16_t* in, uint16_t* out, int nx, int ny, int n
 
 }  // namespace
 
+// ------------------------------------------------------------------ host side
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_fn() {
+  static std::once_flag once;
+  static EncodeTiledFn fn = nullptr;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  });
+  return fn;
+}
+
+int32_t volume_map(CUtensorMap* map, const uint16_t* base, int nx, int ny, int nz, int bx, int by) {
+  EncodeTiledFn enc = encode_fn();
+  if (!enc) return fail(SNK_CUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[3] = {(cuuint64_t)nx, (cuuint64_t)ny, (cuuint64_t)nz};
+  cuuint64_t strides[2] = {(cuuint64_t)nx * 2, (cuuint64_t)nx * ny * 2};
+  cuuint32_t box[3] = {(cuuint32_t)bx, (cuuint32_t)by, 1}, es[3] = {1, 1, 1};
+  const CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT16, 3, const_cast<uint16_t*>(base), dims, strides, box, es,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                         CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(SNK_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+  return SNK_OK;
+}
+
+bool tma_available() { return encode_fn() != nullptr; }
+
 bool blur_tma_ok(const snk_grid* g, int h, const void* in, const void* out) {
   return h >= 1 && h <= 8 && !grid_aniso(g) && g->n[0] % 8 == 0 && (reinterpret_cast<uintptr_t>(in) & 15) == 0 &&
-         (reinterpret_cast<uintptr_t>(out) & 15) == 0 && encode_fn() != nullptr;
+         (reinterpret_cast<uintptr_t>(out) & 15) == 0 && tma_available();
 }
 
 int32_t blur_tma(const snk_grid* g, int h, const int32_t* taps, const uint16_t* in, uint16_t* out,

@@ -319,7 +319,7 @@ def bench_rank(args, cfg):
     torch.cuda.synchronize()
     tdist.barrier()
     l0 = snk.snk_launch_count()
-    from bench import ClockSampler, OPS_PER_SAMPLE, SMS, LANES_PER_SM  # noqa: E402
+    from bench import ClockSampler, GATHER_BYTES, L2_PEAK_GBPS, hbm_peak  # noqa: E402
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(args.steps)]
     with ClockSampler(local_rank) as clk:
         torch.cuda.synchronize()
@@ -332,7 +332,7 @@ def bench_rank(args, cfg):
         torch.cuda.synchronize()
         tdist.barrier()
     red_dev = "cpu" if backend == "gloo" else "cuda"
-    evolve_ms = statistics.mean(a.elapsed_time(b) for a, b in evs)
+    evolve_ms = statistics.median(a.elapsed_time(b) for a, b in evs)
     ms = torch.tensor([s.elapsed_time(e), evolve_ms], dtype=torch.float64, device=red_dev)
     tdist.all_reduce(ms, op=tdist.ReduceOp.MAX)
     total_ms, evolve_ms_max = float(ms[0].item()), float(ms[1].item())
@@ -342,12 +342,12 @@ def bench_rank(args, cfg):
     ci = torch.tensor([r["cell_iters"]], dtype=torch.int64, device=red_dev)
     tdist.all_reduce(ci, op=tdist.ReduceOp.SUM)
     samples = int(ci.item()) * cfg.n_samples
-    # this rank's evolve kernel against the per-GPU ALU peak; reported as the mean over ranks
+    # this rank's evolve kernel: algorithmic gather bytes / its device time (SURVEY
+    # 8(d)(ii)) against the per-GPU HBM and L2 peaks; the mean over ranks
     my_samples = r["cell_iters"] * cfg.n_samples
     clocks = clk.summary()
-    f_clk = (clocks["sm_max_mhz"] or 1965.0) * 1e6
-    peak = SMS * LANES_PER_SM * f_clk / 1e9
-    ach = torch.tensor([my_samples * OPS_PER_SAMPLE / (evolve_ms / 1e3) / 1e9], dtype=torch.float64,
+    hbm, hbm_src = hbm_peak()
+    ach = torch.tensor([my_samples * GATHER_BYTES[cfg.dim] / (evolve_ms / 1e3) / 1e9], dtype=torch.float64,
                        device=red_dev)
     tdist.all_reduce(ach, op=tdist.ReduceOp.SUM)
     achieved = float(ach.item()) / world
@@ -386,10 +386,11 @@ def bench_rank(args, cfg):
                "cells_per_s": n_total * args.steps / (total_ms / 1e3), "gpu_launches": int(launches),
                "phase_ms": {"evolve_max_over_ranks": evolve_ms_max},
                "clocks": clocks,
-               "roofline": {"bound": "alu", "achieved": round(achieved, 1), "peak": round(peak, 1),
-                            "unit": "Glane-op/s", "frac": round(achieved / peak, 4), "traffic": None,
-                            "kernel": "evolve_brick_kernel (slab)", "ops_per_sample": OPS_PER_SAMPLE,
-                            "per": "GPU, mean over ranks"},
+               "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
+                            "frac": round(achieved / hbm, 4), "traffic": None, "peak_source": hbm_src,
+                            "l2": {"peak": L2_PEAK_GBPS, "frac": round(achieved / L2_PEAK_GBPS, 4)},
+                            "algorithmic_bytes_per_sample": GATHER_BYTES[cfg.dim],
+                            "kernel": "evolve_brick_kernel (slab)", "per": "GPU, mean over ranks"},
                "cpu_baseline": cpu,
                "e2e": {"value": samples * args.steps / e2e_s, "unit": "ray-samples/s",
                        "h2d_bytes_per_step": int(nown * 2 * world),

@@ -32,9 +32,20 @@ for cfg, rep in zip(args[::2], args[1::2]):
             v = float(d[k].replace(",", ""))
             return v * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}[unit[k]]
         b = val("dram__bytes_read.sum") + val("dram__bytes_write.sum")
-        t.setdefault(cfg, {})["evolve_brick_kernel"] = {
-            "dram_bytes_per_launch": b, "dram_read": val("dram__bytes_read.sum"),
-            "dram_write": val("dram__bytes_write.sum"), "kernel": name, "source": os.path.basename(rep)}
+        e = {"dram_bytes_per_launch": b, "dram_read": val("dram__bytes_read.sum"),
+             "dram_write": val("dram__bytes_write.sum"), "kernel": name, "source": os.path.basename(rep)}
+        # the binding units' speed-of-light percentages
+        for key, metric in (("issue_pct", "smsp__issue_active.avg.pct_of_peak_sustained_active"),
+                            ("shared_wavefront_pct",
+                             "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed"),
+                            ("l2_throughput_pct", "lts__t_sectors.avg.pct_of_peak_sustained_elapsed"),
+                            ("duration_ns", "gpu__time_duration.sum")):
+            if metric in d and d[metric]:
+                v = float(d[metric].replace(",", ""))
+                if key == "duration_ns":
+                    v *= {"nsecond": 1, "usecond": 1e3, "msecond": 1e6, "second": 1e9}.get(unit[metric], 1)
+                e[key] = v
+        t.setdefault(cfg, {})["evolve_brick_kernel"] = e
         break
 json.dump(t, open(out_path, "w"), indent=1)
 print(json.dumps(t, indent=1))

@@ -56,7 +56,9 @@ def _assert_cells_close(g, o, ctx=""):
                                              (3, (70, 9, 16), 1.0), (3, (41, 6, 24), 2.0), (3, (33, 7, 8), 0.5),
                                              # the TMA blur: several x / y tiles, z chunks of 64 + ragged
                                              (3, (130, 70, 136), 1.0), (3, (67, 33, 64), 2.0),
-                                             (3, (3, 100, 200), 1.0), (2, (1, 97, 520), 1.0)])
+                                             (3, (3, 100, 200), 1.0), (2, (1, 97, 520), 1.0),
+                                             # odd radii (h = 3, 1): TMA stages padded to 128 bytes
+                                             (3, (40, 37, 72), 0.75), (3, (20, 50, 64), 0.25)])
 def test_blur_gradmag_bitexact(gpu, dim, shape, sigma):
     torch, snk, _ = gpu
     rng = np.random.default_rng(hash(shape) % 2 ** 32)
@@ -97,7 +99,8 @@ def test_gradmag_extreme_bitexact(gpu, dim, shape):
 @pytest.mark.parametrize("dim,shape,w", [(3, (30, 26, 64), 3), (3, (21, 19, 40), 0), (3, (40, 36, 32), 8),
                                          (3, (25, 22, 45), 5), (2, (1, 90, 128), 6), (2, (1, 70, 75), 4),
                                          # nz > 32: the column-streamed z fold
-                                         (3, (75, 20, 24), 5), (3, (33, 10, 16), 1), (3, (97, 6, 8), 2)])
+                                         (3, (75, 20, 24), 5), (3, (33, 10, 16), 1), (3, (97, 6, 8), 2),
+                                         (3, (140, 70, 136), 5), (3, (66, 100, 72), 4)])
 def test_seeds_maxima_plateaus_bitexact(gpu, dim, shape, w):
     """a4 MAXIMA on quantised random volumes (many equal values: the tie rule
     decides), vectorised (x % 8 == 0) and fallback paths, w in {0, .., 8}."""
@@ -112,6 +115,26 @@ def test_seeds_maxima_plateaus_bitexact(gpu, dim, shape, w):
     ws = torch.empty(max(snk.snk_workspace_bytes(g, p, 16), 16), dtype=torch.uint8, device="cuda")
     cnt, _ = snk.snk_seeds(g, p, _t(torch, vol), seeds, cap, ws)
     exp = oracle.seeds_maxima(vol, dim, w, 20000)
+    assert cnt == len(exp) > 0
+    assert np.array_equal(seeds[:cnt].cpu().numpy(), exp)
+
+
+@pytest.mark.parametrize("shape,w", [((75, 20, 24), 5), ((40, 36, 32), 8), ((140, 70, 136), 5),
+                                     ((50, 33, 80), 7), ((30, 40, 16), 2), ((66, 100, 72), 4)])
+def test_seeds_maxima_tma_path(gpu, monkeypatch, shape, w):
+    """The one-pass TMA MAXIMA kernel (SNK_TMA_MAXIMA=1: several x / y tiles, z
+    chunks, ragged edges): bit-exact like the default box-max passes."""
+    torch, snk, _ = gpu
+    monkeypatch.setenv("SNK_TMA_MAXIMA", "1")
+    rng = np.random.default_rng(sum(shape) + w)
+    vol = (rng.integers(0, 12, size=shape) * 5000).astype(np.uint16)
+    g = snk.make_grid(3, (shape[2], shape[1], shape[0]))
+    p = snk.make_params(10.0, seed_mode=snk.SEED_MAXIMA, seed_window=w, seed_threshold=20000)
+    cap = int(np.prod(shape)) + 16
+    seeds = torch.empty((cap, 3), dtype=torch.float32, device="cuda")
+    ws = torch.empty(max(snk.snk_workspace_bytes(g, p, 16), 16), dtype=torch.uint8, device="cuda")
+    cnt, _ = snk.snk_seeds(g, p, _t(torch, vol), seeds, cap, ws)
+    exp = oracle.seeds_maxima(vol, 3, w, 20000)
     assert cnt == len(exp) > 0
     assert np.array_equal(seeds[:cnt].cpu().numpy(), exp)
 
@@ -600,6 +623,50 @@ def test_cull_and_label_stage_isolated(gpu, name):
         got = P.labels.cpu().numpy()[pts[:, 2], pts[:, 1], pts[:, 0]]
         assert np.array_equal(got, exp)
     assert (P.labels.cpu().numpy() > 0).any()
+
+
+def _crafted_dets(snk, rng, n, dim, k):
+    """Detections built to exercise every rule of O7: heavily overlapping inner
+    balls (second-ball keys), exact duplicates (equal keys: the smaller index
+    wins), integer centres with radii whose inner ball passes through voxel
+    centres (d2 == thr up to rounding: the fp32 filter's band), balls cut by the
+    volume faces."""
+    d = np.zeros(k, snk.CELL_DTYPE)
+    c = rng.uniform(-3, np.asarray(n, np.float64) + 3, (k, 3)).astype(np.float32)
+    R = rng.uniform(2.0, 9.0, k).astype(np.float32)
+    h = k // 4
+    c[h:2 * h] = c[:h] + rng.uniform(-2, 2, (h, 3)).astype(np.float32)   # overlapping partners
+    c[2 * h:2 * h + h // 2] = c[:h // 2]                                  # exact duplicates
+    R[2 * h:2 * h + h // 2] = R[:h // 2]
+    c[3 * h:] = np.round(c[3 * h:])                                       # boundary-band radii
+    rho = 2.0 ** (-1.0 / dim)
+    R[3 * h:] = (np.sqrt(rng.integers(4, 60, k - 3 * h)) / rho).astype(np.float32)
+    if dim == 2:
+        c[:, 2] = 0.0
+    d["c"], d["R"] = c, R
+    return d
+
+
+@pytest.mark.parametrize("dim,n,k,scale", [(3, (70, 45, 40), 400, (1.0, 1.0, 1.0)),
+                                           (3, (64, 40, 33), 300, (1.0, 1.0, 2.0)),
+                                           (2, (150, 110, 1), 500, (1.0, 1.0, 1.0))])
+def test_label_crafted_bitexact(gpu, dim, n, k, scale):
+    """a8 alone on crafted detection lists: the whole label map equals the
+    oracle's fp64 definition (O7, G19) bit for bit."""
+    torch, snk, _ = gpu
+    rng = np.random.default_rng(k + dim)
+    dets = _crafted_dets(snk, rng, n, dim, k)
+    g = snk.make_grid(dim, n, scale=scale)
+    p = snk.make_params(10.0)
+    d_dets = torch.from_numpy(dets.view(np.uint8)).cuda()
+    lab = torch.empty((n[2], n[1], n[0]), dtype=torch.int32, device="cuda")
+    ws = torch.empty(snk.snk_workspace_bytes(g, p, k), dtype=torch.uint8, device="cuda")
+    snk.snk_label(g, p, d_dets, k, lab, ws)
+    torch.cuda.synchronize()
+    exp = oracle.label(n, dim, dets["c"], dets["R"], scale=scale)
+    got = lab.cpu().numpy()
+    assert (exp > 0).mean() > 0.2
+    assert np.array_equal(got, exp), f"{int((got != exp).sum())} voxels differ"
 
 
 def test_end_to_end_c1_and_host_call(gpu):
