@@ -114,7 +114,8 @@ typedef struct snk_grid {
  *   max_iters T (400)                            n_samples N per cell-iteration, a power of 2
  *   seed_mode LATTICE | MAXIMA | GIVEN                  seed_window w, seed_threshold thr (G20)
  *   image_term INTENSITY | GRADMAG                      cta_warps warps per cell: 0 auto, 1, 2, 4, 8
- *   kernel_variant  0 auto (brick kernel when nx is even), 1 warp kernel, 2 brick kernel
+ *   kernel_variant  0 auto (N < 128: group kernel; else brick kernel when nx is even),
+ *             1 warp kernel, 2 brick kernel, 3 group kernel (N / 8 lanes per cell, 4..16)
  *   estimator SNK_EST_MC | SNK_EST_GRID | SNK_EST_MC_CV | SNK_EST_RAY (not MC: brick
  *             kernel only, even nx)
  *   cull_every  periodic culling ("dynamic culling", reading G25): 0 = off
@@ -128,7 +129,7 @@ typedef struct snk_params {
   double r0, delta_R, eps0, e0, sigma, intensity_scale, max_step, r_min, r_max, leash, conv_tol;
   int32_t max_iters, n_samples, seed_mode, seed_window, image_term, cta_warps;
   uint32_t seed_threshold;
-  uint32_t kernel_variant; /* evolve kernel: 0 auto, 1 warp (global gathers), 2 brick (shared memory) */
+  uint32_t kernel_variant; /* evolve kernel: 0 auto, 1 warp (global gathers), 2 brick (shared memory), 3 group */
   int32_t estimator;       /* SNK_EST_MC (default), _GRID, _MC_CV or _RAY */
   int32_t cull_every;      /* 0 off, else periodic culling every cull_every iterations (G25) */
   uint64_t seed;

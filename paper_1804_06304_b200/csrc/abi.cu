@@ -92,11 +92,11 @@ static int32_t validate_params(const snk_params* p, int dim) {
     return fail(SNK_CONFIG, "seed_window must be in [0, 64]");
   if (p->image_term != SNK_IMAGE_INTENSITY && p->image_term != SNK_IMAGE_GRADMAG)
     return fail(SNK_CONFIG, "bad image_term");
-  if (p->kernel_variant > 2) return fail(SNK_CONFIG, "kernel_variant must be 0, 1 or 2");
+  if (p->kernel_variant > 3) return fail(SNK_CONFIG, "kernel_variant must be 0, 1, 2 or 3");
   if (p->estimator < SNK_EST_MC || p->estimator > SNK_EST_RAY)
     return fail(SNK_CONFIG, "estimator must be SNK_EST_MC, _GRID, _MC_CV or _RAY");
   if (p->cull_every < 0) return fail(SNK_CONFIG, "cull_every must be >= 0");
-  if (p->estimator != SNK_EST_MC && p->kernel_variant == 1)
+  if (p->estimator != SNK_EST_MC && (p->kernel_variant == 1 || p->kernel_variant == 3))
     return fail(SNK_CONFIG, "the grid / CV / ray estimators run in the brick kernel only (kernel_variant 0 or 2)");
   (void)dim;
   return SNK_OK;

@@ -28,6 +28,7 @@
 // Reading of the update (G3/G4/G8): E = gamma A0,
 // dE/dc = -gamma A_c, dE/dR = gamma (A_R - (d/R) A0), gamma = (2R)^-d;
 // (c, R) -= clip((eps0/sqrt(n))/2 * grad, +-max_step); R clamp, leash, domain.
+#include <cstdlib>
 #include <mutex>
 
 #include "common.cuh"
@@ -396,13 +397,13 @@ __device__ __forceinline__ Acc leaves(const EvoParams& P, const CellIt& C, const
 __host__ __device__ constexpr int brick_sx(int S) { return (S + 2) & ~1; }
 
 // Gather modes
-enum { G_GLOBAL = 0, G_GLOBAL_SLAB = 1, G_BRICK_CLAMP = 2, G_BRICK_FAST = 3 };
+enum { G_GLOBAL = 0, G_GLOBAL_SLAB = 1, G_BRICK_CLAMP = 2, G_BRICK_FAST = 3, G_GLOBAL_FAST = 4 };
 
 // d-linear lookup of the image at k (u16 units), through the brick or global memory.
 template <int D, int MODE, int S>
 __device__ __forceinline__ float gather_tri(const EvoParams& P, const CellIt& C, float kx, float ky, float kz,
                                             const uint16_t* brick, uint32_t& halo) {
-  constexpr bool CLAMP = MODE != G_BRICK_FAST;
+  constexpr bool CLAMP = MODE != G_BRICK_FAST && MODE != G_GLOBAL_FAST;
   uint32_t rx, ry, rz = kMagicBits;
   const float fx = split_axis<CLAMP>(kx, P.fnx1, P.mx2, &rx);
   const float fy = split_axis<CLAMP>(ky, P.fny1, P.my2, &ry);
@@ -967,6 +968,66 @@ __global__ void __launch_bounds__(W >= 4 ? 32 * W : 128)
 }
 
 // =========================================================================
+// Group kernel (small N, C5's sweep): G lanes per cell, 32 / G cells per warp,
+// 4 warps per CTA.  A cell's N samples are split G ways (B = N / G per lane,
+// contiguous blocks), summed by the in-lane pairwise tree and a butterfly over
+// the G lanes — the same canonical tree as the warp kernel (bit-identical
+// records) — and every lane takes its cell's update: one instruction stream
+// serves 32 / G cells, so the per-iteration reduce and update (the
+// occupancy / per-contour overhead the paper measured) are amortised over
+// several cells.  No shared memory and no barriers; gathers through L1/L2,
+// unclamped when every cell of the warp has its ball inside the volume.
+template <int D, int G, bool SLAB, int CH, int L>
+__global__ void __launch_bounds__(128, 4) evolve_group_kernel(const __grid_constant__ EvoParams P) {
+  constexpr int CPW = 32 / G;                // cells per warp
+  constexpr int B = CH << L;                 // samples per lane per iteration
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t cell = ((int64_t)blockIdx.x * 4 + warp) * CPW + lane / G;
+  const bool valid = cell < P.n;
+  if (((int64_t)blockIdx.x * 4 + warp) * CPW >= P.n) return;   // whole warp past the end
+  const int sl = lane % G;
+  CellState s;
+  cell_begin(P, valid ? cell : P.n - 1, D, s);   // tail lanes shadow the last cell (no write)
+  uint32_t halo = 0;
+  const uint32_t j0 = (uint32_t)(sl * B);
+  const float n1[3] = {P.fnx1, P.fny1, P.fnz1};
+  for (int it = P.it0; it <= P.it1; ++it) {
+    const CellIt C = cell_iter(P, s, it);
+    Acc sum;
+    bool fast = false;
+    if (!SLAB) {
+      // the d-linear taps of the ball [floor(c - ext), floor(c + ext) + 1] inside the volume
+      const float ext = __fmaf_rn(C.rho_s, 1.0001f, 0.01f);
+      const float c[3] = {C.cx, C.cy, C.cz};
+      bool in = true;
+#pragma unroll
+      for (int a = 0; a < D; ++a) in &= __fsub_rn(c[a], ext) >= 0.0f && __fadd_rn(c[a], ext) + 1.0f <= n1[a];
+      fast = __all_sync(0xffffffffu, in);
+    }
+    if (fast) sum = lane_sum<D, G_GLOBAL_FAST, 1, CH, L>(P, C, j0, nullptr, halo);
+    else sum = lane_sum<D, SLAB ? G_GLOBAL_SLAB : G_GLOBAL, 1, CH, L>(P, C, j0, nullptr, halo);
+    // the lane tree over the group: (l, l^1), (l, l^2), ... as warp_butterfly's first levels
+#pragma unroll
+    for (int o = 1; o < G; o <<= 1) {
+      Acc q;
+      q.a0 = __shfl_xor_sync(0xffffffffu, sum.a0, o);
+      q.cx = __shfl_xor_sync(0xffffffffu, sum.cx, o);
+      q.cy = __shfl_xor_sync(0xffffffffu, sum.cy, o);
+      q.cz = __shfl_xor_sync(0xffffffffu, sum.cz, o);
+      q.aR = __shfl_xor_sync(0xffffffffu, sum.aR, o);
+      sum = acc_add(sum, q);
+    }
+    if (cell_update<D>(P, s, C, sum, it)) break;
+  }
+  if (SLAB) {
+#pragma unroll
+    for (int o = 1; o < G; o <<= 1) halo |= __shfl_xor_sync(0xffffffffu, halo, o);
+    if (halo) s.flags |= SNK_F_HALO;
+  }
+  if (valid && sl == 0) cell_finish(P, s, cell);
+}
+
+// =========================================================================
 // Brick kernel: one CTA (W warps) per cell; the u16 neighbourhood of the cell
 // (x: brick_sx(S) columns from an even origin, y and z: S rows/planes) lives in
 // shared memory, filled by 4-byte cp.async copies (LDGSTS) when the sampled
@@ -1341,6 +1402,46 @@ int32_t launch_warp(const EvoParams& P, cudaStream_t st) {
   return SNK_OK;
 }
 
+template <int D, int G, bool SLAB, int CH, int L>
+int32_t launch_group(const EvoParams& P, cudaStream_t st) {
+  constexpr int CPB = 4 * (32 / G);
+  evolve_group_kernel<D, G, SLAB, CH, L><<<(unsigned)ceil_div(P.n, CPB), 128, 0, st>>>(P);
+  SNK_LAUNCH_CHECK("evolve_group_kernel");
+  return SNK_OK;
+}
+
+template <int D, int G, bool SLAB>
+int32_t group_B(const EvoParams& P, int B, cudaStream_t st) {
+  switch (B) {
+    case 4: return launch_group<D, G, SLAB, 4, 0>(P, st);
+    case 8: return launch_group<D, G, SLAB, 4, 1>(P, st);
+    case 16: return launch_group<D, G, SLAB, 4, 2>(P, st);
+    case 32: return launch_group<D, G, SLAB, 4, 3>(P, st);
+    default: return fail(SNK_CONFIG, "group kernel: 4 .. 32 samples per lane");
+  }
+}
+
+template <int D, bool SLAB>
+int32_t group_G(const EvoParams& P, int G, int B, cudaStream_t st) {
+  switch (G) {
+    case 4: return group_B<D, 4, SLAB>(P, B, st);
+    case 8: return group_B<D, 8, SLAB>(P, B, st);
+    case 16: return group_B<D, 16, SLAB>(P, B, st);
+    default: return fail(SNK_CONFIG, "group kernel: 4, 8 or 16 lanes per cell");
+  }
+}
+
+// lanes per cell of the group kernel: B = 8 samples per lane (SNK_GROUP_B
+// overrides, tuning only; B = 16 measured 15-40% slower on C5); 0 when the
+// group kernel does not apply
+int group_lanes(int n_samples) {
+  const char* e = getenv("SNK_GROUP_B");
+  const int B = e ? atoi(e) : 8;
+  if (B < 4 || B > 32 || (B & (B - 1))) return 0;
+  const int G = n_samples / B;
+  return (G >= 4 && G <= 16 && G * B == n_samples) ? G : 0;
+}
+
 template <int D, int W, int S, bool SLAB, int CH, int L, int EST = 0>
 int32_t launch_brick(const EvoParams& P, cudaStream_t st) {
   auto k = evolve_brick_kernel<D, W, S, SLAB, CH, L, EST>;
@@ -1426,7 +1527,10 @@ int32_t brick_B(const EvoParams& P, int B, cudaStream_t st) {
 // Small N (< 1024) with small contours: 1 or 2 warps per cell keep 8 samples
 // per thread (the per-iteration update is paid per warp), and a 28 x 27 x 27
 // brick (40.8 KB) lets 5 CTAs share an SM.
-constexpr int kS3small = 27;
+#ifndef SNK_BRICK_S3SMALL
+#define SNK_BRICK_S3SMALL 27
+#endif
+constexpr int kS3small = SNK_BRICK_S3SMALL;
 template <int W, bool SLAB>
 int32_t brick_small_B(const EvoParams& P, int B, cudaStream_t st) {
   switch (B) {
@@ -1616,6 +1720,18 @@ int32_t evolve_impl(const snk_grid* g, const snk_params* p, const uint16_t* d_im
   const bool brick_ok = variant != 1 && Bb >= 1 && Bb <= 128 && (Wb == 4 || Wb == 8) &&
                         g->n[0] % 2 == 0 && (reinterpret_cast<uintptr_t>(d_image) & 3) == 0;
   if (variant == 2 && !brick_ok) return fail(SNK_CONFIG, "brick kernel unavailable for this volume");
+  // small N (C5's sweep): several cells per warp (variant 3; auto for N < 128,
+  // where the small-brick kernel would hold one warp per 41 KB brick: C5 at
+  // N = 64 1.89 vs 2.19 ms for the warp kernel; from N = 128 the brick wins)
+  if (variant == 3 || (variant == 0 && p->cta_warps == 0 && p->n_samples < 128)) {
+    const int G = group_lanes(p->n_samples);
+    if (G > 0) {
+      const int B = p->n_samples / G;
+      if (D == 3) return slab ? group_G<3, true>(P, G, B, st) : group_G<3, false>(P, G, B, st);
+      return group_G<2, false>(P, G, B, st);
+    }
+    if (variant == 3) return fail(SNK_CONFIG, "group kernel: n_samples = G x B with G in 4..16, B in 4..32");
+  }
   // small N and small contours (C5's sweep): the small-brick kernel, auto warps only
   const bool small_ok = variant != 1 && D == 3 && p->cta_warps == 0 && p->n_samples >= 128 &&
                         p->n_samples < 1024 && p->r0 <= 9.5 && g->n[0] % 2 == 0 &&

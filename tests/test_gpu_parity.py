@@ -843,6 +843,25 @@ def test_small_n_small_brick_kernel(gpu, N):
     _assert_cells_close(g, o, f"small N={N}")
 
 
+@pytest.mark.parametrize("N,B", [(64, 4), (64, 16), (128, 8), (128, 32), (256, 16), (256, 32)])
+def test_group_kernel_bit_identical_to_warp_kernel(gpu, monkeypatch, N, B):
+    """The group kernel (N / B lanes per cell, several cells per warp; the
+    default for N <= 256) takes the same canonical tree as the warp kernel:
+    byte-identical records, lattice cells near the volume faces included (the
+    clamped and the unclamped gathers mix inside a warp's iterations)."""
+    torch, snk, pipeline = gpu
+    monkeypatch.setenv("SNK_GROUP_B", str(B))
+    cfg = synth.CONFIGS["C1"].with_(r0=9.0, n_samples=N, max_iters=60)
+    P, raw, p = _gpu_smooth_seeds(torch, snk, pipeline, cfg, seed_mode=snk.SEED_LATTICE, kernel_variant=3)
+    P.evolve()
+    torch.cuda.synchronize()
+    g = P.cells_np()
+    P.params = pipeline.params_for(cfg, seed_mode=snk.SEED_LATTICE, kernel_variant=1, cta_warps=1)
+    P.evolve()
+    torch.cuda.synchronize()
+    assert P.cells_np().tobytes() == g.tobytes()
+
+
 @pytest.mark.parametrize("N,W", [(1024, 4), (2048, 8), (1024, 1)])
 def test_brick_fast_path_bit_identical_to_warp_kernel(gpu, N, W):
     """The default launch (brick kernel, f32x2 fast path, 8 samples per thread)
