@@ -143,6 +143,20 @@ def ncu_sol(config: str, kernel: str = "evolve_brick_kernel"):
         return None
 
 
+def workload_config(cfg, n_gpus=1, cull_every=0, estimator="mc", physical=False):
+    """The `config` object of the JSON line: the workload definition only (both
+    arms print the same one; measured counts such as cells and detections are
+    top-level keys)."""
+    iso = list(cfg.iso_n)
+    vbytes = int(np.prod(iso)) * 2
+    return {"workload": workload_name(cfg), "volume_iso": iso, "n_samples": cfg.n_samples,
+            "iters": cfg.max_iters, "seed_mode": cfg.seed_mode,
+            "parallelism": "1 GPU" if n_gpus <= 1 else f"z-slab x{n_gpus}", "cull_every": cull_every,
+            "estimator": estimator, "physical": bool(physical),
+            "l2": "inputs larger than L2 (u16 volume %.2f GiB > 126 MB)" % (vbytes / 2**30)
+            if vbytes > 126 * 2**20 else "volume fits L2 (%.1f MiB); not flushed" % (vbytes / 2**20)}
+
+
 def ncu_traffic(config: str, kernel: str = "evolve_brick_kernel"):
     """DRAM bytes (dram__bytes_read.sum + dram__bytes_write.sum) per launch of the
     dominant kernel from the committed `ncu --set full` capture of this config
@@ -203,13 +217,15 @@ def oracle_crop_run(cfg, raw_full, target_cells: int, threads: int):
     return samples, dt, desc, len(seeds)
 
 
-CPU_CELLS_PER_CORE = 100   # the oracle sample: a centred crop with ~100 cells per host core
+CPU_CELLS_PER_CORE = 100   # the crop sample (configs the plan below does not cover)
+SUBSET = 100                # evolution of the cells with id = 0 mod 100
+SLAB_PLANES = 16            # volume passes timed on a z-slab of this many owned planes
 
 
 def cpu_sample(cfg, threads: int, part=None):
-    """The oracle's bounded sample (both arms time exactly this): the centred crop
-    of the workload holding ~CPU_CELLS_PER_CORE cells per core, a2 -> a4 -> a5/a6
-    -> a7 on it.  Only the crop's planes are generated (outside the timing)."""
+    """The crop sample (configs the SURVEY 8(d) plan does not cover: 2D and
+    anisotropic raw grids): the centred crop of the workload holding
+    ~CPU_CELLS_PER_CORE cells per core, a2 -> a4 -> a5/a6 -> a7 on it."""
     target = CPU_CELLS_PER_CORE * threads
     lo, hi, _, _ = crop_geometry(cfg, target)
     if part is None:
@@ -220,8 +236,77 @@ def cpu_sample(cfg, threads: int, part=None):
     return oracle_crop_run(cfg, raw, target_cells=target, threads=threads), part
 
 
-def cpu_baseline_entry(cfg):
+class CpuPlan:
+    """The oracle timed as SURVEY 8(d) plans it for the full-size 3D workloads:
+    the volume passes (a2 blur, a4 MAXIMA) over a z-slab of SLAB_PLANES owned
+    planes (+ their halo), extrapolated to the whole volume; the evolution
+    (a5/a6) of the deterministic 1% subset (cells with id = 0 mod 100 of the
+    full seed list), extrapolated to every cell; the a7 cull of the subset.
+    Setup, untimed: the full volume's blur and seed list (the subset's inputs).
+    Labels (a8) are not timed."""
+
+    def __init__(self, cfg, threads: int, raw=None):
+        import oracle
+        self.cfg, self.threads = cfg, threads
+        oracle.set_num_threads(threads)
+        self.raw = synth.generate(cfg) if raw is None else raw
+        self.B = oracle.blur(self.raw, 3, 1.0)
+        if cfg.seed_mode == "lattice":
+            self.seeds = oracle.seeds_lattice(cfg.n, 3, cfg.r0)[1]
+        else:
+            self.seeds = oracle.seeds_maxima(self.B, 3, cfg.window, cfg.seed_threshold)
+        self.sub = np.arange(0, len(self.seeds), SUBSET, dtype=np.int64)
+        self.p = oracle.Params(r0=cfg.r0, n_samples=cfg.n_samples, max_iters=cfg.max_iters, dim=3,
+                               seed=cfg.philox_seed)
+        nz = cfg.n[2]
+        self.z0 = nz // 2 - SLAB_PLANES // 2
+        self.z1 = self.z0 + SLAB_PLANES
+
+    def step(self):
+        import oracle
+        cfg, nz = self.cfg, self.cfg.n[2]
+        h = 4 + cfg.window   # blur radius ceil(4 sigma) + the MAXIMA window: the slab's halo
+        lo, hi = max(self.z0 - h, 0), min(self.z1 + h, nz)
+        t0 = time.perf_counter()
+        Bs = oracle.blur(self.raw[lo:hi], 3, 1.0)   # the slab's planes blurred with its own halo
+        if cfg.seed_mode != "lattice":
+            oracle.seeds_maxima(Bs, 3, cfg.window, cfg.seed_threshold, org=(0, 0, lo), n_global=cfg.n,
+                                lo=(0, 0, self.z0), hi=(cfg.n[0] - 1, cfg.n[1] - 1, self.z1 - 1))
+        t_vol = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        cells = oracle.evolve(self.B, self.p, self.seeds[self.sub], ids=self.sub)
+        t_evo = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        oracle.cull(cells["c"].astype(np.float32), cells["R"].astype(np.float32),
+                    cells["E"].astype(np.float32), cells["flags"], cells["id"], 3, self.p.e0)
+        t_cull = time.perf_counter() - t0
+        n, k = len(self.seeds), len(self.sub)
+        t_full = t_vol * nz / SLAB_PLANES + t_evo * n / k + t_cull
+        return {"seconds_full_extrapolated": t_full, "seconds_measured": t_vol + t_evo + t_cull,
+                "samples_full": n * (cfg.max_iters + 1) * cfg.n_samples,
+                "t_volume_slab": t_vol, "t_evolve_subset": t_evo, "t_cull_subset": t_cull}
+
+    def describe(self):
+        return (f"{self.cfg.name}, SURVEY 8(d) plan, EXTRAPOLATED: a2 blur + a4 MAXIMA on planes "
+                f"[{self.z0}, {self.z1}) + halo x {self.cfg.n[2] // SLAB_PLANES}; a5/a6 evolution of the "
+                f"{len(self.sub)} cells with id = 0 mod {SUBSET} of {len(self.seeds)} x {SUBSET}; "
+                f"a7 cull of the subset; a8 not timed (fp64 oracle, OpenMP, {self.threads} threads)")
+
+
+def plan_applies(cfg) -> bool:
+    return cfg.dim == 3 and tuple(cfg.iso_n) == tuple(cfg.n) and cfg.n[2] >= 4 * SLAB_PLANES
+
+
+def cpu_baseline_entry(cfg, raw=None):
     threads = os.cpu_count() or 1
+    if plan_applies(cfg):
+        plan = CpuPlan(cfg, threads, raw)
+        r = plan.step()
+        v = r["samples_full"] / r["seconds_full_extrapolated"]
+        return {"value": v, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": plan.describe(),
+                "extrapolated": True, "seconds_measured": round(r["seconds_measured"], 2),
+                "seconds_full_extrapolated": round(r["seconds_full_extrapolated"], 1),
+                "cells_per_s": len(plan.seeds) / r["seconds_full_extrapolated"]}
     (s, dt, desc, nc), _ = cpu_sample(cfg, threads)
     return {"value": s / dt, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": desc,
             "seconds": round(dt, 2), "cells_per_s": nc / dt}
@@ -383,17 +468,13 @@ def run_ours(args):
                "cells_per_s": n_cells * args.steps / e2e_s, "inflight": k, "mode": args.e2e_mode}
     cpu = None
     if not args.no_cpu_baseline and cfg.dim == 3 and tuple(cfg.iso_n) == tuple(cfg.n):
-        cpu = cpu_baseline_entry(cfg)
+        cpu = cpu_baseline_entry(cfg, raw=h_raw.numpy())
     out = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": workload_name(cfg), "volume_iso": n_iso_l, "cells": n_cells,
-                   "detections": n_dets, "n_samples": cfg.n_samples, "iters": cfg.max_iters,
-                   "seed_mode": cfg.seed_mode, "parallelism": "1 GPU", "cull_every": args.cull_every,
-                   "estimator": args.estimator, "physical": bool(args.physical),
-                   "l2": "inputs larger than L2 (u16 volume %.1f GiB > 126 MB)" % (h_raw.numel() * 2 / 2**30)},
-        "cells_per_s": cells_per_s, "phase_ms": phase,
+        "config": workload_config(cfg, 1, args.cull_every, args.estimator, args.physical),
+        "cells": n_cells, "detections": n_dets, "cells_per_s": cells_per_s, "phase_ms": phase,
         "phase_ms_spread": {k: spread(v) for k, v in phase_lists.items()}, "gpu_launches": int(launches),
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
         "generate_s": round(gen_s, 2),
@@ -404,26 +485,40 @@ def run_ours(args):
 
 # ---------------------------------------------------------------- reference arm (the oracle)
 def run_reference(args):
+    """The oracle as it stands on the host cores, on our arm's workload and metric
+    (the SURVEY 8(d) plan where it applies: every step re-times the slab volume
+    passes and the 1% evolution subset, extrapolated; else the crop sample)."""
     rank, _, world = dist_env()
     if rank != 0:
         return None
     cfg = synth.CONFIGS[args.config]
     threads = os.cpu_count() or 1
-    # the bounded sample, identical to our arm's cpu_baseline (cpu_sample)
     samples = secs = 0.0
-    desc = ""
-    part = None
-    for k in range(args.warmup + args.steps):
-        (s, dt, desc, _), part = cpu_sample(cfg, threads, part)
-        if k >= args.warmup:
-            samples += s
-            secs += dt
+    if plan_applies(cfg):
+        plan = CpuPlan(cfg, threads)
+        for k in range(args.warmup + args.steps):
+            r = plan.step()
+            if k >= args.warmup:
+                samples += r["samples_full"]
+                secs += r["seconds_full_extrapolated"]
+        desc, extra = plan.describe(), {"extrapolated": True}
+        cells = len(plan.seeds)
+    else:
+        part = None
+        desc, cells = "", 0
+        for k in range(args.warmup + args.steps):
+            (s, dt, desc, cells), part = cpu_sample(cfg, threads, part)
+            if k >= args.warmup:
+                samples += s
+                secs += dt
+        extra = {}
     v = samples / secs
     return {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": max(world, args.gpus),
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": secs / args.steps * 1e3,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "config": {"workload": workload_name(cfg)},
-            "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": desc},
+            "data": "synthetic", "config": workload_config(cfg, max(world, args.gpus)),
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": desc, **extra},
+            "cells_per_s": cells * args.steps / secs,
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 
 

@@ -35,7 +35,7 @@
 extern "C" {
 #endif
 
-#define SNK_ABI_VERSION 4
+#define SNK_ABI_VERSION 5
 
 /* Status codes — mirror SPEC's exit scheme plus CUDA / capacity. */
 typedef enum {
@@ -195,6 +195,13 @@ int32_t snk_preprocess(const snk_grid* g, const snk_params* p, const uint16_t* d
                        uint16_t* d_smooth, uint16_t* d_gradmag, void* d_ws, size_t ws_bytes,
                        void* stream);
 
+/* a0 — ingest of an 8-bit volume (SPEC S:348-356, S:402 dtype "u8"; SURVEY
+ * 8(c) O0): d_out[i] = 257 * d_in[i], the exact u16 image of the 8-bit value
+ * (0 -> 0, 255 -> 65535), for n voxels (x-fastest layout unchanged).  Device
+ * buffers are the caller's; any alignment (16-byte aligned buffers take the
+ * vectorised kernel).  Asynchronous on `stream`. */
+int32_t snk_ingest_u8(const uint8_t* d_in, uint16_t* d_out, int64_t n, void* stream);
+
 /* a4 — seeds (P:169 lattice "located at a distance sqrt(1.5) R apart", P:238;
  * north_star seed detection, G20).  LATTICE: centred cubic lattice spaced
  * sqrt(1.5) r0, footprint m = r0 + dR/2 inside (EMPTY_DOMAIN if it does not fit),
@@ -286,6 +293,16 @@ int32_t snk_run(int32_t dim, const int64_t n_raw[3], const double spacing[3],
                 const snk_params* p, const uint16_t* h_raw, snk_cell* h_dets, int64_t det_cap,
                 int64_t* n_dets, int32_t* h_labels, int64_t max_cells, void* d_ws,
                 size_t ws_bytes, void* stream);
+
+/* snk_run for an 8-bit raw volume: h_raw holds n_raw voxels of
+ * u8; they are uploaded as bytes (half the host->device traffic of u16) and
+ * promoted on the device by snk_ingest_u8, then the path runs exactly as
+ * snk_run on the u16 volume 257 * h_raw (bit-identical results).  Same
+ * workspace (snk_run_workspace_bytes).  Synchronises. */
+int32_t snk_run_u8(int32_t dim, const int64_t n_raw[3], const double spacing[3],
+                   const snk_params* p, const uint8_t* h_raw, snk_cell* h_dets, int64_t det_cap,
+                   int64_t* n_dets, int32_t* h_labels, int64_t max_cells, void* d_ws,
+                   size_t ws_bytes, void* stream);
 
 /* snk_run over nvol volumes of the same shape (the end-to-end call for a
  * stream of volumes): volume i is read from h_raw[i], its detections written to

@@ -183,6 +183,15 @@ def q14_taps(sigma):
     return taps[:2 * h + 1].copy()
 
 
+def ingest_u8(vol):
+    """O0 (SPEC S:348-356 loads u8 samples "without rescaling", S:402
+    dtype "u8"): an 8-bit sample v becomes the u16 sample 257 v, so that the path's
+    intensity scale 1/257 (reading G6) gives back v in 8-bit units exactly."""
+    v = np.asarray(vol)
+    assert v.dtype == np.uint8
+    return (v.astype(np.int64) * 257).astype(np.uint16)
+
+
 def blur(vol, dim=3, sigma=1.0):
     """O2; sigma may be a per-axis triple (anisotropic grid, G28: sigma / scale_a)."""
     v = _u16(vol)

@@ -403,10 +403,10 @@ static int32_t run_compute(const RunLayout& L, int32_t dim, const int64_t n_raw[
   return SNK_OK;
 }
 
-int32_t snk_run(int32_t dim, const int64_t n_raw[3], const double spacing[3],
-                const snk_params* p, const uint16_t* h_raw, snk_cell* h_dets, int64_t det_cap,
-                int64_t* n_dets, int32_t* h_labels, int64_t max_cells, void* d_ws,
-                size_t ws_bytes, void* stream) {
+// snk_run / snk_run_u8: h_raw holds u16 (bpv 2) or u8 (bpv 1) voxels
+static int32_t run_host(int32_t dim, const int64_t n_raw[3], const double spacing[3], const snk_params* p,
+                        const void* h_raw, int bpv, snk_cell* h_dets, int64_t det_cap, int64_t* n_dets,
+                        int32_t* h_labels, int64_t max_cells, void* d_ws, size_t ws_bytes, void* stream) {
   clear_error();
   if (!h_raw || !n_dets || det_cap < 0 || (det_cap > 0 && !h_dets) || max_cells < 1)
     return fail(SNK_CONFIG, "bad args");
@@ -420,7 +420,15 @@ int32_t snk_run(int32_t dim, const int64_t n_raw[3], const double spacing[3],
   int32_t* d_labels = reinterpret_cast<int32_t*>(base + L.off_labels);
   const size_t nraw = (size_t)n_raw[0] * n_raw[1] * n_raw[2];
   const size_t niso = (size_t)L.g.n[0] * L.g.n[1] * L.g.n[2];
-  SNK_CUDA_CHECK(cudaMemcpyAsync(d_raw, h_raw, nraw * sizeof(uint16_t), cudaMemcpyHostToDevice, st));
+  if (bpv == 2) {
+    SNK_CUDA_CHECK(cudaMemcpyAsync(d_raw, h_raw, nraw * sizeof(uint16_t), cudaMemcpyHostToDevice, st));
+  } else {
+    // a0: the bytes land in the label region (>= 4 niso >= nraw bytes, written
+    // only by a8), then promote into the raw u16 buffer
+    uint8_t* d_u8 = reinterpret_cast<uint8_t*>(base + L.off_labels);
+    SNK_CUDA_CHECK(cudaMemcpyAsync(d_u8, h_raw, nraw, cudaMemcpyHostToDevice, st));
+    SNK_TRY(ingest_u8_impl(d_u8, d_raw, (int64_t)nraw, st));
+  }
   int64_t nd = 0;
   SNK_TRY(run_compute(L, dim, n_raw, spacing, p, d_raw, d_dets, h_labels ? d_labels : nullptr, max_cells, base,
                       st, nullptr, &nd));
@@ -433,6 +441,28 @@ int32_t snk_run(int32_t dim, const int64_t n_raw[3], const double spacing[3],
   SNK_CUDA_CHECK(cudaStreamSynchronize(st));
   if (nd > det_cap) return fail(SNK_CAPACITY, "detection buffer too small");
   return SNK_OK;
+}
+
+int32_t snk_run(int32_t dim, const int64_t n_raw[3], const double spacing[3],
+                const snk_params* p, const uint16_t* h_raw, snk_cell* h_dets, int64_t det_cap,
+                int64_t* n_dets, int32_t* h_labels, int64_t max_cells, void* d_ws,
+                size_t ws_bytes, void* stream) {
+  return run_host(dim, n_raw, spacing, p, h_raw, 2, h_dets, det_cap, n_dets, h_labels, max_cells, d_ws, ws_bytes,
+                  stream);
+}
+
+int32_t snk_run_u8(int32_t dim, const int64_t n_raw[3], const double spacing[3],
+                   const snk_params* p, const uint8_t* h_raw, snk_cell* h_dets, int64_t det_cap,
+                   int64_t* n_dets, int32_t* h_labels, int64_t max_cells, void* d_ws,
+                   size_t ws_bytes, void* stream) {
+  return run_host(dim, n_raw, spacing, p, h_raw, 1, h_dets, det_cap, n_dets, h_labels, max_cells, d_ws, ws_bytes,
+                  stream);
+}
+
+int32_t snk_ingest_u8(const uint8_t* d_in, uint16_t* d_out, int64_t n, void* stream) {
+  clear_error();
+  if (n < 0 || (n > 0 && (!d_in || !d_out))) return fail(SNK_CONFIG, "bad args");
+  return ingest_u8_impl(d_in, d_out, n, as_stream(stream));
 }
 
 // snk_run over a sequence of volumes: the next volume's upload and the previous

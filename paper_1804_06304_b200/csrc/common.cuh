@@ -92,6 +92,8 @@ size_t resample_ws(int32_t dim, const int64_t n_raw[3], const double spacing[3])
 int32_t preprocess_impl(const snk_grid* g, const snk_params* p, const uint16_t* d_in,
                         uint16_t* d_smooth, uint16_t* d_gradmag, void* d_ws, size_t ws_bytes,
                         cudaStream_t st);
+// a0: u8 -> u16 (x257, exact), volume.cu
+int32_t ingest_u8_impl(const uint8_t* d_in, uint16_t* d_out, int64_t n, cudaStream_t st);
 int32_t resample_impl(int32_t dim, const int64_t n_raw[3], const double spacing[3], int64_t zr_lo,
                       int64_t nzr, const uint16_t* d_raw, int64_t z_lo, int64_t nz_out,
                       uint16_t* d_out, void* d_ws, size_t ws_bytes, cudaStream_t st);

@@ -591,6 +591,38 @@ int32_t launch_fused_blur(const snk_grid* g, const uint16_t* d_in, uint16_t* d_o
   return SNK_OK;
 }
 
+
+// ---------------------------------------------------------------- a0 ingest
+// u8 -> u16 by x257 (an 8-bit volume is promoted exactly; 255 ->
+// 65535), 16 voxels per thread with 16-byte loads where aligned.
+__global__ void ingest_u8_kernel(const uint8_t* __restrict__ in, uint16_t* __restrict__ out, int64_t n) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t i0 = t * 16;
+  if (i0 >= n) return;
+  if (i0 + 16 <= n) {
+    const uint4 q = __ldg(reinterpret_cast<const uint4*>(in + i0));
+    const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+    uint32_t o[8];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      // bytes b0 b1 -> (b0 * 257) | (b1 * 257) << 16: u16 v * 257 = v | v << 8
+      const uint32_t lo = __byte_perm(w[k], 0, 0x4140), hi = __byte_perm(w[k], 0, 0x4342);
+      o[2 * k] = lo | (lo << 8);
+      o[2 * k + 1] = hi | (hi << 8);
+    }
+    uint4* dst = reinterpret_cast<uint4*>(out + i0);
+    dst[0] = make_uint4(o[0], o[1], o[2], o[3]);
+    dst[1] = make_uint4(o[4], o[5], o[6], o[7]);
+  } else {
+    for (int64_t i = i0; i < n; ++i) out[i] = (uint16_t)(in[i] * 257u);
+  }
+}
+
+__global__ void ingest_u8_scalar_kernel(const uint8_t* __restrict__ in, uint16_t* __restrict__ out, int64_t n) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = (uint16_t)(in[i] * 257u);
+}
+
 }  // namespace
 
 size_t preprocess_ws(const snk_grid* g, const snk_params* p) {
@@ -795,6 +827,19 @@ int32_t resample_impl(int32_t dim, const int64_t n_raw[3], const double spacing[
     cur = dst;
     cx = ox; cy = oy; cz = oz; cz0 = oz0;
   }
+  return SNK_OK;
+}
+
+int32_t ingest_u8_impl(const uint8_t* d_in, uint16_t* d_out, int64_t n, cudaStream_t st) {
+  if (n <= 0) return SNK_OK;
+  if ((reinterpret_cast<uintptr_t>(d_in) & 15) || (reinterpret_cast<uintptr_t>(d_out) & 15)) {
+    ingest_u8_scalar_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(d_in, d_out, n);   // unaligned buffers
+    SNK_LAUNCH_CHECK("ingest_u8_scalar_kernel");
+    return SNK_OK;
+  }
+  const int64_t threads = (n + 15) / 16;
+  ingest_u8_kernel<<<(unsigned)ceil_div(threads, 256), 256, 0, st>>>(d_in, d_out, n);
+  SNK_LAUNCH_CHECK("ingest_u8_kernel");
   return SNK_OK;
 }
 

@@ -319,7 +319,7 @@ def bench_rank(args, cfg):
     torch.cuda.synchronize()
     tdist.barrier()
     l0 = snk.snk_launch_count()
-    from bench import ClockSampler, GATHER_BYTES, L2_PEAK_GBPS, hbm_peak  # noqa: E402
+    from bench import ClockSampler, GATHER_BYTES, L2_PEAK_GBPS, hbm_peak, workload_config  # noqa: E402
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(args.steps)]
     with ClockSampler(local_rank) as clk:
         torch.cuda.synchronize()
@@ -370,7 +370,7 @@ def bench_rank(args, cfg):
     cpu = None
     if rank == 0 and not getattr(args, "no_cpu_baseline", False):
         from bench import cpu_baseline_entry  # noqa: E402
-        cpu = cpu_baseline_entry(cfg)
+        cpu = cpu_baseline_entry(cfg)   # the whole workload's plan (rank 0 generates the volume)
     out = None
     if rank == 0:
         out = {"metric": "contour ray-samples/sec and cells segmented/sec at 1/2/4/8 B200; HBM/L2 GB/s",
@@ -378,11 +378,8 @@ def bench_rank(args, cfg):
                "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
                "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "strong",
                "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-               "config": {"workload": f"{cfg.name} z-slabs", "volume_iso": list(cfg.n), "cells": n_total,
-                          "detections": r["n_dets"], "n_samples": cfg.n_samples, "iters": cfg.max_iters,
-                          "parallelism": f"z-slab x{world}", "halo_planes": plan.halo,
-                          "cull_every": p.cull_every,
-                          "l2": "inputs larger than L2", "backend": backend},
+               "config": workload_config(cfg, world, p.cull_every),
+               "cells": n_total, "detections": r["n_dets"], "halo_planes": plan.halo, "backend": backend,
                "cells_per_s": n_total * args.steps / (total_ms / 1e3), "gpu_launches": int(launches),
                "phase_ms": {"evolve_max_over_ranks": evolve_ms_max},
                "clocks": clocks,

@@ -207,8 +207,10 @@ class HostRunner:
         self.n_iso = n_iso
 
     def run(self, h_raw: torch.Tensor, stream=None) -> int:
-        return snk.snk_run(self.dim, self.n_raw, self.spacing, self.params, h_raw, self.h_dets,
-                           self.max_cells, self.h_labels, self.max_cells, self.ws, stream)
+        """h_raw: u16 (snk_run) or u8 (snk_run_u8: promoted x257 on the device)."""
+        f = snk.snk_run_u8 if h_raw.dtype == torch.uint8 else snk.snk_run
+        return f(self.dim, self.n_raw, self.spacing, self.params, h_raw, self.h_dets,
+                 self.max_cells, self.h_labels, self.max_cells, self.ws, stream)
 
     def dets_np(self, n) -> np.ndarray:
         return self.h_dets[: n * snk.CELL_BYTES].numpy().view(snk.CELL_DTYPE).copy()

@@ -91,6 +91,8 @@ _SIGS = {
     "snk_cull": (_i32, [_P(snk_grid), _P(snk_params), _vp, _i64, _vp, _i64, _P(_i64), _vp, _sz, _vp]),
     "snk_label": (_i32, [_P(snk_grid), _P(snk_params), _vp, _i64, _vp, _vp, _sz, _vp]),
     "snk_run_workspace_bytes": (_i32, [_i32, _vp, _vp, _P(snk_params), _i64, _P(_sz)]),
+    "snk_ingest_u8": (_i32, [_vp, _vp, _i64, _vp]),
+    "snk_run_u8": (_i32, [_i32, _vp, _vp, _P(snk_params), _vp, _vp, _i64, _P(_i64), _vp, _i64, _vp, _sz, _vp]),
     "snk_run": (_i32, [_i32, _vp, _vp, _P(snk_params), _vp, _vp, _i64, _P(_i64), _vp, _i64, _vp, _sz,
                        _vp]),
     "snk_run_batch_workspace_bytes": (_i32, [_i32, _vp, _vp, _P(snk_params), _i64, _P(_sz)]),
@@ -273,6 +275,19 @@ def snk_run_workspace_bytes(dim, n_raw, spacing, p, max_cells) -> int:
     _check(_lib.snk_run_workspace_bytes(dim, _i64x3(n_raw), _f64x3(spacing), C.byref(p), max_cells,
                                         C.byref(out)), "snk_run_workspace_bytes")
     return out.value
+
+
+def snk_ingest_u8(d_in, d_out, n, stream=None):
+    _check(_lib.snk_ingest_u8(_ptr(d_in), _ptr(d_out), n, _stream(stream)), "snk_ingest_u8")
+
+
+def snk_run_u8(dim, n_raw, spacing, p, h_raw, h_dets, det_cap, h_labels, max_cells, d_ws,
+               stream=None) -> int:
+    nd = C.c_int64()
+    _check(_lib.snk_run_u8(dim, _i64x3(n_raw), _f64x3(spacing), C.byref(p), _ptr(h_raw), _ptr(h_dets),
+                           det_cap, C.byref(nd), _ptr(h_labels), max_cells, _ptr(d_ws), _nbytes(d_ws),
+                           _stream(stream)), "snk_run_u8")
+    return nd.value
 
 
 def snk_run(dim, n_raw, spacing, p, h_raw, h_dets, det_cap, h_labels, max_cells, d_ws,

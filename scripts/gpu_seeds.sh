@@ -9,7 +9,7 @@ for c in C3 C4; do
   for v in tma old; do
     if [ $v = tma ]; then export SNK_TMA_MAXIMA=1; else unset SNK_TMA_MAXIMA; fi
     timeout 600 python bench.py --config $c --steps 3 --warmup 3 --no-cpu-baseline --no-e2e > $O/${TAG}_${c}_$v.json 2> $O/${TAG}_${c}_$v.err
-    python -c "import json; d=json.loads(open('$O/${TAG}_${c}_$v.json').read().splitlines()[-1]); print('$c $v', d['phase_ms'], d['config']['cells'])"
+    python -c "import json; d=json.loads(open('$O/${TAG}_${c}_$v.json').read().splitlines()[-1]); print('$c $v', d['phase_ms'], d['cells'])"
   done
 done
 unset SNK_TMA_MAXIMA

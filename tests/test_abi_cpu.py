@@ -42,7 +42,7 @@ def test_struct_layouts(snk):
     assert C.sizeof(snk.snk_cell) == 64
     assert C.sizeof(snk.snk_grid) == 88                 # static_assert-ed in abi.cu too
     assert C.sizeof(snk.snk_params) == 136
-    assert snk.snk_abi_version() == 4
+    assert snk.snk_abi_version() == 5
     assert snk.status_string(0) == "ok" and snk.status_string(6) == "capacity exceeded"
 
 

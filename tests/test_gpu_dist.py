@@ -189,9 +189,9 @@ def test_bench_launches_ranks_itself(gpu):
     one, _ = _bench(common + ["--no-e2e"])
     two, _ = _bench(["--gpus", "2"] + common, {"SNK_DIST_BACKEND": "gloo"})
     assert two["n_gpus"] == 2 and one["n_gpus"] == 1
-    assert two["config"]["cells"] == one["config"]["cells"]
-    assert two["config"]["detections"] == one["config"]["detections"]
+    assert two["cells"] == one["cells"]
+    assert two["detections"] == one["detections"]
     nc, err = _bench(["--dist"] + common)
-    assert nc["n_gpus"] == 1 and nc["config"]["backend"] == "nccl"
-    assert nc["config"]["detections"] == one["config"]["detections"]
+    assert nc["n_gpus"] == 1 and nc["backend"] == "nccl"
+    assert nc["detections"] == one["detections"]
     assert "NCCL INFO" in err

@@ -669,6 +669,38 @@ def test_label_crafted_bitexact(gpu, dim, n, k, scale):
     assert np.array_equal(got, exp), f"{int((got != exp).sum())} voxels differ"
 
 
+@pytest.mark.parametrize("n,off", [(1 << 20, 0), (100_003, 0), (4099, 3)])
+def test_ingest_u8_bitexact(gpu, n, off):
+    """a0: snk_ingest_u8 = O0 (257 v), vectorised (16-byte aligned) and scalar
+    (unaligned) kernels, ragged lengths."""
+    torch, snk, _ = gpu
+    rng = np.random.default_rng(n)
+    v = rng.integers(0, 256, n, dtype=np.uint8)
+    d_in = torch.empty(n + 16, dtype=torch.uint8, device="cuda")
+    d_in[off:off + n] = _t(torch, v)
+    d_out = torch.empty(n + 16, dtype=torch.int16, device="cuda")
+    snk.snk_ingest_u8(d_in.data_ptr() + off, d_out.data_ptr() + 2 * off, n)
+    torch.cuda.synchronize()
+    got = d_out.cpu().numpy().view(np.uint16)[off:off + n]
+    assert np.array_equal(got, oracle.ingest_u8(v))
+
+
+def test_run_u8_equals_run(gpu):
+    """snk_run_u8 (8-bit host volume, promoted on the device) gives the
+    detections and label map of snk_run on the u16 volume O0 makes of it."""
+    torch, snk, pipeline = gpu
+    cfg = synth.CONFIGS["C1"].with_(max_iters=80)
+    raw8 = (synth.generate(cfg) // 257).astype(np.uint8)
+    p = pipeline.params_for(cfg)
+    H = pipeline.HostRunner(cfg.dim, cfg.n, p)
+    n8 = H.run(torch.from_numpy(raw8).pin_memory())
+    d8, l8 = H.dets_np(n8), H.h_labels.numpy().copy()
+    n16 = H.run(torch.from_numpy(oracle.ingest_u8(raw8)).pin_memory())
+    assert n8 == n16 > 0
+    assert H.dets_np(n16).tobytes() == d8.tobytes()
+    assert np.array_equal(H.h_labels.numpy(), l8)
+
+
 def test_end_to_end_c1_and_host_call(gpu):
     """C1 through the device pipeline and through snk_run (host buffers) against
     the oracle's own end-to-end run."""

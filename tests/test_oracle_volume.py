@@ -193,3 +193,17 @@ def test_maxima_on_crop_equals_full(ora):
     got = ora.seeds_maxima(crop, 3, w, thr, org=org, n_global=n, lo=lo, hi=hi)
     sel = np.all((full >= lo) & (full <= hi), axis=1)
     assert np.array_equal(got, full[sel])
+
+
+def test_ingest_u8_pins(ora):
+    """O0 against facts independent of its formula: the byte-doubling identity
+    257 v = (v << 8) | v for every 8-bit value, the end points 0 -> 0 and
+    255 -> 65535 (the full u16 range), exact division back to the 8-bit value
+    (reading G6: intensity_scale 1/257), order preserved."""
+    v = np.arange(256, dtype=np.uint8)
+    out = ora.ingest_u8(v)
+    assert out.dtype == np.uint16
+    assert np.array_equal(out, (v.astype(np.uint16) << 8) | v.astype(np.uint16))
+    assert out[0] == 0 and out[255] == 65535
+    assert np.array_equal(out.astype(np.int64) % 257, np.zeros(256)) and np.array_equal(out // 257, v)
+    assert np.all(np.diff(out.astype(np.int64)) == 257)
