@@ -198,15 +198,20 @@ struct Dir {
   float ox, oy, oz, L;
 };
 
+// m = 1 + u in [1, 2): the mantissa word alone (u01 without its subtraction)
+__device__ __forceinline__ float m12(uint32_t x) { return __uint_as_float(0x3F800000u | (x >> 9)); }
+
 template <int D>
 __device__ __forceinline__ Dir dir_words(uint32_t w0, uint32_t w1, uint32_t w2) {
-  const float u1 = u01(w1), u2 = u01(w2);
+  const float u2 = u01(w2);
   float sn, cs;
-  __sincosf(__fmul_rn(6.2831853071795865f, u1), &sn, &cs);
+  // phi = 2 pi u1: sin and cos of 2 pi (1 + u1) are the same (period 2 pi), so
+  // the mantissa word m1 = 1 + u1 is used directly (one subtraction fewer)
+  __sincosf(__fmul_rn(6.2831853071795865f, m12(w1)), &sn, &cs);
   Dir d;
   if (D == 3) {
-    const float u0 = u01(w0);
-    d.oz = __fmaf_rn(-2.0f, u0, 1.0f);
+    // z = 1 - 2 u0 = 3 - 2 m0, exact in fp32 either way (a multiple of 2^-22 in (-1, 1])
+    d.oz = __fmaf_rn(-2.0f, m12(w0), 3.0f);
     const float st = sqrt_approx(__fmaf_rn(-d.oz, d.oz, 1.0f));   // sqrt(1 - z^2) = 2 sqrt(u0 (1 - u0))
     d.ox = __fmul_rn(st, cs);
     d.oy = __fmul_rn(st, sn);

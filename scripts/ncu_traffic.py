@@ -43,7 +43,7 @@ for cfg, rep in zip(args[::2], args[1::2]):
             if metric in d and d[metric]:
                 v = float(d[metric].replace(",", ""))
                 if key == "duration_ns":
-                    v *= {"nsecond": 1, "usecond": 1e3, "msecond": 1e6, "second": 1e9}.get(unit[metric], 1)
+                    v *= {"nsecond": 1, "ns": 1, "usecond": 1e3, "us": 1e3, "msecond": 1e6, "ms": 1e6, "second": 1e9, "s": 1e9}[unit[metric]]
                 e[key] = v
         t.setdefault(cfg, {})["evolve_brick_kernel"] = e
         break
