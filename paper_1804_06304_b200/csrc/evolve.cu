@@ -1049,16 +1049,27 @@ __device__ __forceinline__ void load_brick(uint16_t* brick, const EvoParams& P, 
   const int nw = min(WPR, (P.nx - bx + 1) / 2);     // words inside the volume (x)
   const int ny = min(S, P.ny - by);
   const int nzl = D == 3 ? min(S, P.z_lo + P.nz_buf - bz) : 1;
-  const uint32_t* src = reinterpret_cast<const uint32_t*>(P.img);
+  // word (col, ry, rz) of the brick <- word col of volume row (by + ry, bz + rz);
+  // offsets from the brick's first word, in 32-bit words (< 2^31: the brick spans <= S planes)
+  const uint32_t* src = reinterpret_cast<const uint32_t*>(P.img) +
+                        (((int64_t)(bz - zlo_buf) * P.ny + by) * P.nx + bx) / 2;   // bx even
+  const int rw = P.nx / 2, pw = rw * P.ny;                // words per volume row / plane
   const uint32_t dst0 = smem_u32(brick);
-  for (int w = threadIdx.x; w < ROWS * WPR; w += blockDim.x) {
-    const int row = w / WPR, col = w % WPR;
-    const int ry = row % S, rz = row / S;
-    if (col >= nw || ry >= ny || rz >= nzl) continue;
-    const int64_t g = ((int64_t)(bz - zlo_buf + rz) * P.ny + (by + ry)) * P.nx + bx;   // even
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst0 + (uint32_t)w * 4u),
-                 "l"(src + g / 2 + col)
-                 : "memory");
+  // (col, ry, rz) of word w = threadIdx.x + k * blockDim.x, stepped incrementally
+  // (no division per word): the step advances by dr rows and dc columns
+  const int step = blockDim.x, dr = step / WPR, dc = step - dr * WPR;
+  int w = threadIdx.x;
+  int row = w / WPR, col = w - row * WPR;
+  int rz = row / S, ry = row - rz * S;
+  for (; w < ROWS * WPR; w += step) {
+    if (col < nw && ry < ny && rz < nzl)
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst0 + (uint32_t)w * 4u),
+                   "l"(src + (rz * pw + ry * rw + col))
+                   : "memory");
+    col += dc;
+    ry += dr;
+    if (col >= WPR) { col -= WPR; ++ry; }
+    while (ry >= S) { ry -= S; ++rz; }
   }
   asm volatile("cp.async.wait_all;" ::: "memory");
   __syncthreads();

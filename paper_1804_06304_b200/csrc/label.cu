@@ -126,29 +126,20 @@ __device__ __forceinline__ void prefetch_tile(Prefetch& f, const snk_cell* __res
 
 // The exact O7 rules for one (voxel, candidate) pair the fp32 filter could not
 // settle (near a ball's boundary, or a second ball containing the voxel): rare,
-// so it lives out of line (its fp64 registers stay out of the main loop).
-// key: this voxel's best key (valid once kv; shared memory).  Returns the new
-// best index in the low 32 bits and the key-valid flag in bit 32.
-__device__ __forceinline__ long long label_exact(const snk_cell* __restrict__ dets, double px, double py, double pz,
-                                              double rho2, int i, int best, int kv, double* key, float d2f,
-                                              float lo) {
-  auto pack = [](int b, int v) { return (long long)(uint32_t)b | ((long long)v << 32); };
+// and called from one site.  Returns the new best index (the current best's key
+// is recomputed rather than cached: second balls are rare).
+__device__ __forceinline__ int label_exact(const snk_cell* __restrict__ dets, double px, double py, double pz,
+                                          double rho2, int i, int best, float d2f, float lo) {
   if (!(d2f < lo)) {
     const snk_cell d = dets[i];
-    if (!(exact_d2(px, py, pz, d) <= exact_thr(d, rho2))) return pack(best, kv);
+    if (!(exact_d2(px, py, pz, d) <= exact_thr(d, rho2))) return best;
   }
-  if (best < 0) return pack(i, 0);
-  if (!kv) {
-    const snk_cell b = dets[best];
-    *key = __ddiv_rn(exact_d2(px, py, pz, b), exact_thr(b, rho2));
-  }
+  if (best < 0) return i;
+  const snk_cell b = dets[best];
+  const double kb = __ddiv_rn(exact_d2(px, py, pz, b), exact_thr(b, rho2));
   const snk_cell d = dets[i];
   const double k = __ddiv_rn(exact_d2(px, py, pz, d), exact_thr(d, rho2));
-  if (k < *key || (k == *key && i < best)) {
-    *key = k;
-    return pack(i, 1);
-  }
-  return pack(best, 1);
+  return (k < kb || (k == kb && i < best)) ? i : best;
 }
 
 // D = 3: tile 32 x 8 x kTZ3, thread (x, y) walks the tile's kTZ3 planes; a CTA
@@ -175,7 +166,6 @@ __global__ void __launch_bounds__(kThreads) label_kernel(const snk_cell* __restr
                                                          int32_t* __restrict__ labels) {
   constexpr int NV = D == 3 ? kTZ3 : kTY2 / kTY;   // voxels per thread
   __shared__ Stage S[2];
-  __shared__ double skey[NV][kThreads];            // the exact path's best keys
   __shared__ int sbest[NV][kThreads];              // the exact path's running bests
   const int ntz = D == 3 ? G.nt[2] : 1;
   const int zgroups = D == 3 ? (ntz + kZT - 1) / kZT : 1;
@@ -214,7 +204,7 @@ __global__ void __launch_bounds__(kThreads) label_kernel(const snk_cell* __restr
     int best[NV];
 #pragma unroll
     for (int v = 0; v < NV; ++v) best[v] = -1;
-    uint32_t has = 0, kv = 0;   // planes with a best; planes whose best key is in skey
+    uint32_t has = 0;   // planes with a best
     for (int s0 = 0; s0 < cnt; s0 += kStage) {
       // lists longer than one stage (never on the throughput configs): re-stage synchronously
       const Stage* sp = &st;
@@ -283,10 +273,7 @@ __global__ void __launch_bounds__(kThreads) label_kernel(const snk_cell* __restr
             for (int u = 1; u < NV; ++u) dv = u == v ? d2f[u] : dv;
             const double py = D == 3 ? __dmul_rn((double)y0, G.sc[1]) : __dmul_rn((double)(y0 + v * kTY), G.sc[1]);
             const double pz = D == 3 ? __dmul_rn((double)(zt + v), G.sc[2]) : 0.0;
-            const long long r = label_exact(dets, px, py, pz, G.rho2, i, sbest[v][threadIdx.x], (kv >> v) & 1u,
-                                            &skey[v][threadIdx.x], dv, lo);
-            sbest[v][threadIdx.x] = (int)(uint32_t)r;
-            kv |= (uint32_t)(r >> 32) << v;
+            sbest[v][threadIdx.x] = label_exact(dets, px, py, pz, G.rho2, i, sbest[v][threadIdx.x], dv, lo);
           }
 #pragma unroll
           for (int v = 0; v < NV; ++v) {
