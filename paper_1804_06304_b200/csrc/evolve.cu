@@ -29,6 +29,7 @@
 // dE/dc = -gamma A_c, dE/dR = gamma (A_R - (d/R) A0), gamma = (2R)^-d;
 // (c, R) -= clip((eps0/sqrt(n))/2 * grad, +-max_step); R clamp, leash, domain.
 #include <cstdlib>
+#include <type_traits>
 #include <mutex>
 
 #include "common.cuh"
@@ -399,7 +400,11 @@ __device__ __forceinline__ Acc leaves(const EvoParams& P, const CellIt& C, const
 
 // Brick row length: S + 2 rounded down to even (the x origin is even, the
 // copies are 4-byte words), so a ball box of width SX - 1 always fits in x.
-__host__ __device__ constexpr int brick_sx(int S) { return (S + 2) & ~1; }
+#ifndef SNK_BRICK_ALIGN
+#define SNK_BRICK_ALIGN 2   // brick x origin alignment (elements) = the copy width / 2 bytes
+#endif
+constexpr int kBA = SNK_BRICK_ALIGN;
+__host__ __device__ constexpr int brick_sx(int S) { return (S + 2 * kBA - 2) & ~(kBA - 1); }
 
 // Gather modes
 enum { G_GLOBAL = 0, G_GLOBAL_SLAB = 1, G_BRICK_CLAMP = 2, G_BRICK_FAST = 3, G_GLOBAL_FAST = 4 };
@@ -1044,16 +1049,17 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
 template <int D, int S>
 __device__ __forceinline__ void load_brick(uint16_t* brick, const EvoParams& P, int bx, int by, int bz,
                                            int zlo_buf) {
-  constexpr int SX = brick_sx(S), WPR = SX / 2;          // u16 per row, 32-bit words per row
+  constexpr int SX = brick_sx(S), WPR = SX / kBA;        // u16 per row, copy words per row
   constexpr int ROWS = D == 3 ? S * S : S;
-  const int nw = min(WPR, (P.nx - bx + 1) / 2);     // words inside the volume (x)
+  const int nw = min(WPR, (P.nx - bx + kBA - 1) / kBA);   // words inside the volume (x)
   const int ny = min(S, P.ny - by);
   const int nzl = D == 3 ? min(S, P.z_lo + P.nz_buf - bz) : 1;
   // word (col, ry, rz) of the brick <- word col of volume row (by + ry, bz + rz);
   // offsets from the brick's first word, in 32-bit words (< 2^31: the brick spans <= S planes)
-  const uint32_t* src = reinterpret_cast<const uint32_t*>(P.img) +
-                        (((int64_t)(bz - zlo_buf) * P.ny + by) * P.nx + bx) / 2;   // bx even
-  const int rw = P.nx / 2, pw = rw * P.ny;                // words per volume row / plane
+  using Word = typename std::conditional<kBA == 4, uint2, uint32_t>::type;
+  const Word* src = reinterpret_cast<const Word*>(P.img) +
+                    (((int64_t)(bz - zlo_buf) * P.ny + by) * P.nx + bx) / kBA;   // bx % kBA == 0
+  const int rw = P.nx / kBA, pw = rw * P.ny;              // words per volume row / plane
   const uint32_t dst0 = smem_u32(brick);
   // (col, ry, rz) of word w = threadIdx.x + k * blockDim.x, stepped incrementally
   // (no division per word): the step advances by dr rows and dc columns
@@ -1063,8 +1069,8 @@ __device__ __forceinline__ void load_brick(uint16_t* brick, const EvoParams& P, 
   int rz = row / S, ry = row - rz * S;
   for (; w < ROWS * WPR; w += step) {
     if (col < nw && ry < ny && rz < nzl)
-      asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst0 + (uint32_t)w * 4u),
-                   "l"(src + (rz * pw + ry * rw + col))
+      asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(dst0 + (uint32_t)w * (2u * kBA)),
+                   "l"(src + (rz * pw + ry * rw + col)), "n"(2 * kBA)
                    : "memory");
     col += dc;
     ry += dr;
@@ -1154,7 +1160,7 @@ struct BrickCtl {
       interior &= lo[a] >= 0 && hi[a] <= n[a] - 1;
       lo[a] = max(lo[a], 0);
       hi[a] = min(hi[a], n[a] - 1);
-      fits &= hi[a] - lo[a] + 1 <= (a == 0 ? EXT[0] - 1 : S);
+      fits &= hi[a] - lo[a] + 1 <= (a == 0 ? EXT[0] - (kBA - 1) : S);
       inside &= lo[a] >= b[a] && hi[a] <= b[a] + EXT[a] - 1;
     }
     if (D == 3 && SLAB) fits &= lo[2] >= zlo && hi[2] <= zhi;
@@ -1165,9 +1171,9 @@ struct BrickCtl {
       for (int a = 0; a < D; ++a) {
         const int amin = (a == 2) ? zlo : 0, amax = (a == 2) ? zhi : n[a] - 1;
         int o = lo[a] - (EXT[a] - (hi[a] - lo[a] + 1)) / 2;
-        if (a == 0) o &= ~1;
+        if (a == 0) o &= ~(kBA - 1);
         o = min(o, amax + 1 - EXT[a]);
-        if (a == 0) o &= ~1;
+        if (a == 0) o &= ~(kBA - 1);
         o = max(o, amin);
         b[a] = o;
         const bool in_vol = o >= 0 && o + EXT[a] - 1 <= n[a] - 1;
@@ -1734,7 +1740,7 @@ int32_t evolve_impl(const snk_grid* g, const snk_params* p, const uint16_t* d_im
   // the brick kernel copies 4-byte words from an even x origin: needs even nx
   // and a 4-byte aligned image
   const bool brick_ok = variant != 1 && Bb >= 1 && Bb <= 128 && (Wb == 4 || Wb == 8) &&
-                        g->n[0] % 2 == 0 && (reinterpret_cast<uintptr_t>(d_image) & 3) == 0;
+                        g->n[0] % kBA == 0 && (reinterpret_cast<uintptr_t>(d_image) & (2 * kBA - 1)) == 0;
   if (variant == 2 && !brick_ok) return fail(SNK_CONFIG, "brick kernel unavailable for this volume");
   // small N (C5's sweep): several cells per warp (variant 3; auto for N < 128,
   // where the small-brick kernel would hold one warp per 41 KB brick: C5 at

@@ -532,8 +532,11 @@ __device__ __forceinline__ uint32_t xwin(const uint32_t* E, const uint32_t* O, i
   return m;
 }
 
+#ifndef SNK_QMINB
+#define SNK_QMINB 2
+#endif
 template <int W>
-__global__ void __launch_bounds__(kQThreads, kQThreads > 256 ? 1 : 2)
+__global__ void __launch_bounds__(kQThreads, SNK_QMINB)
     maxima_tma_kernel(const __grid_constant__ CUtensorMap map, const __grid_constant__ MaxTmaArgs A) {
   constexpr int BY = kQY + 2 * W, K = 2 * W + 1;
   constexpr uint32_t kBoxBytes = kQBX * BY * 2;
