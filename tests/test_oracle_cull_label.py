@@ -119,3 +119,23 @@ def test_label_points_and_2d(ora):
     c1 = np.array([[10, 10, 0]], np.float32)
     lab1 = ora.label((21, 21, 1), 2, c1, np.array([4.0], np.float32))
     assert lab1[0, 10, 10] == 1 and lab1[0, 10, 12] == 1 and lab1[0, 10, 13] == 0  # 2 <= 2.83 < 3
+
+
+def test_label_equal_keys_go_to_the_smaller_index(ora):
+    """O7's tie rule (reading G19): an exact duplicate detection never wins, and a
+    voxel on the bisecting plane of two equal balls (equal keys exactly) takes
+    the smaller index."""
+    n = (24, 20, 18)
+    c = np.array([[8.0, 9.0, 9.0], [8.0, 9.0, 9.0], [14.0, 9.0, 9.0]], np.float32)
+    R = np.array([6.0, 6.0, 6.0], np.float32)
+    lab = ora.label(n, 3, c, R)
+    assert not (lab == 2).any()                       # the duplicate of detection 0
+    assert (lab == 1).any() and (lab == 3).any()
+    # x = 11 is equidistant from x = 8 and x = 14: inside both inner balls -> index 0
+    plane = lab[:, :, 11]
+    inside = plane > 0
+    assert inside.any() and np.all(plane[inside] == 1)
+    # swapping the order of the two distinct balls swaps the winner on the plane
+    lab2 = ora.label(n, 3, c[[2, 1, 0]], R)
+    assert np.all(lab2[:, :, 11][lab2[:, :, 11] > 0] == 1)   # now index 0 is the ball at x = 14
+    assert lab2[9, 9, 13] == 1 and lab[9, 9, 13] == 3

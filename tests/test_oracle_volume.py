@@ -207,3 +207,28 @@ def test_ingest_u8_pins(ora):
     assert out[0] == 0 and out[255] == 65535
     assert np.array_equal(out.astype(np.int64) % 257, np.zeros(256)) and np.array_equal(out // 257, v)
     assert np.all(np.diff(out.astype(np.int64)) == 257)
+
+
+def test_resample_half_ratio_rounds_half_up(ora):
+    """O1 on C3's ratio 1/2 against the exact weights: output plane 2m + 1 samples
+    src = m + 1/4 and 2m samples m - 1/4 (S:365 centre-aligned), so the values are
+    (3 v[m] + v[m+1]) / 4 and (v[m-1] + 3 v[m]) / 4 rounded half up —
+    (x + 2) >> 2 on the integer x — with the end planes clamped.
+    Random values (odd differences) make truncation or round-half-even fail."""
+    rng = np.random.default_rng(5)
+    v = rng.integers(0, 65536, size=(9, 3, 4)).astype(np.int64)
+    out = ora.resample(v.astype(np.uint16), (1.0, 1.0, 2.0)).astype(np.int64)
+    assert out.shape == (18, 3, 4)
+    exp = np.empty_like(out)
+    n = v.shape[0]
+    for k in range(18):
+        m = k // 2
+        if k == 0:
+            exp[k] = v[0]
+        elif k == 17:
+            exp[k] = v[n - 1]
+        elif k % 2:
+            exp[k] = (3 * v[m] + v[m + 1] + 2) >> 2
+        else:
+            exp[k] = (v[m - 1] + 3 * v[m] + 2) >> 2
+    assert np.array_equal(out, exp)
