@@ -1061,21 +1061,33 @@ __device__ __forceinline__ void load_brick(uint16_t* brick, const EvoParams& P, 
                     (((int64_t)(bz - zlo_buf) * P.ny + by) * P.nx + bx) / kBA;   // bx % kBA == 0
   const int rw = P.nx / kBA, pw = rw * P.ny;              // words per volume row / plane
   const uint32_t dst0 = smem_u32(brick);
-  // (col, ry, rz) of word w = threadIdx.x + k * blockDim.x, stepped incrementally
-  // (no division per word): the step advances by dr rows and dc columns
-  const int step = blockDim.x, dr = step / WPR, dc = step - dr * WPR;
-  int w = threadIdx.x;
-  int row = w / WPR, col = w - row * WPR;
-  int rz = row / S, ry = row - rz * S;
-  for (; w < ROWS * WPR; w += step) {
-    if (col < nw && ry < ny && rz < nzl)
-      asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(dst0 + (uint32_t)w * (2u * kBA)),
-                   "l"(src + (rz * pw + ry * rw + col)), "n"(2 * kBA)
-                   : "memory");
-    col += dc;
-    ry += dr;
-    if (col >= WPR) { col -= WPR; ++ry; }
-    while (ry >= S) { ry -= S; ++rz; }
+  (void)ROWS;
+  // A thread owns the (col, ry) columns p = threadIdx.x, + blockDim.x, ... of a
+  // plane and copies each down all nzl planes: the bounds test is per column,
+  // and a copy costs the LDGSTS plus two address increments (the per-word
+  // (col, ry, rz) stepping took 29 instructions per word).
+  constexpr uint32_t kPlaneBytes = (uint32_t)(SX * (D == 3 ? S : 1)) * 2u;
+  for (int p = threadIdx.x; p < WPR * S; p += blockDim.x) {
+    const int ry = p / WPR, col = p - ry * WPR;
+    if (col >= nw || ry >= ny) continue;
+    uint32_t dst = dst0 + (uint32_t)(ry * WPR + col) * (2u * kBA);
+    const Word* s = src + (ry * rw + col);
+    int rz = 0;
+#pragma unroll 1
+    for (; rz + 4 <= nzl; rz += 4) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(dst + u * kPlaneBytes), "l"(s + u * pw),
+                     "n"(2 * kBA)
+                     : "memory");
+      dst += 4 * kPlaneBytes;
+      s += 4 * pw;
+    }
+    for (; rz < nzl; ++rz) {
+      asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(dst), "l"(s), "n"(2 * kBA) : "memory");
+      dst += kPlaneBytes;
+      s += pw;
+    }
   }
   asm volatile("cp.async.wait_all;" ::: "memory");
   __syncthreads();
@@ -1238,11 +1250,31 @@ __global__ void __launch_bounds__(32 * W, W == 4 ? SNK_BRICK_MINB4 : (W <= 2 ? 5
       if (mode == 0) {
         if constexpr ((CH == 8 || CH == 4) && SNK_F32X2) part = chunk_fast_x2<D, S, CH, EST>(P, C, dir, brick);
         else part = chunk_sum_dirs<D, G_BRICK_FAST, S, CH, EST>(P, C, dir, brick, halo);
+        if constexpr (SNK_BRICK_PIPE == 4) {
+          // PIPE 4: the next iteration's draws in the same basic block as the
+          // gathers, so the Philox rounds fill the shared-load latency
+          CellIt Cn;
+          Cn.p0 = s.q0 ^ (uint32_t)(it + 1);
+          Cn.p1 = s.q1;
+          Cn.p3 = s.q3;
+          if constexpr (est_kind(EST) == SNK_EST_RAY) draw_dirs_ray<D>(P, Cn, j0 / 8u, dir);
+          else draw_dirs<D, CH>(P, Cn, j0, dir);
+        }
       } else if (mode == 1) {
         part = chunk_sum_dirs<D, G_BRICK_CLAMP, S, CH, EST>(P, C, dir, brick, halo);
       } else {
         part = chunk_sum_dirs<D, SLAB ? G_GLOBAL_SLAB : G_GLOBAL, S, CH, EST>(P, C, dir, brick, halo);
         if (threadIdx.x == 0) atomicAdd(&g_evolve_stats[1], 1ull);
+      }
+      if constexpr (SNK_BRICK_PIPE == 4) {
+        if (mode != 0) {
+          CellIt Cn;
+          Cn.p0 = s.q0 ^ (uint32_t)(it + 1);
+          Cn.p1 = s.q1;
+          Cn.p3 = s.q3;
+          if constexpr (est_kind(EST) == SNK_EST_RAY) draw_dirs_ray<D>(P, Cn, j0 / 8u, dir);
+          else draw_dirs<D, CH>(P, Cn, j0, dir);
+        }
       }
     } else {
       if (mode == 0) {
@@ -1257,7 +1289,15 @@ __global__ void __launch_bounds__(32 * W, W == 4 ? SNK_BRICK_MINB4 : (W <= 2 ? 5
     float* xo = &xch[it & 1][0][0];
     warp_reduce_scatter(part, xo + wsub, lane, W);
     __syncthreads();   // also: every brick read of this iteration is done
-    if constexpr (PIPE && SNK_BRICK_PIPE == 3) {
+    if constexpr (PIPE && SNK_BRICK_PIPE == 4) {
+      Acc sum;
+      sum.a0 = comp_tree<W>(xo + 0 * W);
+      sum.cx = comp_tree<W>(xo + 1 * W);
+      sum.cy = comp_tree<W>(xo + 2 * W);
+      sum.cz = comp_tree<W>(xo + 3 * W);
+      sum.aR = comp_tree<W>(xo + 4 * W);
+      if (cell_update<D, false, EST, true>(P, s, C, sum, it)) break;
+    } else if constexpr (PIPE && SNK_BRICK_PIPE == 3) {
       // PIPE 2 with the next iteration's draws placed before a branch-free
       // update in one basic block, so the two independent streams interleave
       Acc sum;
