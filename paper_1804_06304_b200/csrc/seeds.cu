@@ -306,32 +306,49 @@ __global__ void __launch_bounds__(kMThreads) maxima_fused_kernel(FusedArgs A) {
   }
 }
 
-// compaction of the bitmask: words in linear order, 1024 words per block
-__global__ void __launch_bounds__(1024) bits_count_kernel(const uint32_t* bits, int64_t nwords, int* counts) {
-  const int64_t i = (int64_t)blockIdx.x * 1024 + threadIdx.x;
-  int c = i < nwords ? __popc(bits[i]) : 0;
+// compaction of the bitmask: words in linear order, 1024 words per block, 4
+// consecutive words per thread (256 threads: a quarter of the threads and
+// scan of the one-word-per-thread version; the launches were bound by block
+// scheduling, not by the 4 B per word they read)
+constexpr int kWPT = 4, kBitsThreads = 1024 / kWPT;
+
+__device__ __forceinline__ void load_words(const uint32_t* bits, int64_t nwords, int64_t i0, uint32_t w[kWPT]) {
+#pragma unroll
+  for (int k = 0; k < kWPT; ++k) w[k] = i0 + k < nwords ? bits[i0 + k] : 0u;
+}
+
+__global__ void __launch_bounds__(kBitsThreads) bits_count_kernel(const uint32_t* bits, int64_t nwords, int* counts) {
+  uint32_t w[kWPT];
+  load_words(bits, nwords, (int64_t)blockIdx.x * 1024 + threadIdx.x * kWPT, w);
+  int c = 0;
+#pragma unroll
+  for (int k = 0; k < kWPT; ++k) c += __popc(w[k]);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
-  __shared__ int ws[32];
+  __shared__ int ws[kBitsThreads / 32];
   if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = c;
   __syncthreads();
-  if (threadIdx.x < 32) {
-    int v = ws[threadIdx.x];
+  if (threadIdx.x == 0) {
+    int v = 0;
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    if (threadIdx.x == 0) counts[blockIdx.x] = v;
+    for (int k = 0; k < kBitsThreads / 32; ++k) v += ws[k];
+    counts[blockIdx.x] = v;
   }
 }
 
-__global__ void __launch_bounds__(1024) bits_write_kernel(const uint32_t* bits, int64_t nwords, int wpr,
-                                                          int nx, int ny, int own_z0,
-                                                          const int64_t* offsets, float* seeds,
-                                                          int64_t cap, int linear, double sx = 1.0,
-                                                          double sy = 1.0, double sz = 1.0) {
-  __shared__ int ws[32];
-  const int64_t i = (int64_t)blockIdx.x * 1024 + threadIdx.x;
-  const uint32_t word = i < nwords ? bits[i] : 0u;
-  const int c = __popc(word);
+__global__ void __launch_bounds__(kBitsThreads) bits_write_kernel(const uint32_t* bits, int64_t nwords, int wpr,
+                                                                  int nx, int ny, int own_z0,
+                                                                  const int64_t* offsets, float* seeds,
+                                                                  int64_t cap, int linear, double sx = 1.0,
+                                                                  double sy = 1.0, double sz = 1.0) {
+  constexpr int NWARP = kBitsThreads / 32;
+  __shared__ int ws[NWARP];
+  const int64_t i0 = (int64_t)blockIdx.x * 1024 + threadIdx.x * kWPT;
+  uint32_t w[kWPT];
+  load_words(bits, nwords, i0, w);
+  int c = 0;
+#pragma unroll
+  for (int k = 0; k < kWPT; ++k) c += __popc(w[k]);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   int x = c;
 #pragma unroll
@@ -341,46 +358,44 @@ __global__ void __launch_bounds__(1024) bits_write_kernel(const uint32_t* bits, 
   }
   if (lane == 31) ws[warp] = x;
   __syncthreads();
-  if (warp == 0) {
-    int v = ws[lane];
+  int before = 0;
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int y = __shfl_up_sync(0xffffffffu, v, o);
-      if (lane >= o) v += y;
+  for (int k = 0; k < NWARP; ++k) before += k < warp ? ws[k] : 0;
+  if (!c) return;
+  int64_t o = offsets[blockIdx.x] + before + x - c;
+  const int64_t plane = (int64_t)nx * ny;
+#pragma unroll 1
+  for (int k = 0; k < kWPT; ++k) {
+    uint32_t m = w[k];
+    if (!m) continue;
+    const int64_t i = i0 + k;
+    if (linear) {   // bit b of word i = own-region voxel 32 i + b (x fastest)
+      while (m) {
+        const int b = __ffs(m) - 1;
+        m &= m - 1;
+        const int64_t v = i * 32 + b;
+        if (o < cap) {   // physical coordinates (index x scale, G28; exact for scale 1)
+          seeds[3 * o + 0] = (float)((double)(v % nx) * sx);
+          seeds[3 * o + 1] = (float)((double)((v / nx) % ny) * sy);
+          seeds[3 * o + 2] = (float)((double)(v / plane + own_z0) * sz);
+        }
+        ++o;
+      }
+      continue;
     }
-    ws[lane] = v;
-  }
-  __syncthreads();
-  int64_t o = offsets[blockIdx.x] + (warp > 0 ? ws[warp - 1] : 0) + x - c;
-  if (!word) return;
-  uint32_t m = word;
-  if (linear) {   // bit b of word i = own-region voxel 32 i + b (x fastest)
-    const int64_t plane = (int64_t)nx * ny;
+    const int64_t row = i / wpr;                 // (z - own_z0) * ny + y
+    const int xw = (int)(i % wpr) * 32;
+    const float fy = (float)(row % ny), fz = (float)(row / ny + own_z0);
     while (m) {
       const int b = __ffs(m) - 1;
       m &= m - 1;
-      const int64_t v = i * 32 + b;
-      if (o < cap) {   // physical coordinates (index x scale, G28; exact for scale 1)
-        seeds[3 * o + 0] = (float)((double)(v % nx) * sx);
-        seeds[3 * o + 1] = (float)((double)((v / nx) % ny) * sy);
-        seeds[3 * o + 2] = (float)((double)(v / plane + own_z0) * sz);
+      if (o < cap) {
+        seeds[3 * o + 0] = (float)(xw + b);
+        seeds[3 * o + 1] = fy;
+        seeds[3 * o + 2] = fz;
       }
       ++o;
     }
-    return;
-  }
-  const int64_t row = i / wpr;                 // (z - own_z0) * ny + y
-  const int xw = (int)(i % wpr) * 32;
-  const float fy = (float)(row % ny), fz = (float)(row / ny + own_z0);
-  while (m) {
-    const int b = __ffs(m) - 1;
-    m &= m - 1;
-    if (o < cap) {
-      seeds[3 * o + 0] = (float)(xw + b);
-      seeds[3 * o + 1] = fy;
-      seeds[3 * o + 2] = fz;
-    }
-    ++o;
   }
 }
 
@@ -881,10 +896,10 @@ int32_t seeds_impl(const snk_grid* g, const snk_params* p, const uint16_t* d_smo
       }
     }
     if (!tma_pass) SNK_LAUNCH_CHECK("maxima_pred8_kernel");
-    bits_count_kernel<<<(unsigned)nbw, 1024, 0, st>>>(bits, nw, wcounts);
+    bits_count_kernel<<<(unsigned)nbw, kBitsThreads, 0, st>>>(bits, nw, wcounts);
     SNK_LAUNCH_CHECK("bits_count_kernel");
     SNK_TRY(scan_counts(wcounts, nbw, woff, st, stmp));
-    bits_write_kernel<<<(unsigned)nbw, 1024, 0, st>>>(bits, nw, 0, nx, ny, oz, woff, d_seeds, cap, 1,
+    bits_write_kernel<<<(unsigned)nbw, kBitsThreads, 0, st>>>(bits, nw, 0, nx, ny, oz, woff, d_seeds, cap, 1,
                                                       grid_scale(g, 0), grid_scale(g, 1), grid_scale(g, 2));
     SNK_LAUNCH_CHECK("bits_write_kernel");
     int64_t total = 0;
@@ -946,10 +961,10 @@ int32_t seeds_impl(const snk_grid* g, const snk_params* p, const uint16_t* d_smo
       }
     }
     SNK_LAUNCH_CHECK("maxima_fused_kernel");
-    bits_count_kernel<<<(unsigned)nbw, 1024, 0, st>>>(bits, nw, wcounts);
+    bits_count_kernel<<<(unsigned)nbw, kBitsThreads, 0, st>>>(bits, nw, wcounts);
     SNK_LAUNCH_CHECK("bits_count_kernel");
     SNK_TRY(scan_counts(wcounts, nbw, woff, st, stmp));
-    bits_write_kernel<<<(unsigned)nbw, 1024, 0, st>>>(bits, nw, F.wpr, nx, ny, F.own_z0, woff, d_seeds, cap, 0);
+    bits_write_kernel<<<(unsigned)nbw, kBitsThreads, 0, st>>>(bits, nw, F.wpr, nx, ny, F.own_z0, woff, d_seeds, cap, 0);
     SNK_LAUNCH_CHECK("bits_write_kernel");
     int64_t total = 0;
     SNK_TRY(read_back(woff + nbw, &total, sizeof(int64_t), st));
