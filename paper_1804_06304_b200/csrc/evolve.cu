@@ -987,8 +987,11 @@ __global__ void __launch_bounds__(W >= 4 ? 32 * W : 128)
 // occupancy / per-contour overhead the paper measured) are amortised over
 // several cells.  No shared memory and no barriers; gathers through L1/L2,
 // unclamped when every cell of the warp has its ball inside the volume.
+#ifndef SNK_GROUP_MINB
+#define SNK_GROUP_MINB 4
+#endif
 template <int D, int G, bool SLAB, int CH, int L>
-__global__ void __launch_bounds__(128, 4) evolve_group_kernel(const __grid_constant__ EvoParams P) {
+__global__ void __launch_bounds__(128, SNK_GROUP_MINB) evolve_group_kernel(const __grid_constant__ EvoParams P) {
   constexpr int CPW = 32 / G;                // cells per warp
   constexpr int B = CH << L;                 // samples per lane per iteration
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -1203,8 +1206,12 @@ struct BrickCtl {
   }
 };
 
+// 2D: an 8.4 KB brick, so registers alone set the occupancy
+#ifndef SNK_BRICK_MINB2D
+#define SNK_BRICK_MINB2D 3
+#endif
 template <int D, int W, int S, bool SLAB, int CH, int L, int EST = 0>
-__global__ void __launch_bounds__(32 * W, W == 4 ? SNK_BRICK_MINB4 : (W <= 2 ? 5 : SNK_BRICK_MINB8)) evolve_brick_kernel(const __grid_constant__ EvoParams P) {
+__global__ void __launch_bounds__(32 * W, D == 2 && W == 4 ? SNK_BRICK_MINB2D : (W == 4 ? SNK_BRICK_MINB4 : (W <= 2 ? 5 : SNK_BRICK_MINB8))) evolve_brick_kernel(const __grid_constant__ EvoParams P) {
   constexpr int B = CH << L;
   constexpr bool PIPE = SNK_BRICK_PIPE && L == 0;
   static_assert(EST == 0 || (PIPE && CH == 8), "CV / RAY estimators: 8 samples per thread, pipelined draws");
