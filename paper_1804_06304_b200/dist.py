@@ -297,6 +297,8 @@ def bench_rank(args, cfg):
         if os.environ.get("NCCL_DEBUG", "").upper() in ("", "VERSION", "WARN"):
             os.environ["NCCL_DEBUG"] = "INFO"
             os.environ["NCCL_DEBUG_SUBSYS"] = "INIT"
+        # NCCL logs to stdout by default: keep stdout for the one JSON line
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
         tdist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     else:
         tdist.init_process_group(backend)

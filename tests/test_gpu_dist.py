@@ -3,6 +3,7 @@ sizes 2 and 3 as processes sharing one GPU (gloo, host-staged exchanges — the
 round's GPU box has one device; NCCL runs the same code on 8).  Seeds, cells,
 detections and the label map must be bit-identical to the single-GPU pipeline
 (DESIGN.md §7)."""
+import json
 import os
 import socket
 
@@ -177,7 +178,7 @@ def _bench(args, env=None):
                        env=e, timeout=900, cwd=root)
     assert r.returncode == 0, r.stderr[-3000:]
     line = [ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1]
-    return json.loads(line), r.stdout + r.stderr
+    return json.loads(line), r.stdout, r.stderr
 
 
 def test_bench_launches_ranks_itself(gpu):
@@ -186,12 +187,15 @@ def test_bench_launches_ranks_itself(gpu):
     same cells and detections as one GPU; `--dist` runs the driver's NCCL branch
     at N = 1."""
     common = ["--config", "C1", "--steps", "1", "--warmup", "3", "--no-cpu-baseline"]
-    one, _ = _bench(common + ["--no-e2e"])
-    two, _ = _bench(["--gpus", "2"] + common, {"SNK_DIST_BACKEND": "gloo"})
+    one, _, _ = _bench(common + ["--no-e2e"])
+    two, _, _ = _bench(["--gpus", "2"] + common, {"SNK_DIST_BACKEND": "gloo"})
     assert two["n_gpus"] == 2 and one["n_gpus"] == 1
     assert two["cells"] == one["cells"]
     assert two["detections"] == one["detections"]
-    nc, err = _bench(["--dist"] + common)
+    nc, out, err = _bench(["--dist"] + common)
     assert nc["n_gpus"] == 1 and nc["backend"] == "nccl"
     assert nc["detections"] == one["detections"]
+    # NCCL's communicator lines are kept, on stderr: stdout is the one JSON line
     assert "NCCL INFO" in err
+    lines = [ln for ln in out.splitlines() if ln.strip()]
+    assert len(lines) == 1 and json.loads(lines[0]) == nc, out[-2000:]
