@@ -88,6 +88,12 @@ struct Acc {
 // EST template values: the estimator in bits 0-1 (SNK_EST_MC, _MC_CV, _RAY) and
 // bit 2 = anisotropic grid sampled in physical coordinates (G28)
 constexpr int kAniso = 4;
+// bit 3: no axis of the domain is shorter than a ball (P.dom_small == 0), so the
+// update's domain clamp needs no small-axis selects (a launch-time choice)
+constexpr int kBig = 8;
+#ifndef SNK_BIG
+#define SNK_BIG 1
+#endif
 __host__ __device__ constexpr int est_kind(int e) { return e & 3; }
 __host__ __device__ constexpr bool est_aniso(int e) { return (e & kAniso) != 0; }
 
@@ -863,7 +869,7 @@ __device__ __forceinline__ bool cell_update(const EvoParams& P, CellState& s, co
   float dx, dy, dz = lz;
   if (NB) {
     const float m2 = __fmul_rn(2.0f, m);
-    const bool small = P.dom_small != 0;
+    const bool small = !(EST & kBig) && P.dom_small != 0;
     dx = (small && P.dom1[0] < m2) ? __fsub_rn(__fmul_rn(0.5f, P.dom1[0]), s.sx)
                                    : clampf(lx, __fsub_rn(m, s.sx), __fsub_rn(__fsub_rn(P.dom1[0], m), s.sx));
     dy = (small && P.dom1[1] < m2) ? __fsub_rn(__fmul_rn(0.5f, P.dom1[1]), s.sy)
@@ -1585,7 +1591,9 @@ int32_t brick_B(const EvoParams& P, int B, cudaStream_t st) {
     case 1: return launch_brick<D, W, S, SLAB, 1, 0>(P, st);
     case 2: return launch_brick<D, W, S, SLAB, 2, 0>(P, st);
     case 4: return launch_brick<D, W, S, SLAB, 4, 0>(P, st);
-    case 8: return launch_brick<D, W, S, SLAB, (C8 < 8 ? C8 : 8), (C8 < 8 ? 1 : 0)>(P, st);
+    case 8:
+      if (SNK_BIG && C8 == 8 && !P.dom_small && SNK_BRICK_PIPE == 3) return launch_brick<D, W, S, SLAB, 8, 0, kBig>(P, st);
+      return launch_brick<D, W, S, SLAB, (C8 < 8 ? C8 : 8), (C8 < 8 ? 1 : 0)>(P, st);
     case 16: return launch_brick<D, W, S, SLAB, C8, (C8 < 8 ? 2 : 1)>(P, st);
     case 32: return launch_brick<D, W, S, SLAB, C8, (C8 < 8 ? 3 : 2)>(P, st);
     case 64: return launch_brick<D, W, S, SLAB, C8, (C8 < 8 ? 4 : 3)>(P, st);

@@ -357,14 +357,44 @@ def bench_rank(args, cfg):
     # and its labels + the detections out, wall clock, max over ranks
     h_labels = torch.empty(tuple(be.labels.shape), dtype=torch.int32, pin_memory=True)
     h_dets = torch.empty(be.dets.numel(), dtype=torch.uint8, pin_memory=True)
+    # double-buffered: step k+1's planes go up and step k's labels / detections
+    # come down on two copy streams while the next step computes (each step's
+    # outputs are first snapshotted on the compute stream, device to device)
+    comp, cs, cd = torch.cuda.current_stream(), torch.cuda.Stream(), torch.cuda.Stream()   # compute, up, down
+    owns = [own, torch.empty_like(own)]
+    labs = [torch.empty_like(be.labels) for _ in range(2)]
+    dsnap = [torch.empty_like(be.dets) for _ in range(2)]
+    up = [torch.cuda.Event() for _ in range(2)]
+    done = [torch.cuda.Event() for _ in range(2)]
+    down = [torch.cuda.Event() for _ in range(2)]
     tdist.barrier()
     t0 = time.perf_counter()
-    for _ in range(args.steps):
-        own.copy_(h_raw, non_blocking=True)
-        r = run.step(own)
-        h_labels.copy_(r["labels"], non_blocking=True)
-        h_dets[:r["n_dets"] * CELL_BYTES].copy_(r["dets"][:r["n_dets"] * CELL_BYTES], non_blocking=True)
-        torch.cuda.synchronize()
+    with torch.cuda.stream(cs):
+        owns[0].copy_(h_raw, non_blocking=True)
+        up[0].record(cs)
+    for k in range(args.steps):
+        b = k & 1
+        if k + 1 < args.steps:   # step k+1's upload runs under step k (the driver syncs the host inside a step)
+            with torch.cuda.stream(cs):
+                if k >= 1:
+                    cs.wait_event(done[b ^ 1])   # step k-1 has finished reading owns[b ^ 1]
+                owns[b ^ 1].copy_(h_raw, non_blocking=True)
+                up[b ^ 1].record(cs)
+        comp.wait_event(up[b])
+        r = run.step(owns[b])
+        nb = r["n_dets"] * CELL_BYTES
+        if k >= 2:
+            comp.wait_event(down[b])   # step k-2's downloads are done with labs[b] / dsnap[b]
+        labs[b].copy_(r["labels"])
+        dsnap[b][:nb].copy_(r["dets"][:nb])
+        done[b].record(comp)
+        with torch.cuda.stream(cd):
+            cd.wait_event(done[b])
+            h_labels.copy_(labs[b], non_blocking=True)
+            h_dets[:nb].copy_(dsnap[b][:nb], non_blocking=True)
+            down[b].record(cd)
+    torch.cuda.synchronize()
+    del owns, labs, dsnap
     wall = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=red_dev)
     tdist.all_reduce(wall, op=tdist.ReduceOp.MAX)
     e2e_s = float(wall.item())

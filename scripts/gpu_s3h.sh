@@ -1,0 +1,6 @@
+#!/bin/bash
+# overlapped e2e loop of the slab driver: dist tests, C4 --dist at N = 1, 2 gloo ranks on C3-sized C1? (C1)
+cd "$GRAFT_REPO_ROOT"; O=gpurun_out; mkdir -p $O; TAG=${TAG:-s3h}
+timeout 1200 python -m pytest tests/test_gpu_dist.py -m gpu -x -q > $O/${TAG}_tests.txt 2>&1; tail -2 $O/${TAG}_tests.txt
+timeout 600 python bench.py --config C4 --dist --no-cpu-baseline --steps 5 > $O/${TAG}_C4_dist1.json 2> $O/${TAG}_C4_dist1.err
+python -c "import json; d=json.loads(open('$O/${TAG}_C4_dist1.json').read().splitlines()[-1]); print('C4 dist1', d['ms_per_step'], d['value']/1e9, d['roofline']['frac'], d['detections'], 'e2e', d['e2e']['value']/1e9)"
