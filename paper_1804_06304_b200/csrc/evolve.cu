@@ -1059,7 +1059,6 @@ template <int D, int S>
 __device__ __forceinline__ void load_brick(uint16_t* brick, const EvoParams& P, int bx, int by, int bz,
                                            int zlo_buf) {
   constexpr int SX = brick_sx(S), WPR = SX / kBA;        // u16 per row, copy words per row
-  constexpr int ROWS = D == 3 ? S * S : S;
   const int nw = min(WPR, (P.nx - bx + kBA - 1) / kBA);   // words inside the volume (x)
   const int ny = min(S, P.ny - by);
   const int nzl = D == 3 ? min(S, P.z_lo + P.nz_buf - bz) : 1;
@@ -1070,7 +1069,6 @@ __device__ __forceinline__ void load_brick(uint16_t* brick, const EvoParams& P, 
                     (((int64_t)(bz - zlo_buf) * P.ny + by) * P.nx + bx) / kBA;   // bx % kBA == 0
   const int rw = P.nx / kBA, pw = rw * P.ny;              // words per volume row / plane
   const uint32_t dst0 = smem_u32(brick);
-  (void)ROWS;
   // A thread owns the (col, ry) columns p = threadIdx.x, + blockDim.x, ... of a
   // plane and copies each down all nzl planes: the bounds test is per column,
   // and a copy costs the LDGSTS plus two address increments (the per-word
