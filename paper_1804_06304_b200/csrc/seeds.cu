@@ -434,18 +434,21 @@ __device__ __forceinline__ bool tie_free_warp(const MaxArgs& A, int x, int y, in
 }
 
 template <int D, int W>
+// Grid (x groups / 256, y, owned planes): the (x group, y, z) of a thread come
+// from the block indices (the 64-bit divisions of a flat index cost ~1/3 of
+// the kernel's instructions).
 __global__ void __launch_bounds__(256) maxima_pred8_kernel(MaxArgs A, const uint16_t* __restrict__ XY,
                                                            uint8_t* __restrict__ mask, int64_t ngroups,
                                                            int own_z0) {
-  const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const bool valid = t0 < ngroups;          // every lane stays for the warp-wide tie checks
-  const int64_t t = valid ? t0 : ngroups - 1;
+  (void)ngroups;
   const int lane = threadIdx.x & 31;
   const int nc = A.nx >> 3;
-  const int xc = (int)(t % nc);
-  const int64_t row = t / nc;
-  const int y = (int)(row % A.ny);
-  const int zo = (int)(row / A.ny) + own_z0;   // global plane
+  const int xc0 = blockIdx.x * blockDim.x + threadIdx.x;
+  const bool valid = xc0 < nc;              // every lane stays for the warp-wide tie checks
+  const int xc = valid ? xc0 : nc - 1;
+  const int y = blockIdx.y;
+  const int zo = (int)blockIdx.z + own_z0;   // global plane
+  const int64_t t = ((int64_t)blockIdx.z * A.ny + y) * nc + xc;   // the group's index in the owned region
   const int64_t idx = ((int64_t)(zo - A.z_lo) * A.ny + y) * nc + xc;
   const uint4 bq = __ldg(reinterpret_cast<const uint4*>(A.B) + idx);
   uint32_t b[8], m[8];
@@ -869,7 +872,7 @@ int32_t seeds_impl(const snk_grid* g, const snk_params* p, const uint16_t* d_smo
     A.v0 = A.v1 = 0;
     const int64_t ng = nown / 8;
     uint8_t* mask = reinterpret_cast<uint8_t*>(bits);
-    const unsigned grid = (unsigned)ceil_div(ng, 256);
+    const dim3 grid((unsigned)ceil_div(nx / 8, 256), (unsigned)ny, (unsigned)(g->own_z1 - g->own_z0));
     const int oz = (int)g->own_z0;
     if (tma_pass) {
       MaxTmaArgs T;
