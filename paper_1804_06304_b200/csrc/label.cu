@@ -180,6 +180,10 @@ __global__ void __launch_bounds__(kThreads) label_kernel(const snk_cell* __restr
   const float pyf0 = __fmul_rn((float)y0, G.scf[1]);
   const int64_t plane = (int64_t)G.ny * G.nx;
   const int64_t vstep = D == 3 ? plane : (int64_t)kTY * G.nx;   // between a thread's voxels
+  // the store stride in bytes, held in a register: left to itself the compiler
+  // re-derives ny * nx for every plane's address (IMAD.WIDE + LEA + LEA.HI.X)
+  int64_t vstep_b = vstep * (int64_t)sizeof(int32_t);
+  asm("" : "+l"(vstep_b));
   auto tile_id = [&](int tz) { return ((int64_t)tz * G.nt[1] + ty) * G.nt[0] + tx; };
   Prefetch f;
   prefetch_tile(f, dets, G, offsets, entries, tile_id(tz0));
@@ -285,13 +289,13 @@ __global__ void __launch_bounds__(kThreads) label_kernel(const snk_cell* __restr
     }
     if (cnt > kStage) __syncthreads();   // the re-staged buffer is the next tile's stage
     if (x < G.nx) {
-      int32_t* dst = labels + ((int64_t)(zt - G.z0) * G.ny + y0) * G.nx + x;
+      char* dst = reinterpret_cast<char*>(labels + ((int64_t)(zt - G.z0) * G.ny + y0) * G.nx + x);
       const int nv = D == 3 ? min(NV, G.z1 - zt) : min(NV, (G.ny - y0 + kTY - 1) / kTY);
       if (D == 3 && y0 >= G.ny) continue;
 #pragma unroll
       for (int v = 0; v < NV; ++v) {
-        if (v < nv) *dst = best[v] + 1;
-        dst += vstep;
+        if (v < nv) *reinterpret_cast<int32_t*>(dst) = best[v] + 1;
+        dst += vstep_b;
       }
     }
   }
