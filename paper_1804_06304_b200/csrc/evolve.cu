@@ -1509,8 +1509,14 @@ int32_t group_G(const EvoParams& P, int G, int B, cudaStream_t st) {
 // overrides, tuning only; B = 16 measured 15-40% slower on C5); 0 when the
 // group kernel does not apply
 int group_lanes(int n_samples) {
+  // default: as many lanes per cell as allowed (G <= 16, B >= 4 samples per
+  // lane) — small N leaves few warps in flight (C5_0 at N = 64: 4 warps per SM
+  // with B = 8), so parallelism beats the longer butterfly: B = 4 measured
+  // C5_0 1.88 -> 1.36 ms, C5_3 9.56 -> 8.35 ms at N = 64
   const char* e = getenv("SNK_GROUP_B");
-  const int B = e ? atoi(e) : 8;
+  int B = 4;
+  while (n_samples / B > 16) B *= 2;
+  if (e) B = atoi(e);
   if (B < 4 || B > 32 || (B & (B - 1))) return 0;
   const int G = n_samples / B;
   return (G >= 4 && G <= 16 && G * B == n_samples) ? G : 0;
