@@ -1819,7 +1819,10 @@ int32_t evolve_impl(const snk_grid* g, const snk_params* p, const uint16_t* d_im
                         p->n_samples < 1024 && p->r0 <= 9.5 && g->n[0] % 2 == 0 &&
                         (reinterpret_cast<uintptr_t>(d_image) & 3) == 0;
   if (small_ok) {
-    const int Ws = p->n_samples >= 512 ? 2 : 1;
+    // 2 warps per cell from N = 256 (C5 at N = 256: 1.95 -> 1.74 ms / 14.9 -> 13.7
+    // ms against 1 warp with 8 samples per lane; at N = 128 one warp is faster)
+    int Ws = p->n_samples >= 256 ? 2 : 1;
+    if (const char* e = getenv("SNK_SMALL_W")) Ws = atoi(e) == 2 ? 2 : 1;   // tuning experiments
     const int Bs = p->n_samples / (32 * Ws);
     if (Ws == 2) return slab ? brick_small_B<2, true>(P, Bs, st) : brick_small_B<2, false>(P, Bs, st);
     return slab ? brick_small_B<1, true>(P, Bs, st) : brick_small_B<1, false>(P, Bs, st);
