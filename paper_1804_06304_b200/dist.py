@@ -134,12 +134,13 @@ def allgather_counts(count: int, device, group=None) -> list:
     return [int(o.item()) for o in outs]
 
 
-def allgather_records(rec: torch.Tensor, count: int, device, group=None, rec_bytes: int = CELL_BYTES):
-    """N3: concatenate every rank's `count` records (uint8, rec_bytes each) in rank order."""
+def allgather_records(rec: torch.Tensor, count: int, device, group=None, rec_bytes: int = CELL_BYTES, meta=None):
+    """N3: concatenate every rank's `count` records (uint8, rec_bytes each) in rank order.
+    meta: an optional host-side (gloo) group for the counts."""
     if _staged(group) and torch.device(device).type == "cuda":
         allrec, tot, counts = allgather_records(rec[:count * rec_bytes].cpu(), count, "cpu", group, rec_bytes)
         return allrec.to(device), tot, counts
-    counts = allgather_counts(count, device, group)
+    counts = allgather_counts(count, device, group if meta is None else meta)
     m = max(max(counts), 1)
     pad = torch.zeros(m * rec_bytes, dtype=torch.uint8, device=device)
     if count:
@@ -167,9 +168,12 @@ class SlabRun:
     the N6 exchange at every checkpoint (T = max_iters)."""
 
     def __init__(self, plan: SlabPlan, backend, device, group=None, cull_every: int = 0,
-                 max_iters: int = 0):
+                 max_iters: int = 0, meta_group=None):
         self.plan, self.be, self.device, self.group = plan, backend, device, group
         self.cull_every, self.T = cull_every, max_iters
+        # meta_group (gloo): the per-rank counts travel host to host, so reading
+        # them never waits behind a bulk device-to-host copy on the copy engine
+        self.meta = meta_group
 
     def step(self, own_raw: torch.Tensor, ev=None) -> dict:
         """ev: optional pair of CUDA events recorded around a5/a6 (bench)."""
@@ -177,7 +181,7 @@ class SlabRun:
         local = exchange_halo(pl, own_raw, self.group)                 # N1
         smooth = self.be.preprocess(pl, local)                          # a2/a3
         seeds, ns = self.be.seeds(pl, smooth)                           # a4
-        counts = allgather_counts(ns, self.device, self.group)          # N2
+        counts = allgather_counts(ns, self.device, self.group if self.meta is None else self.meta)   # N2
         id_base = sum(counts[:pl.rank])
         if ev is not None:
             ev[0].record()
@@ -192,7 +196,7 @@ class SlabRun:
                 cell_iters += live * (b - a + 1)
                 if i + 1 < len(segs):                                           # checkpoint
                     cand, nc = self.be.compact(cells, live)
-                    allc, ntot, _ = allgather_records(cand, nc, self.device, self.group)   # N6
+                    allc, ntot, _ = allgather_records(cand, nc, self.device, self.group, meta=self.meta)   # N6
                     surv, nsurv = self.be.cull(pl, allc, ntot)
                     cells, live = self.be.select_ids(surv, nsurv, id_base, id_base + ns)
         else:
@@ -200,7 +204,7 @@ class SlabRun:
         if ev is not None:
             ev[1].record()
         cand, nc = self.be.compact(cells, live)                         # a7: E0
-        allc, ntot, _ = allgather_records(cand, nc, self.device, self.group)   # N3
+        allc, ntot, _ = allgather_records(cand, nc, self.device, self.group, meta=self.meta)   # N3
         dets, nd = self.be.cull(pl, allc, ntot)                         # a7: overlap
         labels = self.be.label(pl, dets, nd)                            # a8
         return {"n_seeds": ns, "n_live": live, "id_base": id_base, "n_total": sum(counts), "cells": cells,
@@ -314,8 +318,11 @@ def bench_rank(args, cfg):
     synth.generate_into_ptr(cfg, h_raw.data_ptr(), z0, z1)
     own = torch.empty(h_raw.shape, dtype=torch.uint16, device="cuda")
     own.copy_(h_raw)
+    # the seed / candidate counts go host to host over gloo (a D2H read of an
+    # NCCL-gathered count would queue behind the end-to-end loop's bulk copies)
+    meta = tdist.new_group(backend="gloo") if backend == "nccl" else None
     run = SlabRun(plan, be, torch.device("cuda", local_rank), cull_every=p.cull_every,
-                  max_iters=p.max_iters)
+                  max_iters=p.max_iters, meta_group=meta)
     for _ in range(args.warmup):
         r = run.step(own)
     torch.cuda.synchronize()
