@@ -512,15 +512,26 @@ __device__ __forceinline__ float2 lerp2(float2 a, float2 b, float2 f) {
   return __ffma2_rn(f, __fadd2_rn(b, neg2(a)), a);
 }
 
-// split_axis<false> for two coordinates: r = k + 2^23 rounded down, fraction k - (r - 2^23)
-__device__ __forceinline__ float2 split2(float2 k, uint32_t* r0, uint32_t* r1) {
-  const float2 r = __fadd2_rd(k, bc2(kMagic));
+// split_axis<CLAMP> for two coordinates: r = k + 2^23 rounded down, fraction
+// k - (r - 2^23); CLAMP: k clamped to [0, n - 1] and r to 2^23 + (n - 2) first
+// (per component, the scalar split_axis<true> operations)
+template <bool CLAMP = false>
+__device__ __forceinline__ float2 split2(float2 k, uint32_t* r0, uint32_t* r1, float n1 = 0.0f, float m2 = 0.0f) {
+  if (CLAMP) {
+    k.x = fminf(fmaxf(k.x, 0.0f), n1);
+    k.y = fminf(fmaxf(k.y, 0.0f), n1);
+  }
+  float2 r = __fadd2_rd(k, bc2(kMagic));
+  if (CLAMP) {
+    r.x = fminf(r.x, m2);
+    r.y = fminf(r.y, m2);
+  }
   *r0 = __float_as_uint(r.x);
   *r1 = __float_as_uint(r.y);
   return __fadd2_rn(k, neg2(__fadd2_rn(r, bc2(-kMagic))));
 }
 
-template <int D, int S, int EST = 0>
+template <int D, int S, int EST = 0, bool CLAMP = false>
 __device__ __forceinline__ Acc2 sample_pair_fast(const EvoParams& P, const CellIt& C, const Draw& d0,
                                                  const Draw& d1, const uint16_t* brick, int salt = 0) {
   constexpr int SX = brick_sx(S), SP = SX * S;
@@ -535,10 +546,10 @@ __device__ __forceinline__ Acc2 sample_pair_fast(const EvoParams& P, const CellI
     ky = __fmul2_rn(ky, bc2(P.isc[1]));
     kz = __fmul2_rn(kz, bc2(P.isc[2]));
   }
-  const float2 fx = split2(kx, &rx0, &rx1);
-  const float2 fy = split2(ky, &ry0, &ry1);
+  const float2 fx = split2<CLAMP>(kx, &rx0, &rx1, P.fnx1, P.mx2);
+  const float2 fy = split2<CLAMP>(ky, &ry0, &ry1, P.fny1, P.my2);
   float2 fz = bc2(0.0f);
-  if (D == 3) fz = split2(kz, &rz0, &rz1);
+  if (D == 3) fz = split2<CLAMP>(kz, &rz0, &rz1, P.fnz1, P.mz2);
   uint32_t li0 = ry0 * SX + rx0, li1 = ry1 * SX + rx1;
   if (D == 3) { li0 += rz0 * SP; li1 += rz1 * SP; }
   li0 -= C.boff;
@@ -593,14 +604,14 @@ __device__ __forceinline__ Acc2 tree_sum2(const Acc2* l) {
   else return acc2_add(tree_sum2<N / 2>(l), tree_sum2<N / 2>(l + N / 2));
 }
 
-template <int D, int S, int CH, int EST = 0>
+template <int D, int S, int CH, int EST = 0, bool CLAMP = false>
 __device__ __forceinline__ Acc chunk_fast_x2(const EvoParams& P, const CellIt& C, const Dir* d,
                                              const uint16_t* brick) {
   constexpr int H = CH / 2;
   Acc2 l[H];
 #pragma unroll
   for (int k = 0; k < H; ++k)
-    l[k] = sample_pair_fast<D, S, EST>(P, C, finish_draw<D, EST>(C, d[k]), finish_draw<D, EST>(C, d[k + H]),
+    l[k] = sample_pair_fast<D, S, EST, CLAMP>(P, C, finish_draw<D, EST>(C, d[k]), finish_draw<D, EST>(C, d[k + H]),
                                        brick, k);
   const Acc2 h = tree_sum2<H>(l);
   return Acc{__fadd_rn(h.a0.x, h.a0.y), __fadd_rn(h.cx.x, h.cx.y), __fadd_rn(h.cy.x, h.cy.y),
@@ -1273,7 +1284,9 @@ __global__ void __launch_bounds__(32 * W, D == 2 && W == 4 ? SNK_BRICK_MINB2D : 
           else draw_dirs<D, CH>(P, Cn, j0, dir);
         }
       } else if (mode == 1) {
-        part = chunk_sum_dirs<D, G_BRICK_CLAMP, S, CH, EST>(P, C, dir, brick, halo);
+        // a ball touching a face: the same f32x2 path with clamped coordinates
+        if constexpr ((CH == 8 || CH == 4) && SNK_F32X2) part = chunk_fast_x2<D, S, CH, EST, true>(P, C, dir, brick);
+        else part = chunk_sum_dirs<D, G_BRICK_CLAMP, S, CH, EST>(P, C, dir, brick, halo);
       } else {
         part = chunk_sum_dirs<D, SLAB ? G_GLOBAL_SLAB : G_GLOBAL, S, CH, EST>(P, C, dir, brick, halo);
         if (threadIdx.x == 0) atomicAdd(&g_evolve_stats[1], 1ull);
